@@ -1,0 +1,131 @@
+/*
+ * sfdb200 — B200 (sm_100a) backend for the damped acoustic stencil hot path
+ * of stencilfd (/root/reference/proj), exported as a plain C ABI.
+ *
+ * The reference executes each operator as ONE call of a JIT-compiled C kernel
+ * through the uniform trampoline `int <Name>_call(void **argv)`
+ * (proj/src/codegen.cpp:598-607, resolved by dlsym in proj/src/runtime.cpp:246-248,
+ * stored as `int (*call)(void**)` in runtime::CompiledKernel, runtime.hpp:65-71).
+ * Its problem constants (extents, halo, nt, dt, h, FD taps) are baked into the
+ * generated source; here they travel in an sfdb200_desc instead, and
+ * sfdb200_call(desc, argv) is the drop-in for `<Name>_call(argv)` with the SAME
+ * argv layout (codegen::signature, proj/src/codegen.cpp:247-265):
+ *
+ *   Forward  (seismic.cpp:241-267): u, m, damp, src_idx, src_w, src_data, rec_idx, rec_w, rec_data
+ *   Adjoint  (seismic.cpp:269-296): v, m, damp, src_idx, src_w, src_data, rec_idx, rec_w, rec_data
+ *   Gradient (seismic.cpp:298-331): v, u, m, damp, grad, rec_idx, rec_w, rec_data
+ *   (+ optional trailing block-size `long*` args, accepted and ignored)
+ *
+ * Grids are host `double*` in the reference's padded row-major layout, sparse
+ * indices `long*` [npoints][ndim], weights `double*` [npoints][2^ndim], traces
+ * `double*` [nt][npoints].  Results are written in place like the reference
+ * kernel (u/v slots, sampled traces, grad).  Return 0 on success; non-zero is
+ * an error code with a thread-local message (sfdb200_last_error), which the
+ * reference's runtime::run turns into RuntimeError (runtime.cpp:344-345).
+ *
+ * Semantics follow the generated kernel, including first-touch zeroing of the
+ * written grids (codegen.cpp:464-492) and, for Gradient, the host-side row-2
+ * term of seismic::gradient (seismic.cpp:468-490) so that `grad` is final.
+ * Arithmetic is fp32 on the device (see DESIGN.md for the error budget).
+ */
+#ifndef SFDB200_H
+#define SFDB200_H
+
+#if defined(__GNUC__)
+#define SFDB200_API __attribute__((visibility("default")))
+#else
+#define SFDB200_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum sfdb200_kind { SFDB200_FORWARD = 0, SFDB200_ADJOINT = 1, SFDB200_GRADIENT = 2 };
+
+enum sfdb200_status {
+    SFDB200_OK = 0,
+    SFDB200_EINVAL = 1,   /* bad descriptor / argument (reference: std::invalid_argument) */
+    SFDB200_ECUDA = 2,    /* CUDA runtime or driver failure */
+    SFDB200_ENOMEM = 3,   /* device allocation failed */
+    SFDB200_ENONFINITE = 4 /* non-finite output (reference: check_finite, seismic.cpp:39-44) */
+};
+
+/* What the reference bakes into the generated source (lowering.hpp:61-87). */
+typedef struct sfdb200_desc {
+    int kind;            /* sfdb200_kind */
+    int ndim;            /* 2 or 3; d0 = z (slowest) */
+    long padded[3];      /* padded extents n + 2*(nbpml + so/2) (seismic.hpp:29-31) */
+    int space_order;     /* even, 2..16 */
+    long nt;             /* trace samples; written slots [2, nt) (lowering.hpp:78-80) */
+    double dt, h;
+    long nsrc, nrec;     /* sparse-set sizes (Gradient: nsrc ignored) */
+    int save;            /* Forward only: u holds nt+1 history rows (seismic.hpp:91-93) */
+    int device;          /* CUDA device ordinal */
+} sfdb200_desc;
+
+typedef struct sfdb200_plan sfdb200_plan;
+
+/* ---- reference-ABI entry points ---------------------------------------- */
+
+/* Drop-in for `<Name>_call(void **argv)`: plans are cached per descriptor. */
+SFDB200_API int sfdb200_call(const sfdb200_desc* desc, void** argv);
+
+/* Explicit plan lifecycle (device buffers, streams, tensor maps). */
+SFDB200_API int sfdb200_plan_create(const sfdb200_desc* desc, sfdb200_plan** out);
+SFDB200_API int sfdb200_plan_destroy(sfdb200_plan* plan);
+/* upload + execute + download, argv as above. */
+SFDB200_API int sfdb200_run(sfdb200_plan* plan, void** argv);
+
+/* ---- staged execution (device-resident timing) -------------------------- */
+
+/* H2D + fp64->fp32 conversion of every input in argv (model, sparse sets,
+ * traces; Gradient: the u history). */
+SFDB200_API int sfdb200_upload(sfdb200_plan* plan, void** argv);
+/* The whole device-resident time loop on the plan's stream; no host sync. */
+SFDB200_API int sfdb200_execute(sfdb200_plan* plan);
+/* D2H + fp32->fp64 of every output into argv; synchronises the stream. */
+SFDB200_API int sfdb200_download(sfdb200_plan* plan, void** argv);
+/* Gradient plans: take the u history from a saved Forward plan's device
+ * buffer (same problem) instead of uploading a host copy. */
+SFDB200_API int sfdb200_bind_history(sfdb200_plan* gradient_plan, const sfdb200_plan* forward_plan);
+/* Launch on a caller stream (a cudaStream_t passed as void*); 0 = plan's own. */
+SFDB200_API int sfdb200_set_stream(sfdb200_plan* plan, void* cuda_stream);
+/* When on, execute() brackets every stencil launch with CUDA events. */
+SFDB200_API int sfdb200_set_timing(sfdb200_plan* plan, int on);
+/* Stencil-kernel time of the last timed execute(): total ms and launches. */
+SFDB200_API int sfdb200_stencil_time(sfdb200_plan* plan, double* total_ms, long* launches);
+/* Kernels launched by one execute() (stencil + sparse + bookkeeping). */
+SFDB200_API long sfdb200_launches_per_execute(const sfdb200_plan* plan);
+/* Updated points per step ((n + 2 nbpml)^ndim, lowering.cpp:111-121) and steps (nt-2). */
+SFDB200_API long sfdb200_points_per_step(const sfdb200_plan* plan);
+SFDB200_API long sfdb200_steps(const sfdb200_plan* plan);
+/* Host<->device bytes moved by upload()/download() for this plan. */
+SFDB200_API long sfdb200_h2d_bytes(const sfdb200_plan* plan);
+SFDB200_API long sfdb200_d2h_bytes(const sfdb200_plan* plan);
+
+/* ---- host helpers mirroring sfd::seismic (bit-exact with the reference) -- */
+
+/* fd_coefficients(2, so) as doubles, w[0..so] for offsets -so/2..so/2 (fd.cpp:8-60). */
+SFDB200_API int sfdb200_fd2(int space_order, double* w);
+/* make_model: padded extents, m (edge-replicated), damp (seismic.cpp:100-173). */
+SFDB200_API int sfdb200_make_model(int ndim, const long* interior, double h, long nbpml, int space_order,
+                       const double* m_interior, long* padded, double* m, double* damp);
+/* build_damping (seismic.cpp:47-62,152-173): per-cell max of the axis tapers. */
+SFDB200_API int sfdb200_build_damping(int ndim, const long* padded, long nbpml, long halo,
+                                      double h, double* out);
+/* locate_points (seismic.cpp:195-230): idx [n][ndim] (padded frame), w [n][2^ndim]. */
+SFDB200_API int sfdb200_locate_points(int ndim, const long* interior, double h, long nbpml,
+                          int space_order, long npoints, const double* coords, long* idx,
+                          double* w);
+/* ricker (seismic.cpp:175-185) and critical_dt (seismic.cpp:187-193). */
+SFDB200_API int sfdb200_ricker(double f0, double t0, long nt, double dt, double* out);
+SFDB200_API double sfdb200_critical_dt(int ndim, double h, int space_order, double m_min);
+
+SFDB200_API const char* sfdb200_last_error(void);
+SFDB200_API const char* sfdb200_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SFDB200_H */

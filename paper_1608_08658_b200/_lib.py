@@ -1,0 +1,204 @@
+"""ctypes binding of the C ABI in include/sfdb200.h (libsfdb200.so, in-tree).
+
+No fallback: if the CUDA library is missing or a call fails, this raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+PKG_DIR = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG_DIR, "libsfdb200.so")
+
+FORWARD, ADJOINT, GRADIENT = 0, 1, 2
+OK, EINVAL, ECUDA, ENOMEM, ENONFINITE = 0, 1, 2, 3, 4
+
+
+class Desc(C.Structure):
+    """sfdb200_desc (include/sfdb200.h)."""
+
+    _fields_ = [("kind", C.c_int), ("ndim", C.c_int), ("padded", C.c_long * 3),
+                ("space_order", C.c_int), ("nt", C.c_long), ("dt", C.c_double),
+                ("h", C.c_double), ("nsrc", C.c_long), ("nrec", C.c_long), ("save", C.c_int),
+                ("device", C.c_int)]
+
+
+class SfdError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(msg)
+        self.code = code
+
+
+class InvalidArgument(SfdError, ValueError):
+    """Mirrors the reference's std::invalid_argument."""
+
+
+_i, _L, _D, _P = C.c_int, C.c_long, C.c_double, C.c_void_p
+_dp, _lp = C.POINTER(C.c_double), C.POINTER(C.c_long)
+_SIGS = {
+    "sfdb200_call": (_i, [_P, _P]),
+    "sfdb200_plan_create": (_i, [_P, _P]),
+    "sfdb200_plan_destroy": (_i, [_P]),
+    "sfdb200_run": (_i, [_P, _P]),
+    "sfdb200_upload": (_i, [_P, _P]),
+    "sfdb200_execute": (_i, [_P]),
+    "sfdb200_download": (_i, [_P, _P]),
+    "sfdb200_bind_history": (_i, [_P, _P]),
+    "sfdb200_set_stream": (_i, [_P, _P]),
+    "sfdb200_set_timing": (_i, [_P, _i]),
+    "sfdb200_stencil_time": (_i, [_P, _dp, _lp]),
+    "sfdb200_launches_per_execute": (_L, [_P]),
+    "sfdb200_points_per_step": (_L, [_P]),
+    "sfdb200_steps": (_L, [_P]),
+    "sfdb200_h2d_bytes": (_L, [_P]),
+    "sfdb200_d2h_bytes": (_L, [_P]),
+    "sfdb200_fd2": (_i, [_i, _dp]),
+    "sfdb200_make_model": (_i, [_i, _lp, _D, _L, _i, _dp, _lp, _dp, _dp]),
+    "sfdb200_build_damping": (_i, [_i, _lp, _L, _L, _D, _dp]),
+    "sfdb200_locate_points": (_i, [_i, _lp, _D, _L, _i, _L, _dp, _lp, _dp]),
+    "sfdb200_ricker": (_i, [_D, _D, _L, _D, _dp]),
+    "sfdb200_critical_dt": (_D, [_i, _D, _i, _D]),
+    "sfdb200_last_error": (C.c_char_p, []),
+    "sfdb200_version": (C.c_char_p, []),
+}
+EXPORTS = tuple(_SIGS)
+
+_lib = None
+
+
+def lib():
+    """Loads libsfdb200.so (fails loudly when it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: build it with "
+                              "`python -c 'import __graft_entry__ as g; g.build()'`")
+        lib_ = C.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            f = getattr(lib_, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = lib_
+    return _lib
+
+
+def check(rc):
+    if rc != OK:
+        msg = lib().sfdb200_last_error().decode()
+        if rc == EINVAL:
+            raise InvalidArgument(rc, msg)
+        raise SfdError(rc, msg)
+
+
+def dptr(a):
+    return a.ctypes.data_as(_dp)
+
+
+def lptr(a):
+    return a.ctypes.data_as(_lp)
+
+
+def argv_of(arrays):
+    """void*[] over numpy arrays (None -> NULL), keeping the arrays alive."""
+    arr = (C.c_void_p * len(arrays))()
+    for i, a in enumerate(arrays):
+        arr[i] = None if a is None else a.ctypes.data
+    return arr
+
+
+class Plan:
+    """Owning handle of an sfdb200_plan."""
+
+    def __init__(self, kind, ndim, padded, space_order, nt, dt, h, nsrc, nrec, save=False,
+                 device=0):
+        d = Desc()
+        d.kind, d.ndim, d.space_order = kind, ndim, space_order
+        for i in range(3):
+            d.padded[i] = int(padded[i]) if i < len(padded) else 0
+        d.nt, d.dt, d.h, d.nsrc, d.nrec = int(nt), float(dt), float(h), int(nsrc), int(nrec)
+        d.save, d.device = int(bool(save)), int(device)
+        self.desc = d
+        h_ = C.c_void_p()
+        check(lib().sfdb200_plan_create(C.byref(d), C.byref(h_)))
+        self.handle = h_
+        self._keep = None
+
+    def close(self):
+        if self.handle:
+            lib().sfdb200_plan_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def upload(self, arrays):
+        self._keep = arrays
+        check(lib().sfdb200_upload(self.handle, argv_of(arrays)))
+
+    def execute(self):
+        check(lib().sfdb200_execute(self.handle))
+
+    def download(self, arrays):
+        check(lib().sfdb200_download(self.handle, argv_of(arrays)))
+
+    def run(self, arrays):
+        check(lib().sfdb200_run(self.handle, argv_of(arrays)))
+
+    def bind_history(self, forward_plan):
+        check(lib().sfdb200_bind_history(self.handle, forward_plan.handle))
+
+    def set_stream(self, stream_handle):
+        check(lib().sfdb200_set_stream(self.handle, C.c_void_p(stream_handle or None)))
+
+    def set_timing(self, on):
+        check(lib().sfdb200_set_timing(self.handle, int(bool(on))))
+
+    def stencil_time(self):
+        ms = C.c_double()
+        n = C.c_long()
+        check(lib().sfdb200_stencil_time(self.handle, C.byref(ms), C.byref(n)))
+        return ms.value, n.value
+
+    @property
+    def launches_per_execute(self):
+        return lib().sfdb200_launches_per_execute(self.handle)
+
+    @property
+    def points_per_step(self):
+        return lib().sfdb200_points_per_step(self.handle)
+
+    @property
+    def steps(self):
+        return lib().sfdb200_steps(self.handle)
+
+    @property
+    def h2d_bytes(self):
+        return lib().sfdb200_h2d_bytes(self.handle)
+
+    @property
+    def d2h_bytes(self):
+        return lib().sfdb200_d2h_bytes(self.handle)
+
+
+def call(kind, ndim, padded, space_order, nt, dt, h, nsrc, nrec, save, arrays, device=0):
+    """sfdb200_call: the `<Name>_call(argv)` drop-in with a descriptor."""
+    d = Desc()
+    d.kind, d.ndim, d.space_order = kind, ndim, space_order
+    for i in range(3):
+        d.padded[i] = int(padded[i]) if i < len(padded) else 0
+    d.nt, d.dt, d.h, d.nsrc, d.nrec = int(nt), float(dt), float(h), int(nsrc), int(nrec)
+    d.save, d.device = int(bool(save)), int(device)
+    check(lib().sfdb200_call(C.byref(d), argv_of(arrays)))
+
+
+def f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def i64(a):
+    return np.ascontiguousarray(a, dtype=np.int64)

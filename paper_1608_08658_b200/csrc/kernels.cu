@@ -1,0 +1,460 @@
+// sm_100a kernels for the damped acoustic stencil hot path.
+//
+// Reference semantics (what each kernel replaces):
+//   sweep3d / sweep2d  the emitted spatial sweep, proj/src/codegen.cpp:348-417
+//                      (golden proj/tests/golden/forward_3d_full.c:41-50); the
+//                      damping term is fused (it is part of the solved update)
+//   GRAD variant       the second assignment of build_gradient_ir,
+//                      proj/src/seismic.cpp:311-318, in summation-by-parts form
+//   inject             Inject sparse op, codegen.cpp:436-449 / interpreter.cpp:135-149
+//   sample             Sample sparse op, codegen.cpp:450-458 / interpreter.cpp:150-160
+//
+// Design: the 3-D sweep is a 2.5-D z-streaming stencil.  A CTA
+// owns a 32 x TY column of (y, x) and marches along z.  Per z-plane one thread
+// issues TMA box loads (cp.async.bulk.tensor) into a ring of shared-memory
+// stages guarded by mbarriers: the u1 plane with its R-wide x/y halo, the u1
+// centre box R planes ahead (feeds the per-thread register queue that holds
+// the 2R+1 z-neighbours), and the u2 / c1 / c2 (and u_t) centre boxes.  Every
+// HBM byte is read once per step (halo re-reads hit L2), the output is stored
+// straight from registers with 128-byte coalesced rows.
+#include "kernels.cuh"
+
+#include <cmath>
+
+namespace sfdb200 {
+namespace {
+
+// ---------------------------------------------------------------- PTX helpers
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void fence_barrier_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            int c2, int c3, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
+        "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ float* align128(unsigned char* p) {
+    return reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(p) + 127) & ~uintptr_t(127));
+}
+
+template <int R, int BY, int NY, bool GRAD>
+struct Tile {
+    static constexpr int TX = 32;
+    static constexpr int TY = BY * NY;
+    static constexpr int BW = (TX + 2 * R + 3) & ~3;           // halo row pitch (16 B multiple)
+    static constexpr int HF = ((TY + 2 * R) * BW + 31) & ~31;  // halo floats, 128 B multiple
+    static constexpr int CF = TY * TX;                         // centre box floats
+    static constexpr int NC = GRAD ? 5 : 4;                    // u1c, u2, c1, c2, [ut]
+    static constexpr int SF = HF + NC * CF;                    // floats per stage
+    static constexpr uint32_t BYTES = static_cast<uint32_t>(SF) * 4u;
+};
+
+// ---------------------------------------------------------------- 3-D sweep
+
+template <int R, int BY, int NY, int S, bool GRAD>
+__global__ void __launch_bounds__(32 * BY)
+    sweep3d_kernel(const __grid_constant__ CUtensorMap tm_uh,
+                   const __grid_constant__ CUtensorMap tm_uc,
+                   const __grid_constant__ CUtensorMap tm_c1,
+                   const __grid_constant__ CUtensorMap tm_c2,
+                   const __grid_constant__ CUtensorMap tm_ut, const SweepArgs a, const int Px,
+                   const int Py, const long long py, const long long pz) {
+    using T = Tile<R, BY, NY, GRAD>;
+    extern __shared__ unsigned char smem_raw[];
+    float* smem = align128(smem_raw);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * T::SF);
+
+    const int lx = threadIdx.x;
+    const int ly0 = threadIdx.y * NY;
+    const int tid = threadIdx.y * 32 + lx;
+    const int x0 = R + blockIdx.x * T::TX;
+    const int y0 = R + blockIdx.y * T::TY;
+    const int zb = a.zlo + blockIdx.z * a.zchunk;
+    const int ze = min(zb + a.zchunk, a.zhi);
+    if (zb >= ze) return;
+    const int n = ze - zb;
+    const int x = x0 + lx;
+
+    auto issue = [&](int stage, int z) {
+        float* sb = smem + stage * T::SF;
+        uint64_t* bar = &bars[stage];
+        mbar_arrive_expect_tx(bar, T::BYTES);
+        tma_load_4d(sb, &tm_uh, x0 - R, y0 - R, z, a.row_u1, bar);
+        tma_load_4d(sb + T::HF, &tm_uc, x0, y0, z + R, a.row_u1, bar);
+        tma_load_4d(sb + T::HF + T::CF, &tm_uc, x0, y0, z, a.row_u2, bar);
+        tma_load_4d(sb + T::HF + 2 * T::CF, &tm_c1, x0, y0, z, 0, bar);
+        tma_load_4d(sb + T::HF + 3 * T::CF, &tm_c2, x0, y0, z, 0, bar);
+        if constexpr (GRAD) tma_load_4d(sb + T::HF + 4 * T::CF, &tm_ut, x0, y0, z, a.row_ut, bar);
+    };
+
+    if (tid == 0) {
+#pragma unroll
+        for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+        fence_barrier_init();
+    }
+    __syncthreads();
+    if (tid == 0) {
+        for (int s = 0; s < S && s < n; ++s) issue(s, zb + s);
+    }
+
+    // Register queue: q[j][i] = u1 at plane z - R + i for this thread's column.
+    float q[NY][2 * R + 1];
+    bool valid[NY];
+    const bool xin = x < Px - R;
+#pragma unroll
+    for (int j = 0; j < NY; ++j) {
+        const int y = y0 + ly0 + j;
+        valid[j] = xin && (y < Py - R);
+        const float* col = a.u1 + static_cast<long long>(y) * py + x;
+#pragma unroll
+        for (int i = 0; i < 2 * R; ++i)
+            q[j][i] = valid[j] ? __ldg(col + static_cast<long long>(zb - R + i) * pz) : 0.0f;
+    }
+
+    float* outp = a.out + static_cast<long long>(y0 + ly0) * py + x;
+    float* gp = GRAD ? a.grad + static_cast<long long>(y0 + ly0) * py + x : nullptr;
+
+    for (int i = 0; i < n; ++i) {
+        const int st = i % S;
+        mbar_wait(&bars[st], static_cast<uint32_t>((i / S) & 1));
+        const float* H = smem + st * T::SF;
+        const float* Cq = H + T::HF;
+        const float* U2 = Cq + T::CF;
+        const float* C1 = U2 + T::CF;
+        const float* C2 = C1 + T::CF;
+        const float* UT = C2 + T::CF;
+
+#pragma unroll
+        for (int j = 0; j < NY; ++j) q[j][2 * R] = Cq[(ly0 + j) * T::TX + lx];
+
+        // y-neighbour column: rows outside this thread's NY block.
+        float ya[R], yb[R];
+        const float* hcol = H + ly0 * T::BW + lx + R;
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+            ya[k] = hcol[k * T::BW];                // smem row k   -> tile row ly0 + k - R
+            yb[k] = hcol[(NY + R + k) * T::BW];     // smem row NY+R+k
+        }
+        const long long zoff = static_cast<long long>(zb + i) * pz;
+
+#pragma unroll
+        for (int j = 0; j < NY; ++j) {
+            const float c0 = q[j][R];
+            const float* hrow = H + (ly0 + j + R) * T::BW + lx + R;
+            float lap = 0.0f;
+#pragma unroll
+            for (int k = 1; k <= R; ++k) {
+                // smem row index of the y-neighbours of point j at -k / +k
+                const int rm = j + R - k, rp = j + R + k;
+                const float ym = rm < R ? ya[rm] : (rm < R + NY ? q[rm - R][R] : yb[rm - R - NY]);
+                const float yp = rp < R + NY ? (rp < R ? ya[rp] : q[rp - R][R]) : yb[rp - R - NY];
+                float s = (hrow[-k] + hrow[k]) + (ym + yp);
+                s += q[j][R - k] + q[j][R + k];
+                s = fmaf(a.neg2nd, c0, s);
+                lap = fmaf(a.w[k], s, lap);
+            }
+            const int ci = (ly0 + j) * T::TX + lx;
+            const float d = c0 - U2[ci];
+            const float inc = fmaf(C1[ci], d, C2[ci] * lap);
+            if (valid[j]) {
+                outp[zoff + j * py] = c0 + inc;
+                if constexpr (GRAD) {
+                    float* g = gp + zoff + j * py;
+                    *g = fmaf(a.nidt2 * UT[ci], inc - d, *g);
+                }
+            }
+        }
+
+#pragma unroll
+        for (int j = 0; j < NY; ++j)
+#pragma unroll
+            for (int k = 0; k < 2 * R; ++k) q[j][k] = q[j][k + 1];
+
+        __syncthreads();
+        if (tid == 0 && i + S < n) {
+            fence_proxy_async();
+            issue(st, zb + i + S);
+        }
+    }
+}
+
+template <int R, int BY, int NY, int S, bool GRAD>
+cudaError_t launch3d_t(const FieldGeom& g, const SweepConfig& cfg, const SweepMaps& m,
+                       const SweepArgs& a, cudaStream_t s) {
+    auto kern = sweep3d_kernel<R, BY, NY, S, GRAD>;
+    const size_t smem = sweep3d_smem_bytes(R, cfg, GRAD);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    dim3 grid(cfg.tiles_x, cfg.tiles_y, cfg.zchunks);
+    dim3 block(32, BY);
+    kern<<<grid, block, smem, s>>>(m.uh, m.uc, m.c1, m.c2, m.ut, a, g.Px, g.Py, g.py, g.pz);
+    return cudaGetLastError();
+}
+
+template <int R, bool GRAD>
+cudaError_t launch3d_r(const FieldGeom& g, const SweepConfig& cfg, const SweepMaps& m,
+                       const SweepArgs& a, cudaStream_t s) {
+    if (cfg.by == 4 && cfg.ny == 4 && cfg.stages == 4)
+        return launch3d_t<R, 4, 4, 4, GRAD>(g, cfg, m, a, s);
+    if (cfg.by == 8 && cfg.ny == 2 && cfg.stages == 4)
+        return launch3d_t<R, 8, 2, 4, GRAD>(g, cfg, m, a, s);
+    if (cfg.by == 4 && cfg.ny == 8 && cfg.stages == 3)
+        return launch3d_t<R, 4, 8, 3, GRAD>(g, cfg, m, a, s);
+    return cudaErrorInvalidConfiguration;
+}
+
+// ---------------------------------------------------------------- 2-D sweep
+// 2-D fields are small (cfg1: 285^2 cells = 0.3 MB per row, L2-resident):
+// one thread per point, neighbours through L1.
+
+template <int R, bool GRAD>
+__global__ void __launch_bounds__(256) sweep2d_kernel(const SweepArgs a, const int Px,
+                                                       const long long pz) {
+    const int x = R + blockIdx.x * 32 + threadIdx.x;
+    const int z = R + blockIdx.y * 8 + threadIdx.y;
+    if (x >= Px - R || z >= a.zhi) return;
+    const long long o = static_cast<long long>(z) * pz + x;
+    const float* u1 = a.u1 + o;
+    const float c0 = __ldg(u1);
+    float lap = 0.0f;
+#pragma unroll
+    for (int k = 1; k <= R; ++k) {
+        float s = (__ldg(u1 - k) + __ldg(u1 + k)) + (__ldg(u1 - k * pz) + __ldg(u1 + k * pz));
+        s = fmaf(a.neg2nd, c0, s);
+        lap = fmaf(a.w[k], s, lap);
+    }
+    const float d = c0 - __ldg(a.u2 + o);
+    const float inc = fmaf(__ldg(a.c1 + o), d, __ldg(a.c2 + o) * lap);
+    a.out[o] = c0 + inc;
+    if constexpr (GRAD) a.grad[o] = fmaf(a.nidt2 * __ldg(a.ut + o), inc - d, a.grad[o]);
+}
+
+// ---------------------------------------------------------------- sparse ops
+
+__global__ void inject_kernel(float* __restrict__ field, const long long* __restrict__ off,
+                              const float* __restrict__ coef, const float* __restrict__ row,
+                              long total, int corners_log2, float* __restrict__ grad,
+                              const float* __restrict__ ut,
+                              const unsigned char* __restrict__ gmask, float nidt2) {
+    const long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
+    if (i >= total) return;
+    const long p = i >> corners_log2;
+    const long long o = off[i];
+    const float delta = coef[i] * row[p];
+    atomicAdd(field + o, delta);
+    if (grad && gmask[i]) atomicAdd(grad + o, nidt2 * ut[o] * delta);
+}
+
+__global__ void sample_kernel(const float* __restrict__ field, const long long* __restrict__ off,
+                              const float* __restrict__ w, float* __restrict__ row, long n,
+                              int corners) {
+    const long p = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
+    if (p >= n) return;
+    float acc = 0.0f;
+    for (int c = 0; c < corners; ++c) acc = fmaf(w[p * corners + c], field[off[p * corners + c]], acc);
+    row[p] = acc;
+}
+
+// ---------------------------------------------------------------- conversions
+
+__global__ void coeffs_kernel(const double* __restrict__ m, const double* __restrict__ damp,
+                              double dt, float* __restrict__ c1, float* __restrict__ c2,
+                              long long cells, int Px, int XP) {
+    const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (i >= cells) return;
+    const long long r = i / Px, x = i - r * Px;
+    const double a = m[i] / (dt * dt);
+    const double b = damp[i] / (2.0 * dt);
+    c1[r * XP + x] = static_cast<float>((a - b) / (a + b));
+    c2[r * XP + x] = static_cast<float>(1.0 / (a + b));
+}
+
+__global__ void to_f32_kernel(const double* __restrict__ src, float* __restrict__ dst,
+                              long long n, int Px, int XP) {
+    const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    const long long r = i / Px, x = i - r * Px;
+    dst[r * XP + x] = static_cast<float>(src[i]);
+}
+
+__global__ void to_f64_kernel(const float* __restrict__ src, double* __restrict__ dst,
+                              long long n, int Px, int XP) {
+    const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    const long long r = i / Px, x = i - r * Px;
+    dst[i] = static_cast<double>(src[r * XP + x]);
+}
+
+__global__ void nonfinite_kernel(const float* __restrict__ a, long long n,
+                                 unsigned long long* counter) {
+    unsigned long long bad = 0;
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x)
+        bad += !isfinite(a[i]);
+    bad = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(bad));
+    if ((threadIdx.x & 31) == 0 && bad) atomicAdd(counter, bad);
+}
+
+unsigned grid_for(long long n, int block) {
+    return static_cast<unsigned>((n + block - 1) / block);
+}
+
+}  // namespace
+
+size_t sweep3d_smem_bytes(int R, const SweepConfig& cfg, bool grad) {
+    const int TY = cfg.ty();
+    const int BW = cfg.bw(R);
+    const int HF = ((TY + 2 * R) * BW + 31) & ~31;
+    const int CF = TY * 32;
+    const int SF = HF + (grad ? 5 : 4) * CF;
+    return static_cast<size_t>(cfg.stages) * SF * 4 + cfg.stages * 8 + 128;
+}
+
+cudaError_t launch_sweep3d(const FieldGeom& g, const SweepConfig& cfg, const SweepMaps& m,
+                           const SweepArgs& a, bool grad, cudaStream_t s) {
+#define SFDB_R_CASE(RR)                                                   \
+    case RR:                                                              \
+        return grad ? launch3d_r<RR, true>(g, cfg, m, a, s)               \
+                    : launch3d_r<RR, false>(g, cfg, m, a, s);
+    switch (g.R) {
+        SFDB_R_CASE(1)
+        SFDB_R_CASE(2)
+        SFDB_R_CASE(3)
+        SFDB_R_CASE(4)
+        SFDB_R_CASE(5)
+        SFDB_R_CASE(6)
+        SFDB_R_CASE(7)
+        SFDB_R_CASE(8)
+        default:
+            return cudaErrorInvalidValue;
+    }
+#undef SFDB_R_CASE
+}
+
+cudaError_t launch_sweep2d(const FieldGeom& g, const SweepArgs& a, bool grad, cudaStream_t s) {
+    const dim3 block(32, 8);
+    const dim3 grid(grid_for(g.Px - 2 * g.R, 32), grid_for(g.Pz - 2 * g.R, 8));
+#define SFDB_R_CASE(RR)                                                          \
+    case RR:                                                                     \
+        if (grad)                                                                \
+            sweep2d_kernel<RR, true><<<grid, block, 0, s>>>(a, g.Px, g.pz);      \
+        else                                                                     \
+            sweep2d_kernel<RR, false><<<grid, block, 0, s>>>(a, g.Px, g.pz);     \
+        break;
+    switch (g.R) {
+        SFDB_R_CASE(1)
+        SFDB_R_CASE(2)
+        SFDB_R_CASE(3)
+        SFDB_R_CASE(4)
+        SFDB_R_CASE(5)
+        SFDB_R_CASE(6)
+        SFDB_R_CASE(7)
+        SFDB_R_CASE(8)
+        default:
+            return cudaErrorInvalidValue;
+    }
+#undef SFDB_R_CASE
+    return cudaGetLastError();
+}
+
+cudaError_t launch_inject(float* field, const long long* off, const float* coef,
+                          const float* row, long npoints, int corners, float* grad,
+                          const float* ut, const unsigned char* gmask, float nidt2,
+                          cudaStream_t s) {
+    const long total = npoints * corners;
+    if (total == 0) return cudaSuccess;
+    int lg = 0;
+    while ((1 << lg) < corners) ++lg;
+    inject_kernel<<<grid_for(total, 128), 128, 0, s>>>(field, off, coef, row, total, lg, grad,
+                                                       ut, gmask, nidt2);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sample(const float* field, const long long* off, const float* w, float* row,
+                          long npoints, int corners, cudaStream_t s) {
+    if (npoints == 0) return cudaSuccess;
+    sample_kernel<<<grid_for(npoints, 256), 256, 0, s>>>(field, off, w, row, npoints, corners);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_coeffs(const FieldGeom& g, const double* m, const double* damp, double dt,
+                          float* c1, float* c2, cudaStream_t s) {
+    const long long cells = static_cast<long long>(g.Pz) * g.Py * g.Px;
+    coeffs_kernel<<<grid_for(cells, 256), 256, 0, s>>>(m, damp, dt, c1, c2, cells, g.Px, g.XP);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_to_f32(const FieldGeom& g, const double* src, float* dst, long long rows,
+                          cudaStream_t s) {
+    const long long n = rows * g.Pz * g.Py * g.Px;
+    if (n == 0) return cudaSuccess;
+    to_f32_kernel<<<grid_for(n, 256), 256, 0, s>>>(src, dst, n, g.Px, g.XP);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_to_f64(const FieldGeom& g, const float* src, double* dst, long long rows,
+                          cudaStream_t s) {
+    const long long n = rows * g.Pz * g.Py * g.Px;
+    if (n == 0) return cudaSuccess;
+    to_f64_kernel<<<grid_for(n, 256), 256, 0, s>>>(src, dst, n, g.Px, g.XP);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dense_to_f32(const double* src, float* dst, long long n, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    to_f32_kernel<<<grid_for(n, 256), 256, 0, s>>>(src, dst, n, 1, 1);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_dense_to_f64(const float* src, double* dst, long long n, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    to_f64_kernel<<<grid_for(n, 256), 256, 0, s>>>(src, dst, n, 1, 1);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_count_nonfinite(const float* a, long long n, unsigned long long* counter,
+                                   cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    nonfinite_kernel<<<592, 256, 0, s>>>(a, n, counter);
+    return cudaGetLastError();
+}
+
+}  // namespace sfdb200

@@ -1,0 +1,96 @@
+// Internal interface between the plan/runtime layer (plan.cu) and the sm_100a
+// kernels (kernels.cu).  No torch, no reference types: plain pointers.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace sfdb200 {
+
+constexpr int kMaxRadius = 8;  // space order 16
+
+// Device field layout: fp32, row-major
+// [row][z][y][x] with x padded to a 128-byte pitch XP (XP % 32 == 0), y
+// unpadded.  2-D problems use Py == 1 ([row][z][1][x]).
+struct FieldGeom {
+    int ndim;
+    int R;                 // stencil radius = space_order / 2
+    int Pz, Py, Px;        // padded extents (Py == 1 in 2-D)
+    int XP;                // x pitch in elements
+    long long py, pz;      // element strides of y rows and z planes
+    long long slot;        // elements per time row (Pz * pz)
+};
+
+// Sweep of the solved damped update, written in the incremental form
+//   out = u1 + c1 (u1 - u2) + c2 lap(u1),  c1 = (a-b)/(a+b), c2 = 1/(a+b),
+//   a = m/dt^2, b = damp/(2 dt)
+// (algebraically the reference's (2a u1 - (a-b) u2 + lap)/(a+b),
+// tests/golden/forward_3d_full.c:44-49).  With GRAD the same pass accumulates
+// the imaging condition grad += -(1/dt^2) u_t (v_t - 2 v_{t+1} + v_{t+2}).
+struct SweepArgs {
+    float* out;             // output row base
+    const float* u1;        // row read at stencil offsets
+    const float* u2;        // row read at the centre
+    const float* c1;
+    const float* c2;
+    const float* ut;        // GRAD: u history row t
+    float* grad;            // GRAD
+    int row_out, row_u1, row_u2, row_ut;  // row coordinates for the tensor maps
+    int zlo, zhi, zchunk;   // updated z range and planes per CTA
+    float w[kMaxRadius + 1];  // w_k / h^2
+    float neg2nd;           // -2 * ndim
+    float nidt2;            // -1 / dt^2
+};
+
+struct SweepMaps {          // TMA descriptors (3-D only)
+    CUtensorMap uh;         // u1 rows, halo box (BW, TY+2R, 1, 1)
+    CUtensorMap uc;         // u1/u2 rows, centre box (32, TY, 1, 1)
+    CUtensorMap c1, c2;     // coefficient fields, centre box
+    CUtensorMap ut;         // GRAD: history rows, centre box
+};
+
+struct SweepConfig {        // 3-D tiling, chosen by choose_config()
+    int by = 4;             // warps per CTA (each warp: 32 x-columns)
+    int ny = 4;             // y rows per thread
+    int stages = 4;         // TMA pipeline depth
+    int zchunks = 1;        // CTAs along z per (x, y) tile
+    int tiles_x = 0, tiles_y = 0;
+    size_t smem_bytes = 0;
+    int ty() const { return by * ny; }
+    int bw(int R) const { return (32 + 2 * R + 3) & ~3; }
+};
+
+size_t sweep3d_smem_bytes(int R, const SweepConfig& cfg, bool grad);
+cudaError_t launch_sweep3d(const FieldGeom& g, const SweepConfig& cfg, const SweepMaps& maps,
+                           const SweepArgs& a, bool grad, cudaStream_t s);
+cudaError_t launch_sweep2d(const FieldGeom& g, const SweepArgs& a, bool grad, cudaStream_t s);
+
+// Sparse operators.  off[p][c] = element offset of corner c of point p inside
+// one row; coef = w dt^2 / m[corner] (inject) or w (sample), fp32.
+// GRAD: the imaging condition of the row just finalised also sees the
+// injected increment, grad[c] += -(1/dt^2) u_t[c] delta, for corners inside
+// the updated region (gmask[p][c] != 0).
+cudaError_t launch_inject(float* field, const long long* off, const float* coef,
+                          const float* row, long npoints, int corners, float* grad,
+                          const float* ut, const unsigned char* gmask, float nidt2,
+                          cudaStream_t s);
+cudaError_t launch_sample(const float* field, const long long* off, const float* w, float* row,
+                          long npoints, int corners, cudaStream_t s);
+
+// Format conversion between the reference's dense fp64 layout and the device
+// fp32 pitched layout.
+cudaError_t launch_coeffs(const FieldGeom& g, const double* m, const double* damp, double dt,
+                          float* c1, float* c2, cudaStream_t s);
+cudaError_t launch_to_f32(const FieldGeom& g, const double* src, float* dst, long long rows,
+                          cudaStream_t s);
+cudaError_t launch_to_f64(const FieldGeom& g, const float* src, double* dst, long long rows,
+                          cudaStream_t s);
+cudaError_t launch_dense_to_f32(const double* src, float* dst, long long n, cudaStream_t s);
+cudaError_t launch_dense_to_f64(const float* src, double* dst, long long n, cudaStream_t s);
+// Counts non-finite values (the reference's check_finite, seismic.cpp:39-44).
+cudaError_t launch_count_nonfinite(const float* a, long long n, unsigned long long* counter,
+                                   cudaStream_t s);
+
+}  // namespace sfdb200
