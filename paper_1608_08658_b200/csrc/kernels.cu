@@ -48,16 +48,26 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                  : "memory");
 }
 
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
     asm volatile(
         "{\n"
         ".reg .pred p;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
         : "memory");
+    return ok != 0;
+}
+
+// Spins on the stage barrier; a transaction count that can never complete
+// (a bug) traps instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t spins = 0;
+    while (!mbar_try_wait(bar, parity))
+        if (++spins == (1u << 26)) __trap();
 }
 
 __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1,
@@ -78,12 +88,16 @@ template <int R, int BY, int NY, bool GRAD>
 struct Tile {
     static constexpr int TX = 32;
     static constexpr int TY = BY * NY;
-    static constexpr int BW = (TX + 2 * R + 3) & ~3;           // halo row pitch (16 B multiple)
+    // TMA box starts must be 16-byte aligned in x: tiles start at multiples of
+    // 32 columns and the x halo is widened to RA = roundup(R, 4).
+    static constexpr int RA = (R + 3) & ~3;
+    static constexpr int BW = TX + 2 * RA;                     // halo row pitch
     static constexpr int HF = ((TY + 2 * R) * BW + 31) & ~31;  // halo floats, 128 B multiple
     static constexpr int CF = TY * TX;                         // centre box floats
     static constexpr int NC = GRAD ? 5 : 4;                    // u1c, u2, c1, c2, [ut]
     static constexpr int SF = HF + NC * CF;                    // floats per stage
-    static constexpr uint32_t BYTES = static_cast<uint32_t>(SF) * 4u;
+    // Bytes the TMA boxes of one stage deliver (the mbarrier transaction count).
+    static constexpr uint32_t BYTES = static_cast<uint32_t>((TY + 2 * R) * BW + NC * CF) * 4u;
 };
 
 // ---------------------------------------------------------------- 3-D sweep
@@ -104,7 +118,7 @@ __global__ void __launch_bounds__(32 * BY)
     const int lx = threadIdx.x;
     const int ly0 = threadIdx.y * NY;
     const int tid = threadIdx.y * 32 + lx;
-    const int x0 = R + blockIdx.x * T::TX;
+    const int x0 = blockIdx.x * T::TX;
     const int y0 = R + blockIdx.y * T::TY;
     const int zb = a.zlo + blockIdx.z * a.zchunk;
     const int ze = min(zb + a.zchunk, a.zhi);
@@ -116,7 +130,7 @@ __global__ void __launch_bounds__(32 * BY)
         float* sb = smem + stage * T::SF;
         uint64_t* bar = &bars[stage];
         mbar_arrive_expect_tx(bar, T::BYTES);
-        tma_load_4d(sb, &tm_uh, x0 - R, y0 - R, z, a.row_u1, bar);
+        tma_load_4d(sb, &tm_uh, x0 - T::RA, y0 - R, z, a.row_u1, bar);
         tma_load_4d(sb + T::HF, &tm_uc, x0, y0, z + R, a.row_u1, bar);
         tma_load_4d(sb + T::HF + T::CF, &tm_uc, x0, y0, z, a.row_u2, bar);
         tma_load_4d(sb + T::HF + 2 * T::CF, &tm_c1, x0, y0, z, 0, bar);
@@ -137,7 +151,7 @@ __global__ void __launch_bounds__(32 * BY)
     // Register queue: q[j][i] = u1 at plane z - R + i for this thread's column.
     float q[NY][2 * R + 1];
     bool valid[NY];
-    const bool xin = x < Px - R;
+    const bool xin = x >= R && x < Px - R;
 #pragma unroll
     for (int j = 0; j < NY; ++j) {
         const int y = y0 + ly0 + j;
@@ -166,7 +180,7 @@ __global__ void __launch_bounds__(32 * BY)
 
         // y-neighbour column: rows outside this thread's NY block.
         float ya[R], yb[R];
-        const float* hcol = H + ly0 * T::BW + lx + R;
+        const float* hcol = H + ly0 * T::BW + lx + T::RA;
 #pragma unroll
         for (int k = 0; k < R; ++k) {
             ya[k] = hcol[k * T::BW];                // smem row k   -> tile row ly0 + k - R
@@ -177,7 +191,7 @@ __global__ void __launch_bounds__(32 * BY)
 #pragma unroll
         for (int j = 0; j < NY; ++j) {
             const float c0 = q[j][R];
-            const float* hrow = H + (ly0 + j + R) * T::BW + lx + R;
+            const float* hrow = H + (ly0 + j + R) * T::BW + lx + T::RA;
             float lap = 0.0f;
 #pragma unroll
             for (int k = 1; k <= R; ++k) {

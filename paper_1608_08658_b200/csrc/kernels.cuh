@@ -59,7 +59,7 @@ struct SweepConfig {        // 3-D tiling, chosen by choose_config()
     int tiles_x = 0, tiles_y = 0;
     size_t smem_bytes = 0;
     int ty() const { return by * ny; }
-    int bw(int R) const { return (32 + 2 * R + 3) & ~3; }
+    int bw(int R) const { return 32 + 2 * ((R + 3) & ~3); }
 };
 
 size_t sweep3d_smem_bytes(int R, const SweepConfig& cfg, bool grad);

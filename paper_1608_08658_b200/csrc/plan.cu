@@ -214,7 +214,7 @@ void choose_config(sfdb200_plan& p) {
     if (const char* t = std::getenv("SFDB200_TILE")) {
         std::sscanf(t, "%d,%d,%d", &c.by, &c.ny, &c.stages);
     }
-    c.tiles_x = static_cast<int>((p.g.Px - 2 * R + 31) / 32);
+    c.tiles_x = static_cast<int>((p.g.Px - R + 31) / 32);  // tiles start at x = 0 (TMA alignment)
     c.tiles_y = static_cast<int>((p.g.Py - 2 * R + c.ty() - 1) / c.ty());
     c.smem_bytes = sweep3d_smem_bytes(R, c, p.grad_kind());
     const int by_smem = static_cast<int>((227 * 1024) / (c.smem_bytes + 1024));
