@@ -1,0 +1,339 @@
+#!/usr/bin/env python
+"""Benchmark of the damped acoustic stencil hot path (BASELINE.json metric:
+"Gpts/s (grid-point updates/sec) 3D acoustic so-8; % of HBM roofline").
+
+One bench step = one full operator run (all nt-2 time steps) over one
+synthetic problem.  At N=1 the workload is BASELINE configs[1] (cfg2: 3-D
+forward, 256^3 + 40-point damping layer, so 8, 1000 steps, 65,536 receivers).
+
+  value    Gpts/s with inputs resident in HBM (plan.execute() only), device-timed
+           with CUDA events on the plan's stream, max over ranks
+  e2e      the same metric through the C ABI with pinned HOST fp64 buffers
+           (sfdb200_run: H2D + fp64->fp32, the run, fp32->fp64 + D2H)
+  roofline dominant kernel (the 3-D sweep): algorithmic bytes per launch
+           (20 B/pt forward, 32 B/pt gradient) / mean launch time
+  cpu_baseline  the unmodified reference (oracle/_ref) on this host's cores,
+           full grid, truncated step count
+
+--impl reference runs the reference's own CPU implementation of the path
+(oracle/_ref, else the oracle C port) and prints the same metric.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# The reference's JIT'd kernels use OpenMP: all host threads, bound close.
+os.environ.setdefault("STENCILFD_THREADS", str(os.cpu_count() or 1))
+os.environ.setdefault("OMP_PROC_BIND", "close")
+os.environ.setdefault("OMP_PLACES", "cores")
+os.environ.setdefault("STENCILFD_CACHE_DIR", "/tmp/stencilfd-cache")
+
+import numpy as np  # noqa: E402
+
+BYTES_PER_POINT = {"forward": 20, "adjoint": 20, "gradient": 32}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg2",
+                    help="cfg1 | cfg2 | cfg4-so{2,4,8,12,16} | cfg5")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-steps", type=int, default=0, help="reference sample steps (0: auto)")
+    ap.add_argument("--time-steps", type=int, default=0,
+                    help="override the workload's time steps (profiling runs only)")
+    return ap.parse_args()
+
+
+def make_workload(name, time_steps=0):
+    w = _make_workload(name)
+    if time_steps:
+        w.nt = time_steps + 2
+        w.wavelet = np.ascontiguousarray(w.wavelet[:w.nt])
+    return w
+
+
+def _make_workload(name):
+    from paper_1608_08658_b200 import configs
+    if name == "cfg1":
+        return configs.cfg1()
+    if name == "cfg2":
+        return configs.cfg2()
+    if name.startswith("cfg4-so"):
+        return configs.cfg4(int(name[len("cfg4-so"):]))
+    if name == "cfg5":
+        return configs.cfg5()
+    raise SystemExit(f"unknown workload {name}")
+
+
+def problem(w):
+    from paper_1608_08658_b200 import seismic as S
+    model = S.make_model(w.interior, w.h, w.nbpml, w.space_order, w.m_interior)
+    src = S.locate_points(model, w.src_coords)
+    rec = S.locate_points(model, w.rec_coords)
+    return model, src, rec
+
+
+def config_of(w, n, extra=None):
+    c = {"workload": f"{w.name}: interior {'x'.join(map(str, w.interior))} + {w.nbpml}-pt "
+                     f"damping layer, so {w.space_order}, {w.steps} steps, "
+                     f"{len(w.src_coords)} src, {len(w.rec_coords)} rec",
+         "padded": w.padded, "space_order": w.space_order, "time_steps": w.steps,
+         "points_per_step": w.points_per_step, "nsrc": len(w.src_coords),
+         "nrec": len(w.rec_coords), "parallelism": f"replicas x{n}" if n > 1 else "1 GPU",
+         "l2": "inputs larger than L2 (each fp32 field 4*prod(padded) B > 126 MB)"
+               if 4 * int(np.prod(w.padded)) > 126e6 else "working set fits L2"}
+    if extra:
+        c.update(extra)
+    return c
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is None:
+            self.summary = None
+            return
+        time.sleep(0.25)
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        rows = [r.split(",") for r in out.strip().splitlines() if r.strip()]
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[1]))
+                mx = max(mx, float(r[2]))
+                for nm, v in zip(names, r[5:9]):
+                    if v.strip().lower() == "active":
+                        reasons.add(nm)
+            except (ValueError, IndexError):
+                continue
+        self.summary = {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
+                        "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+def ncu_traffic(workload):
+    """dram bytes per sweep launch from the committed ncu --set full summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as fh:
+            d = json.load(fh)
+        return d.get(workload, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def cpu_baseline(w, steps_hint):
+    """The reference (oracle/_ref) timed on this host's cores: full grid,
+    truncated step count.  Falls back to the C port when _ref was not built."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracle_lib as O
+    cores = int(os.environ["STENCILFD_THREADS"])
+    steps = steps_hint or max(4, min(40, int(2.0e9 / w.points_per_step)))
+    nt = steps + 2
+    trace = np.ascontiguousarray(w.wavelet[:nt])
+    if O.have_ref():
+        _, _, secs = O.ref_forward(w.interior, w.h, w.nbpml, w.space_order, w.m_interior,
+                                   w.src_coords, trace, w.rec_coords, nt, w.dt, want_u=False)
+        kind = "reference"
+    else:
+        from paper_1608_08658_b200 import seismic as S
+        model, src, rec = problem(w)
+        t0 = time.perf_counter()
+        O.forward(model.padded, w.space_order, w.h, w.dt, nt, model.m, model.damp, src.idx,
+                  src.w, trace, rec.idx, rec.w)
+        secs = time.perf_counter() - t0
+        kind = "port"
+    gpts = w.points_per_step * steps / secs / 1e9
+    return {"value": gpts, "unit": "Gpts/s", "cores": cores, "kind": kind,
+            "sample": f"seismic::forward on the full {'x'.join(map(str, w.padded))} padded grid, "
+                      f"{steps} of {w.steps} time steps (RunStats.seconds of the kernel call, "
+                      f"STENCILFD_THREADS={cores})", "seconds": secs}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    w = make_workload(args.workload, args.time_steps)
+    vals = []
+    cb = None
+    for i in range(args.warmup + args.steps):
+        cb = cpu_baseline(w, args.cpu_steps or 0)
+        if i >= args.warmup:
+            vals.append(cb["value"])
+    v = float(np.median(vals))
+    cb["value"] = v
+    line = {"metric": "Gpts/s (grid-point updates/sec) 3D acoustic so-8", "value": v,
+            "unit": "Gpts/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": cb["seconds"] * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": config_of(w, 1, {"sample": cb["sample"]}), "cpu_baseline": cb,
+            "e2e": {"value": v, "unit": "Gpts/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def run_ours(args):
+    import torch
+    from paper_1608_08658_b200 import _lib as L
+    from paper_1608_08658_b200 import seismic as S
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+
+    w = make_workload(args.workload, args.time_steps)
+    model, src, rec = problem(w)
+    S.check_dt(model, w.dt)
+    nd = model.ndim()
+    plan = L.Plan(L.FORWARD, nd, model.padded, w.space_order, w.nt, w.dt, w.h, src.npoints,
+                  rec.npoints, False, local)
+    stream = torch.cuda.Stream()
+    plan.set_stream(stream.cuda_stream)
+
+    # Pinned host buffers in the reference's layout (fp64 grids, long idx).
+    def pinned(shape, dtype):
+        return torch.empty(shape, dtype=dtype, pin_memory=True).numpy()
+
+    u = pinned((3, *model.padded), torch.float64)
+    m = pinned(model.m.shape, torch.float64); m[:] = model.m
+    damp = pinned(model.damp.shape, torch.float64); damp[:] = model.damp
+    rec_data = pinned((w.nt, rec.npoints), torch.float64)
+    trace = pinned(w.wavelet.shape, torch.float64); trace[:] = w.wavelet
+    argv = [u, m, damp, L.i64(src.idx), L.f64(src.w), trace, L.i64(rec.idx), L.f64(rec.w),
+            rec_data]
+
+    # ---- device-resident timing (value)
+    plan.upload(argv)
+    for _ in range(args.warmup):
+        plan.execute()
+    torch.cuda.synchronize()
+    plan.set_timing(True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with Clocks(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            plan.execute()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    sweep_ms, sweep_n = plan.stencil_time()  # last execute(), per-launch events
+    plan.set_timing(False)
+    if dist:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    pts = plan.points_per_step * plan.steps
+    value = pts * args.steps * world / (ms / 1e3) / 1e9
+    launches = plan.launches_per_execute * args.steps
+
+    # ---- end to end through the C ABI with host buffers (e2e)
+    e2e = None
+    if not args.no_e2e:
+        plan.run(argv)  # warm
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            plan.run(argv)
+        el = time.perf_counter() - t0
+        if dist:
+            t = torch.tensor([el], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = float(t.item())
+        e2e = {"value": pts * args.steps * world / el / 1e9, "unit": "Gpts/s",
+               "h2d_bytes_per_step": plan.h2d_bytes, "d2h_bytes_per_step": plan.d2h_bytes,
+               "ms_per_step": el / args.steps * 1e3,
+               "path": "sfdb200_run(plan, argv): reference argv, pinned fp64 host buffers"}
+
+    peak, peak_src = measured_peak()
+    per_launch_ms = sweep_ms / max(1, sweep_n)
+    alg = BYTES_PER_POINT["forward"] * plan.points_per_step
+    achieved = alg / (per_launch_ms / 1e3) / 1e9
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": ncu_traffic(w.name),
+            "kernel": "sweep3d_kernel" if nd == 3 else "sweep2d_kernel",
+            "alg_bytes_per_launch": alg, "mean_launch_ms": per_launch_ms,
+            "kernel_share_of_step": sweep_ms / (ms / args.steps), "peak_source": peak_src}
+
+    cb = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cb = cpu_baseline(w, args.cpu_steps or 0)
+        cb.pop("seconds", None)
+
+    if rank == 0:
+        line = {"metric": "Gpts/s (grid-point updates/sec) 3D acoustic so-8", "value": value,
+                "unit": "Gpts/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": config_of(w, world), "roofline": roof, "cpu_baseline": cb,
+                "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary}
+        print(json.dumps(line))
+    plan.close()
+    if dist:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

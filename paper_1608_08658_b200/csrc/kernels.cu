@@ -20,6 +20,7 @@
 #include "kernels.cuh"
 
 #include <cmath>
+#include <utility>
 
 namespace sfdb200 {
 namespace {
@@ -80,14 +81,11 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, i
         : "memory");
 }
 
-__device__ __forceinline__ float* align128(unsigned char* p) {
-    return reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(p) + 127) & ~uintptr_t(127));
-}
-
 template <int R, int BY, int NY, bool GRAD>
 struct Tile {
     static constexpr int TX = 32;
-    static constexpr int TY = BY * NY;
+    static constexpr int HALF = BY * NY;  // rows per tile half
+    static constexpr int TY = 2 * HALF;
     // TMA box starts must be 16-byte aligned in x: tiles start at multiples of
     // 32 columns and the x halo is widened to RA = roundup(R, 4).
     static constexpr int RA = (R + 3) & ~3;
@@ -98,11 +96,32 @@ struct Tile {
     static constexpr int SF = HF + NC * CF;                    // floats per stage
     // Bytes the TMA boxes of one stage deliver (the mbarrier transaction count).
     static constexpr uint32_t BYTES = static_cast<uint32_t>((TY + 2 * R) * BW + NC * CF) * 4u;
+    static constexpr int Q = 2 * R + 1;                        // z-queue length
+};
+
+__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+
+template <int V>
+struct IC {
+    static constexpr int value = V;
 };
 
 // ---------------------------------------------------------------- 3-D sweep
+//
+// Thread (lx, wy) owns column x = x0 + lx and NY rows in EACH half of the
+// tile: rows ly0 + j (top) and HALF + ly0 + j (bottom), j < NY.  Every value
+// is a float2 {top, bottom}, so the whole update runs on the packed fp32x2
+// pipe (FADD2/FFMA2/FMUL2, sm_100): per k and per point pair, 5 FADD2 for the
+// six neighbours and 2 FFMA2 for
+//     lap += w_k * ((sum of the 2*ndim neighbours at distance k) - 2*ndim*u0)
+// (the centred per-k form keeps the fp32 error ~1e-6).  The z
+// neighbours live in a register queue of Q = 2R+1 planes; with ROT the z loop
+// is unrolled by Q so the queue rotates by renaming (no moves).
 
-template <int R, int BY, int NY, int S, bool GRAD>
+template <int R, int BY, int NY, int S, bool GRAD, bool ROT>
 __global__ void __launch_bounds__(32 * BY)
     sweep3d_kernel(const __grid_constant__ CUtensorMap tm_uh,
                    const __grid_constant__ CUtensorMap tm_uc,
@@ -111,8 +130,9 @@ __global__ void __launch_bounds__(32 * BY)
                    const __grid_constant__ CUtensorMap tm_ut, const SweepArgs a, const int Px,
                    const int Py, const long long py, const long long pz) {
     using T = Tile<R, BY, NY, GRAD>;
-    extern __shared__ unsigned char smem_raw[];
-    float* smem = align128(smem_raw);
+    constexpr int Q = T::Q;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    float* smem = reinterpret_cast<float*>(smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u));
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * T::SF);
 
     const int lx = threadIdx.x;
@@ -148,24 +168,66 @@ __global__ void __launch_bounds__(32 * BY)
         for (int s = 0; s < S && s < n; ++s) issue(s, zb + s);
     }
 
-    // Register queue: q[j][i] = u1 at plane z - R + i for this thread's column.
-    float q[NY][2 * R + 1];
-    bool valid[NY];
+    const int cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    // Fused Sample of the previous step (its row is this launch's u1, complete
+    // since the previous launch): codegen.cpp:450-458, interpolation order
+    // c = 0..7.  Run after the first plane, while the TMA stages are in flight.
+    auto sample_prev = [&]() {
+        const int p0 = cta * a.smp_per_cta;
+        const int p1 = min(a.smp_n, p0 + a.smp_per_cta);
+        for (int p = p0 + tid; p < p1; p += 32 * BY) {
+            const long long* off = a.smp_off + 8LL * p;
+            const float* w = a.smp_w + 8LL * p;
+            float v[8];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) v[c] = __ldg(a.u1 + __ldg(off + c));
+            float acc = 0.0f;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) acc = fmaf(__ldg(w + c), v[c], acc);
+            a.smp_row[p] = acc;
+        }
+    };
+    int ent = 0, ent_end = 0;
+    if (a.inj_begin) {
+        ent = a.inj_begin[cta];
+        ent_end = a.inj_begin[cta + 1];
+    }
+
+    // Queue slot of plane zb - R + t is t mod Q.
+    float2 q[NY][Q];
+    bool va[NY], vb[NY];
     const bool xin = x >= R && x < Px - R;
 #pragma unroll
     for (int j = 0; j < NY; ++j) {
-        const int y = y0 + ly0 + j;
-        valid[j] = xin && (y < Py - R);
-        const float* col = a.u1 + static_cast<long long>(y) * py + x;
+        const int ya_ = y0 + ly0 + j, yb_ = ya_ + T::HALF;
+        va[j] = xin && ya_ < Py - R;
+        vb[j] = xin && yb_ < Py - R;
+        const float* ca = a.u1 + static_cast<long long>(ya_) * py + x;
+        const float* cb = a.u1 + static_cast<long long>(yb_) * py + x;
 #pragma unroll
-        for (int i = 0; i < 2 * R; ++i)
-            q[j][i] = valid[j] ? __ldg(col + static_cast<long long>(zb - R + i) * pz) : 0.0f;
+        for (int t = 0; t < 2 * R; ++t) {
+            const long long o = static_cast<long long>(zb - R + t) * pz;
+            q[j][t] = f2(va[j] ? __ldg(ca + o) : 0.0f, vb[j] ? __ldg(cb + o) : 0.0f);
+        }
     }
 
-    float* outp = a.out + static_cast<long long>(y0 + ly0) * py + x;
-    float* gp = GRAD ? a.grad + static_cast<long long>(y0 + ly0) * py + x : nullptr;
+    const float2 neg2nd = f2(a.neg2nd, a.neg2nd);
+    const float2 mone = f2(-1.0f, -1.0f);
+    float2 wk[R + 1];
+#pragma unroll
+    for (int k = 0; k <= R; ++k) wk[k] = f2(a.w[k], a.w[k]);
+    const float2 nidt2 = f2(a.nidt2, a.nidt2);
 
-    for (int i = 0; i < n; ++i) {
+    float* outa = a.out + static_cast<long long>(y0 + ly0) * py + x;
+    float* outb = outa + T::HALF * py;
+    float* ga = GRAD ? a.grad + static_cast<long long>(y0 + ly0) * py + x : nullptr;
+    float* gb = GRAD ? ga + T::HALF * py : nullptr;
+
+    // One z plane.  PH is the compile-time phase of plane i within the queue
+    // rotation (always 0 without ROT, where the queue is shifted instead).
+    auto plane = [&](auto ph_c, const int i) {
+        constexpr int PH = decltype(ph_c)::value;
+        auto slot = [](int off) { return ((PH + off + R) % Q + Q) % Q; };
         const int st = i % S;
         mbar_wait(&bars[st], static_cast<uint32_t>((i / S) & 1));
         const float* H = smem + st * T::SF;
@@ -174,65 +236,101 @@ __global__ void __launch_bounds__(32 * BY)
         const float* C1 = U2 + T::CF;
         const float* C2 = C1 + T::CF;
         const float* UT = C2 + T::CF;
+        const int ca = ly0 * T::TX + lx, cb = ca + T::HALF * T::TX;
 
 #pragma unroll
-        for (int j = 0; j < NY; ++j) q[j][2 * R] = Cq[(ly0 + j) * T::TX + lx];
+        for (int j = 0; j < NY; ++j)
+            q[j][slot(R)] = f2(Cq[ca + j * T::TX], Cq[cb + j * T::TX]);
 
-        // y-neighbour column: rows outside this thread's NY block.
-        float ya[R], yb[R];
-        const float* hcol = H + ly0 * T::BW + lx + T::RA;
+        // y neighbours outside this thread's NY rows (both halves).
+        float2 ya[R], yb[R];
+        const float* hA = H + ly0 * T::BW + lx + T::RA;   // smem row ly0 <-> tile row ly0 - R
+        const float* hB = hA + T::HALF * T::BW;
 #pragma unroll
         for (int k = 0; k < R; ++k) {
-            ya[k] = hcol[k * T::BW];                // smem row k   -> tile row ly0 + k - R
-            yb[k] = hcol[(NY + R + k) * T::BW];     // smem row NY+R+k
+            ya[k] = f2(hA[k * T::BW], hB[k * T::BW]);
+            yb[k] = f2(hA[(NY + R + k) * T::BW], hB[(NY + R + k) * T::BW]);
         }
         const long long zoff = static_cast<long long>(zb + i) * pz;
 
 #pragma unroll
         for (int j = 0; j < NY; ++j) {
-            const float c0 = q[j][R];
-            const float* hrow = H + (ly0 + j + R) * T::BW + lx + T::RA;
-            float lap = 0.0f;
+            const float2 c0 = q[j][slot(0)];
+            const float* ra = hA + (j + R) * T::BW;
+            const float* rb = hB + (j + R) * T::BW;
+            float2 lap = f2(0.0f, 0.0f);
 #pragma unroll
             for (int k = 1; k <= R; ++k) {
-                // smem row index of the y-neighbours of point j at -k / +k
-                const int rm = j + R - k, rp = j + R + k;
-                const float ym = rm < R ? ya[rm] : (rm < R + NY ? q[rm - R][R] : yb[rm - R - NY]);
-                const float yp = rp < R + NY ? (rp < R ? ya[rp] : q[rp - R][R]) : yb[rp - R - NY];
-                float s = (hrow[-k] + hrow[k]) + (ym + yp);
-                s += q[j][R - k] + q[j][R + k];
-                s = fmaf(a.neg2nd, c0, s);
-                lap = fmaf(a.w[k], s, lap);
+                const int rm = j + R - k, rp = j + R + k;  // smem rows of the y neighbours
+                const float2 ym = rm < R ? ya[rm] : (rm < R + NY ? q[rm - R][slot(0)] : yb[rm - R - NY]);
+                const float2 yp = rp < R ? ya[rp] : (rp < R + NY ? q[rp - R][slot(0)] : yb[rp - R - NY]);
+                const float2 xs = add2(f2(ra[-k], rb[-k]), f2(ra[k], rb[k]));
+                const float2 zs = add2(q[j][slot(-k)], q[j][slot(k)]);
+                float2 sk = add2(add2(xs, add2(ym, yp)), zs);
+                sk = fma2(neg2nd, c0, sk);
+                lap = fma2(wk[k], sk, lap);
             }
-            const int ci = (ly0 + j) * T::TX + lx;
-            const float d = c0 - U2[ci];
-            const float inc = fmaf(C1[ci], d, C2[ci] * lap);
-            if (valid[j]) {
-                outp[zoff + j * py] = c0 + inc;
-                if constexpr (GRAD) {
-                    float* g = gp + zoff + j * py;
-                    *g = fmaf(a.nidt2 * UT[ci], inc - d, *g);
-                }
+            const int ia = ca + j * T::TX, ib = cb + j * T::TX;
+            const float2 d = fma2(f2(U2[ia], U2[ib]), mone, c0);           // c0 - u2, exact form
+            const float2 inc = fma2(f2(C1[ia], C1[ib]), d, mul2(f2(C2[ia], C2[ib]), lap));
+            const float2 o = add2(c0, inc);
+            const long long off = zoff + j * py;
+            if (va[j]) outa[off] = o.x;
+            if (vb[j]) outb[off] = o.y;
+            if constexpr (GRAD) {
+                // grad += -(1/dt^2) u_t (v_t - 2 v_{t+1} + v_{t+2}) = nidt2 * u_t * (inc - d)
+                const float2 vtt = fma2(d, mone, inc);
+                const float2 coef = mul2(nidt2, f2(UT[ia], UT[ib]));
+                if (va[j]) ga[off] = fmaf(coef.x, vtt.x, ga[off]);
+                if (vb[j]) gb[off] = fmaf(coef.y, vtt.y, gb[off]);
             }
         }
 
+        if constexpr (!ROT) {
 #pragma unroll
-        for (int j = 0; j < NY; ++j)
+            for (int j = 0; j < NY; ++j)
 #pragma unroll
-            for (int k = 0; k < 2 * R; ++k) q[j][k] = q[j][k + 1];
-
+                for (int t = 0; t < 2 * R; ++t) q[j][t] = q[j][t + 1];
+        }
         __syncthreads();
         if (tid == 0 && i + S < n) {
             fence_proxy_async();
             issue(st, zb + i + S);
         }
+        if (i == 0 && a.smp_n) sample_prev();
+        // Fused Inject into the plane just stored (codegen.cpp:436-449): the
+        // barrier above makes the plane's stores visible; colliding corners
+        // are summed with atomics.
+        if (ent < ent_end) {
+            const int z = zb + i;
+            int hi = ent;
+            while (hi < ent_end && __ldg(a.inj_z + hi) == z) ++hi;
+            for (int e = ent + tid; e < hi; e += 32 * BY) {
+                const long long o = a.inj_off[e];
+                const float delta = a.inj_coef[e] * __ldg(a.inj_row + a.inj_pt[e]);
+                atomicAdd(a.out + o, delta);
+                if constexpr (GRAD)
+                    if (a.inj_gm[e]) atomicAdd(a.grad + o, a.nidt2 * __ldg(a.ut + o) * delta);
+            }
+            ent = hi;
+        }
+    };
+
+    if constexpr (ROT) {
+        for (int base = 0; base < n; base += Q) {
+            [&]<int... P>(std::integer_sequence<int, P...>) {
+                ((base + P < n ? (plane(IC<P>{}, base + P), true) : false) && ...);
+            }(std::make_integer_sequence<int, Q>{});
+        }
+    } else {
+        for (int i = 0; i < n; ++i) plane(IC<0>{}, i);
     }
 }
 
-template <int R, int BY, int NY, int S, bool GRAD>
+template <int R, int BY, int NY, int S, bool GRAD, bool ROT>
 cudaError_t launch3d_t(const FieldGeom& g, const SweepConfig& cfg, const SweepMaps& m,
                        const SweepArgs& a, cudaStream_t s) {
-    auto kern = sweep3d_kernel<R, BY, NY, S, GRAD>;
+    auto kern = sweep3d_kernel<R, BY, NY, S, GRAD, ROT>;
     const size_t smem = sweep3d_smem_bytes(R, cfg, GRAD);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
@@ -246,12 +344,16 @@ cudaError_t launch3d_t(const FieldGeom& g, const SweepConfig& cfg, const SweepMa
 template <int R, bool GRAD>
 cudaError_t launch3d_r(const FieldGeom& g, const SweepConfig& cfg, const SweepMaps& m,
                        const SweepArgs& a, cudaStream_t s) {
-    if (cfg.by == 4 && cfg.ny == 4 && cfg.stages == 4)
-        return launch3d_t<R, 4, 4, 4, GRAD>(g, cfg, m, a, s);
-    if (cfg.by == 8 && cfg.ny == 2 && cfg.stages == 4)
-        return launch3d_t<R, 8, 2, 4, GRAD>(g, cfg, m, a, s);
-    if (cfg.by == 4 && cfg.ny == 8 && cfg.stages == 3)
-        return launch3d_t<R, 4, 8, 3, GRAD>(g, cfg, m, a, s);
+    // (by, ny, stages, rot) variants compiled for every radius.
+    if (cfg.by == 4 && cfg.ny == 2 && cfg.stages == 4)
+        return cfg.rot ? launch3d_t<R, 4, 2, 4, GRAD, true>(g, cfg, m, a, s)
+                       : launch3d_t<R, 4, 2, 4, GRAD, false>(g, cfg, m, a, s);
+    if (cfg.by == 4 && cfg.ny == 1 && cfg.stages == 4)
+        return cfg.rot ? launch3d_t<R, 4, 1, 4, GRAD, true>(g, cfg, m, a, s)
+                       : launch3d_t<R, 4, 1, 4, GRAD, false>(g, cfg, m, a, s);
+    if (cfg.by == 8 && cfg.ny == 1 && cfg.stages == 3)
+        return cfg.rot ? launch3d_t<R, 8, 1, 3, GRAD, true>(g, cfg, m, a, s)
+                       : launch3d_t<R, 8, 1, 3, GRAD, false>(g, cfg, m, a, s);
     return cudaErrorInvalidConfiguration;
 }
 

@@ -42,6 +42,24 @@ struct SweepArgs {
     float w[kMaxRadius + 1];  // w_k / h^2
     float neg2nd;           // -2 * ndim
     float nidt2;            // -1 / dt^2
+
+    // Fused sparse operators (3-D sweep only; nullptr / 0 disables them).
+    // Sample: the previous step's row (this step's u1) is interpolated at the
+    // start of the launch, smp_per_cta points per CTA.
+    const long long* smp_off;
+    const float* smp_w;
+    float* smp_row;
+    int smp_n, smp_per_cta;
+    int corners;
+    // Inject into this step's output, per CTA (CSR over the linear CTA id),
+    // entries sorted by z and applied right after the owning plane is stored.
+    const int* inj_begin;
+    const int* inj_z;
+    const long long* inj_off;
+    const float* inj_coef;
+    const int* inj_pt;
+    const unsigned char* inj_gm;  // GRAD: corner inside the updated region
+    const float* inj_row;         // trace row of this step
 };
 
 struct SweepMaps {          // TMA descriptors (3-D only)
@@ -53,12 +71,14 @@ struct SweepMaps {          // TMA descriptors (3-D only)
 
 struct SweepConfig {        // 3-D tiling, chosen by choose_config()
     int by = 4;             // warps per CTA (each warp: 32 x-columns)
-    int ny = 4;             // y rows per thread
+    int ny = 2;             // y rows per thread in each tile half (tile is 2*by*ny rows)
     int stages = 4;         // TMA pipeline depth
+    int rot = 1;            // z loop unrolled by 2R+1 (register queue rotates by renaming)
     int zchunks = 1;        // CTAs along z per (x, y) tile
+    int zlen = 1;           // planes per z chunk
     int tiles_x = 0, tiles_y = 0;
     size_t smem_bytes = 0;
-    int ty() const { return by * ny; }
+    int ty() const { return 2 * by * ny; }
     int bw(int R) const { return 32 + 2 * ((R + 3) & ~3); }
 };
 

@@ -117,6 +117,24 @@ struct SparseDev {
     float* w = nullptr;          // w                     (sample)
     unsigned char* gmask = nullptr;  // corner inside the updated region
     float* trace = nullptr;      // [nt][n]
+    // Injection entries re-ordered per sweep CTA (3-D fused inject).
+    int* f_begin = nullptr;      // [ctas + 1]
+    int* f_z = nullptr;
+    long long* f_off = nullptr;
+    float* f_coef = nullptr;
+    int* f_pt = nullptr;
+    unsigned char* f_gm = nullptr;
+    int f_ctas = 0;
+    void free_fused() {
+        for (void* q : {(void*)f_begin, (void*)f_z, (void*)f_off, (void*)f_coef, (void*)f_pt,
+                        (void*)f_gm})
+            cudaFree(q);
+        f_begin = f_z = f_pt = nullptr;
+        f_off = nullptr;
+        f_coef = nullptr;
+        f_gm = nullptr;
+        f_ctas = 0;
+    }
 };
 
 }  // namespace
@@ -164,6 +182,7 @@ struct sfdb200_plan {
             cudaFree(s->w);
             cudaFree(s->gmask);
             cudaFree(s->trace);
+            s->free_fused();
         }
         cudaFree(staging);
         cudaFree(counter);
@@ -212,7 +231,7 @@ void choose_config(sfdb200_plan& p) {
     SweepConfig& c = p.cfg;
     const int R = p.g.R;
     if (const char* t = std::getenv("SFDB200_TILE")) {
-        std::sscanf(t, "%d,%d,%d", &c.by, &c.ny, &c.stages);
+        std::sscanf(t, "%d,%d,%d,%d", &c.by, &c.ny, &c.stages, &c.rot);
     }
     c.tiles_x = static_cast<int>((p.g.Px - R + 31) / 32);  // tiles start at x = 0 (TMA alignment)
     c.tiles_y = static_cast<int>((p.g.Py - 2 * R + c.ty() - 1) / c.ty());
@@ -227,6 +246,8 @@ void choose_config(sfdb200_plan& p) {
     zc = std::min(zc, std::max(1, zupd / (4 * R + 8)));
     c.zchunks = env_int("SFDB200_ZCHUNKS", zc);
     c.zchunks = std::max(1, std::min(c.zchunks, zupd));
+    c.zlen = (zupd + c.zchunks - 1) / c.zchunks;
+    c.zchunks = (zupd + c.zlen - 1) / c.zlen;  // no empty chunks
 }
 
 void build_maps(sfdb200_plan& p) {
@@ -301,6 +322,68 @@ void create(const sfdb200_desc& d, sfdb200_plan& p) {
     ck(cudaStreamSynchronize(p.stream), "plan setup");
 }
 
+// Injection entries grouped by the sweep CTA that stores their corner (tile
+// of the corner's (y, x), z chunk of its z), sorted by (z, point, corner) so a
+// CTA applies them plane by plane in the reference's (p, c) order.  Corners
+// the sweep never writes (halo cells) go to CTA 0's first plane.
+void build_fused(sfdb200_plan& p, SparseDev& s, const long* idx,
+                 const std::vector<long long>& off, const std::vector<float>& coef,
+                 const std::vector<unsigned char>& mask) {
+    const SweepConfig& c = p.cfg;
+    const int R = p.g.R, C = p.corners, TY = c.ty();
+    const int ctas = c.tiles_x * c.tiles_y * c.zchunks;
+    struct E { int cta, z; size_t i; };
+    std::vector<E> es;
+    es.reserve(off.size());
+    for (long q = 0; q < s.n; ++q)
+        for (int k = 0; k < C; ++k) {
+            const long z = idx[q * 3] + ((k >> 2) & 1), y = idx[q * 3 + 1] + ((k >> 1) & 1),
+                       x = idx[q * 3 + 2] + (k & 1);
+            const size_t i = static_cast<size_t>(q) * C + k;
+            const bool inside = z >= R && z < p.g.Pz - R && y >= R && y < p.g.Py - R &&
+                                x >= R && x < p.g.Px - R;
+            if (!inside) {
+                es.push_back({0, R, i});
+                continue;
+            }
+            const int bx = static_cast<int>(x / 32), by = static_cast<int>((y - R) / TY),
+                      bz = static_cast<int>((z - R) / c.zlen);
+            es.push_back({bx + c.tiles_x * (by + c.tiles_y * bz), static_cast<int>(z), i});
+        }
+    std::stable_sort(es.begin(), es.end(), [](const E& a, const E& b) {
+        return a.cta != b.cta ? a.cta < b.cta : a.z < b.z;
+    });
+    std::vector<int> begin(static_cast<size_t>(ctas) + 1, 0), ez(es.size()), ept(es.size());
+    std::vector<long long> eoff(es.size());
+    std::vector<float> ecoef(es.size());
+    std::vector<unsigned char> egm(es.size());
+    for (size_t j = 0; j < es.size(); ++j) {
+        ++begin[static_cast<size_t>(es[j].cta) + 1];
+        ez[j] = es[j].z;
+        eoff[j] = off[es[j].i];
+        ecoef[j] = coef[es[j].i];
+        ept[j] = static_cast<int>(es[j].i / C);
+        egm[j] = mask[es[j].i];
+    }
+    for (int j = 0; j < ctas; ++j) begin[static_cast<size_t>(j) + 1] += begin[static_cast<size_t>(j)];
+    s.free_fused();
+    s.f_ctas = ctas;
+    s.f_begin = dalloc<int>(begin.size());
+    s.f_z = dalloc<int>(ez.size());
+    s.f_off = dalloc<long long>(eoff.size());
+    s.f_coef = dalloc<float>(ecoef.size());
+    s.f_pt = dalloc<int>(ept.size());
+    s.f_gm = dalloc<unsigned char>(egm.size());
+    cudaStream_t st = p.stream;
+    ck(cudaMemcpyAsync(s.f_begin, begin.data(), begin.size() * 4, cudaMemcpyHostToDevice, st), "H2D");
+    ck(cudaMemcpyAsync(s.f_z, ez.data(), ez.size() * 4, cudaMemcpyHostToDevice, st), "H2D");
+    ck(cudaMemcpyAsync(s.f_off, eoff.data(), eoff.size() * 8, cudaMemcpyHostToDevice, st), "H2D");
+    ck(cudaMemcpyAsync(s.f_coef, ecoef.data(), ecoef.size() * 4, cudaMemcpyHostToDevice, st), "H2D");
+    ck(cudaMemcpyAsync(s.f_pt, ept.data(), ept.size() * 4, cudaMemcpyHostToDevice, st), "H2D");
+    ck(cudaMemcpyAsync(s.f_gm, egm.data(), egm.size(), cudaMemcpyHostToDevice, st), "H2D");
+    ck(cudaStreamSynchronize(st), "fused sparse upload");
+}
+
 // Host-side sparse tables: corner offsets in the device layout, inject
 // coefficients w*dt^2/m[corner] (the reference's v = w; v *= scale; v *= data;
 // v /= m, interpreter.cpp:144-147, with the data factor applied on device),
@@ -338,6 +421,7 @@ void upload_sparse(sfdb200_plan& p, SparseDev& s, const long* idx, const double*
     ck(cudaMemcpyAsync(s.coef, coef.data(), coef.size() * 4, cudaMemcpyHostToDevice, p.stream), "H2D");
     ck(cudaMemcpyAsync(s.w, w32.data(), w32.size() * 4, cudaMemcpyHostToDevice, p.stream), "H2D");
     ck(cudaMemcpyAsync(s.gmask, mask.data(), mask.size(), cudaMemcpyHostToDevice, p.stream), "H2D");
+    if (nd == 3) build_fused(p, s, idx, off, coef, mask);
     ck(cudaStreamSynchronize(p.stream), "sparse upload");
     p.h2d += static_cast<long>(s.n) * (nd * 8 + C * 8);
 }
@@ -461,6 +545,10 @@ void do_execute(sfdb200_plan& p) {
     SparseDev* smp = p.sampled();
     const bool fwd = d.kind == SFDB200_FORWARD;
     const bool save = fwd && d.save;
+    const bool fused = g.ndim == 3;  // 3-D: sparse ops ride inside the sweep launches
+    const int ctas = fused ? p.cfg.tiles_x * p.cfg.tiles_y * p.cfg.zchunks : 0;
+    long prev_srow = -1;             // sample row still owed by the previous step
+    const float* prev_out = nullptr;
     for (long i = 0; i < nsteps; ++i) {
         const long t = fwd ? 2 + i : d.nt - 1 - i;
         long r0, r1, r2;
@@ -485,25 +573,54 @@ void do_execute(sfdb200_plan& p) {
             a.grad = p.grad;
             a.row_ut = static_cast<int>(t);
         }
-        a.zchunk = (a.zhi - a.zlo + p.cfg.zchunks - 1) / std::max(1, p.cfg.zchunks);
+        a.zchunk = p.cfg.zlen;
+        a.corners = p.corners;
+        // Sparse section in list order, inject then sample (codegen.cpp:426-462):
+        // inject trace row t-1 (forward, trace_offset -1) or t (adjoint, gradient);
+        // sample rec row t (forward) or src row t-1 (adjoint).
+        const long irow = fwd ? t - 1 : t;
+        const long srow = fwd ? t : t - 1;
+        if (fused) {
+            if (inj.n) {
+                a.inj_begin = inj.f_begin;
+                a.inj_z = inj.f_z;
+                a.inj_off = inj.f_off;
+                a.inj_coef = inj.f_coef;
+                a.inj_pt = inj.f_pt;
+                a.inj_gm = inj.f_gm;
+                a.inj_row = inj.trace + irow * inj.n;
+            }
+            if (smp && smp->n && prev_srow >= 0) {  // previous step's row == this u1
+                a.smp_off = smp->off;
+                a.smp_w = smp->w;
+                a.smp_row = smp->trace + prev_srow * smp->n;
+                a.smp_n = static_cast<int>(smp->n);
+                a.smp_per_cta = static_cast<int>((smp->n + ctas - 1) / ctas);
+            }
+        }
         if (p.timing) ck(cudaEventRecord(p.events[2 * i], s), "event");
         sweep(p, a);
         if (p.timing) ck(cudaEventRecord(p.events[2 * i + 1], s), "event");
         ++p.timed_launches;
-        // Sparse section in list order: inject, then sample (codegen.cpp:426-462).
-        const long irow = fwd ? t - 1 : t;  // trace_offset -1 (forward) / 0 (adjoint, gradient)
-        if (inj.n)
-            ck(launch_inject(a.out, inj.off, inj.coef, inj.trace + irow * inj.n, inj.n, p.corners,
-                             p.grad, p.grad_kind() ? a.ut : nullptr, inj.gmask,
-                             p.base.nidt2, s),
-               "inject");
-        if (smp && smp->n) {
-            const long srow = fwd ? t : t - 1;  // rec row t (forward) / src row t-1 (adjoint)
-            ck(launch_sample(a.out, smp->off, smp->w, smp->trace + srow * smp->n, smp->n,
-                             p.corners, s),
-               "sample");
+        if (!fused) {
+            if (inj.n)
+                ck(launch_inject(a.out, inj.off, inj.coef, inj.trace + irow * inj.n, inj.n,
+                                 p.corners, p.grad, p.grad_kind() ? a.ut : nullptr, inj.gmask,
+                                 p.base.nidt2, s),
+                   "inject");
+            if (smp && smp->n)
+                ck(launch_sample(a.out, smp->off, smp->w, smp->trace + srow * smp->n, smp->n,
+                                 p.corners, s),
+                   "sample");
         }
+        prev_srow = srow;
+        prev_out = a.out;
     }
+    // The last step's samples have no following sweep to ride on.
+    if (fused && smp && smp->n && prev_out)
+        ck(launch_sample(prev_out, smp->off, smp->w, smp->trace + prev_srow * smp->n, smp->n,
+                         p.corners, s),
+           "sample");
     ck(cudaGetLastError(), "execute");
 }
 
@@ -677,13 +794,13 @@ int sfdb200_stencil_time(sfdb200_plan* p, double* total_ms, long* launches) {
 
 long sfdb200_launches_per_execute(const sfdb200_plan* p) {
     if (!p) return -1;
-    long per = 1;
     const SparseDev& inj = p->d.kind == SFDB200_FORWARD ? p->src : p->rec;
-    if (inj.n) ++per;
     const SparseDev* smp = p->d.kind == SFDB200_FORWARD ? &p->rec
                            : p->d.kind == SFDB200_ADJOINT ? &p->src : nullptr;
-    if (smp && smp->n) ++per;
-    return per * p->steps();
+    const bool has_smp = smp && smp->n;
+    if (p->g.ndim == 3)  // sparse ops fused into the sweep; one trailing sample
+        return p->steps() + (has_smp && p->steps() ? 1 : 0);
+    return (1 + (inj.n ? 1 : 0) + (has_smp ? 1 : 0)) * p->steps();
 }
 
 long sfdb200_points_per_step(const sfdb200_plan* p) {
