@@ -169,28 +169,30 @@ __global__ void __launch_bounds__(32 * BY)
     }
 
     const int cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
-    // Fused Sample of the previous step (its row is this launch's u1, complete
-    // since the previous launch): codegen.cpp:450-458, interpolation order
-    // c = 0..7.  Run after the first plane, while the TMA stages are in flight.
-    auto sample_prev = [&]() {
-        const int p0 = cta * a.smp_per_cta;
-        const int p1 = min(a.smp_n, p0 + a.smp_per_cta);
-        for (int p = p0 + tid; p < p1; p += 32 * BY) {
-            const long long* off = a.smp_off + 8LL * p;
-            const float* w = a.smp_w + 8LL * p;
-            float v[8];
-#pragma unroll
-            for (int c = 0; c < 8; ++c) v[c] = __ldg(a.u1 + __ldg(off + c));
-            float acc = 0.0f;
-#pragma unroll
-            for (int c = 0; c < 8; ++c) acc = fmaf(__ldg(w + c), v[c], acc);
-            a.smp_row[p] = acc;
-        }
+    // Plane ranges with fused sparse work: loaded once, so planes without
+    // sparse work (nearly all) never touch the tables.
+    const int* stab = a.smp_tab ? a.smp_tab + static_cast<long long>(cta) * (a.zchunk + 1) : nullptr;
+    const int* itab = a.inj_tab ? a.inj_tab + static_cast<long long>(cta) * (a.zchunk + 1) : nullptr;
+    const int2 srng = stab ? a.smp_rng[cta] : make_int2(0, 0);
+    const int2 irng = itab ? a.inj_rng[cta] : make_int2(0, 0);
+    // Warm L2 with this CTA's entry records so the planes that use them do
+    // not stall on DRAM latency.
+    auto prefetch = [&](const void* base, long long bytes) {
+        const char* b = static_cast<const char*>(base);
+        for (long long o = tid * 128LL; o < bytes; o += 32LL * BY * 128)
+            asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(b + o));
     };
-    int ent = 0, ent_end = 0;
-    if (a.inj_begin) {
-        ent = a.inj_begin[cta];
-        ent_end = a.inj_begin[cta + 1];
+    if (srng.y > srng.x) {
+        const int e0 = stab[srng.x], e1 = stab[srng.y];
+        prefetch(a.smp_hidx + e0, 4LL * (e1 - e0));
+        prefetch(a.smp_pt + e0, 4LL * (e1 - e0));
+        prefetch(a.smp_w + 8LL * e0, 32LL * (e1 - e0));
+    }
+    if (irng.y > irng.x) {
+        const int e0 = itab[irng.x], e1 = itab[irng.y];
+        prefetch(a.inj_off + e0, 8LL * (e1 - e0));
+        prefetch(a.inj_coef + e0, 4LL * (e1 - e0));
+        prefetch(a.inj_pt + e0, 4LL * (e1 - e0));
     }
 
     // Queue slot of plane zb - R + t is t mod Q.
@@ -292,27 +294,39 @@ __global__ void __launch_bounds__(32 * BY)
 #pragma unroll
                 for (int t = 0; t < 2 * R; ++t) q[j][t] = q[j][t + 1];
         }
+        // Fused Sample from the staged u1 plane (see SweepArgs): second halves
+        // of receivers based on the previous plane, first halves of those based here.
+        if (i >= srng.x && i < srng.y) {
+            const int e0 = i > 0 ? stab[i - 1] : stab[0], e1 = stab[i], e2 = stab[i + 1];
+            for (int e = e0 + tid; e < e2; e += 32 * BY) {
+                const float* hp = H + a.smp_hidx[e];
+                const float* w = a.smp_w + 8LL * e;
+                const int c0 = e < e1 ? 4 : 0;
+                float acc = e < e1 ? a.smp_acc[e] : 0.0f;
+                acc = fmaf(__ldg(w + c0 + 0), hp[0], acc);
+                acc = fmaf(__ldg(w + c0 + 1), hp[1], acc);
+                acc = fmaf(__ldg(w + c0 + 2), hp[T::BW], acc);
+                acc = fmaf(__ldg(w + c0 + 3), hp[T::BW + 1], acc);
+                if (e < e1) a.smp_row[a.smp_pt[e]] = acc;
+                else a.smp_acc[e] = acc;
+            }
+        }
         __syncthreads();
         if (tid == 0 && i + S < n) {
             fence_proxy_async();
             issue(st, zb + i + S);
         }
-        if (i == 0 && a.smp_n) sample_prev();
-        // Fused Inject into the plane just stored (codegen.cpp:436-449): the
-        // barrier above makes the plane's stores visible; colliding corners
-        // are summed with atomics.
-        if (ent < ent_end) {
-            const int z = zb + i;
-            int hi = ent;
-            while (hi < ent_end && __ldg(a.inj_z + hi) == z) ++hi;
-            for (int e = ent + tid; e < hi; e += 32 * BY) {
+        // Fused Inject (see SweepArgs): the barrier above made the plane's
+        // stores visible to the whole CTA.
+        if (i >= irng.x && i < irng.y) {
+            const int e0 = itab[i], e1 = itab[i + 1];
+            for (int e = e0 + tid; e < e1; e += 32 * BY) {
                 const long long o = a.inj_off[e];
                 const float delta = a.inj_coef[e] * __ldg(a.inj_row + a.inj_pt[e]);
                 atomicAdd(a.out + o, delta);
                 if constexpr (GRAD)
                     if (a.inj_gm[e]) atomicAdd(a.grad + o, a.nidt2 * __ldg(a.ut + o) * delta);
             }
-            ent = hi;
         }
     };
 
@@ -399,14 +413,24 @@ __global__ void inject_kernel(float* __restrict__ field, const long long* __rest
     if (grad && gmask[i]) atomicAdd(grad + o, nidt2 * ut[o] * delta);
 }
 
+template <int C>
 __global__ void sample_kernel(const float* __restrict__ field, const long long* __restrict__ off,
-                              const float* __restrict__ w, float* __restrict__ row, long n,
-                              int corners) {
+                              const float* __restrict__ w, const int* __restrict__ pt,
+                              float* __restrict__ row, long n, int corners) {
     const long p = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
     if (p >= n) return;
+    const int nc = C > 0 ? C : corners;
+    float v[C > 0 ? C : 8];
     float acc = 0.0f;
-    for (int c = 0; c < corners; ++c) acc = fmaf(w[p * corners + c], field[off[p * corners + c]], acc);
-    row[p] = acc;
+    if constexpr (C > 0) {
+#pragma unroll
+        for (int c = 0; c < C; ++c) v[c] = __ldg(field + __ldg(off + p * C + c));
+#pragma unroll
+        for (int c = 0; c < C; ++c) acc = fmaf(__ldg(w + p * C + c), v[c], acc);
+    } else {
+        for (int c = 0; c < nc; ++c) acc = fmaf(w[p * nc + c], field[off[p * nc + c]], acc);
+    }
+    row[pt ? pt[p] : p] = acc;
 }
 
 // ---------------------------------------------------------------- conversions
@@ -524,10 +548,16 @@ cudaError_t launch_inject(float* field, const long long* off, const float* coef,
     return cudaGetLastError();
 }
 
-cudaError_t launch_sample(const float* field, const long long* off, const float* w, float* row,
-                          long npoints, int corners, cudaStream_t s) {
+cudaError_t launch_sample(const float* field, const long long* off, const float* w,
+                          const int* pt, float* row, long npoints, int corners, cudaStream_t s) {
     if (npoints == 0) return cudaSuccess;
-    sample_kernel<<<grid_for(npoints, 256), 256, 0, s>>>(field, off, w, row, npoints, corners);
+    const unsigned grid = grid_for(npoints, 128);
+    if (corners == 8)
+        sample_kernel<8><<<grid, 128, 0, s>>>(field, off, w, pt, row, npoints, corners);
+    else if (corners == 4)
+        sample_kernel<4><<<grid, 128, 0, s>>>(field, off, w, pt, row, npoints, corners);
+    else
+        sample_kernel<0><<<grid, 128, 0, s>>>(field, off, w, pt, row, npoints, corners);
     return cudaGetLastError();
 }
 

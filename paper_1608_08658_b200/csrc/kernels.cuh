@@ -43,18 +43,25 @@ struct SweepArgs {
     float neg2nd;           // -2 * ndim
     float nidt2;            // -1 / dt^2
 
-    // Fused sparse operators (3-D sweep only; nullptr / 0 disables them).
-    // Sample: the previous step's row (this step's u1) is interpolated at the
-    // start of the launch, smp_per_cta points per CTA.
-    const long long* smp_off;
-    const float* smp_w;
-    float* smp_row;
-    int smp_n, smp_per_cta;
-    int corners;
-    // Inject into this step's output, per CTA (CSR over the linear CTA id),
-    // entries sorted by z and applied right after the owning plane is stored.
-    const int* inj_begin;
-    const int* inj_z;
+    // Fused sparse operators (3-D sweep only; nullptr disables them).  Both
+    // use per-CTA plane tables: entries of CTA c at its local plane i are
+    // [tab[c*(zchunk+1) + i], tab[c*(zchunk+1) + i + 1]).
+    //
+    // Sample the PREVIOUS step's row (= this launch's u1) straight from the
+    // staged halo plane in shared memory: corners c = 0..3 (plane z0) when z0
+    // is staged, c = 4..7 (plane z0 + 1) on the next plane, summed in the
+    // reference's order (codegen.cpp:450-458) through a per-entry scratch.
+    const int* smp_tab;
+    const int2* smp_rng;    // [cta] planes [x, y) that have sample work (one load per CTA)
+    const int* smp_hidx;    // halo-plane smem index of corner 0
+    const float* smp_w;     // [entry][8]
+    const int* smp_pt;      // receiver index
+    float* smp_acc;         // [entry] half sums
+    float* smp_row;         // trace row being sampled
+    // Inject into this step's output right after the owning plane is stored
+    // (codegen.cpp:436-449); colliding corners are summed with atomics.
+    const int* inj_tab;
+    const int2* inj_rng;    // [cta] planes [x, y) that have injections
     const long long* inj_off;
     const float* inj_coef;
     const int* inj_pt;
@@ -96,8 +103,9 @@ cudaError_t launch_inject(float* field, const long long* off, const float* coef,
                           const float* row, long npoints, int corners, float* grad,
                           const float* ut, const unsigned char* gmask, float nidt2,
                           cudaStream_t s);
-cudaError_t launch_sample(const float* field, const long long* off, const float* w, float* row,
-                          long npoints, int corners, cudaStream_t s);
+// pt (optional): output index of each sampled point (a subset of the set).
+cudaError_t launch_sample(const float* field, const long long* off, const float* w,
+                          const int* pt, float* row, long npoints, int corners, cudaStream_t s);
 
 // Format conversion between the reference's dense fp64 layout and the device
 // fp32 pitched layout.

@@ -117,24 +117,37 @@ struct SparseDev {
     float* w = nullptr;          // w                     (sample)
     unsigned char* gmask = nullptr;  // corner inside the updated region
     float* trace = nullptr;      // [nt][n]
-    // Injection entries re-ordered per sweep CTA (3-D fused inject).
-    int* f_begin = nullptr;      // [ctas + 1]
-    int* f_z = nullptr;
+    // 3-D fused operators: device buffers owned by this set, freed together.
+    std::vector<void*> fused_bufs;
+    // Inject entries per (sweep CTA, plane): table + entry arrays.
+    int* f_tab = nullptr;
+    int2* f_rng = nullptr;
     long long* f_off = nullptr;
     float* f_coef = nullptr;
     int* f_pt = nullptr;
     unsigned char* f_gm = nullptr;
-    int f_ctas = 0;
+    // Sample entries per (sweep CTA, base plane), read from the staged plane.
+    int* s_tab = nullptr;
+    int2* s_rng = nullptr;
+    int* s_hidx = nullptr;
+    float* s_w = nullptr;
+    int* s_pt = nullptr;
+    float* s_acc = nullptr;
+    // Receivers no sweep CTA can sample (corner planes split across z chunks,
+    // or halo cells): sampled by sample_kernel after the sweep.
+    long fb_n = 0;
+    long long* fb_off = nullptr;
+    float* fb_w = nullptr;
+    int* fb_pt = nullptr;
     void free_fused() {
-        for (void* q : {(void*)f_begin, (void*)f_z, (void*)f_off, (void*)f_coef, (void*)f_pt,
-                        (void*)f_gm})
-            cudaFree(q);
-        f_begin = f_z = f_pt = nullptr;
-        f_off = nullptr;
-        f_coef = nullptr;
-        f_gm = nullptr;
-        f_ctas = 0;
+        for (void* q : fused_bufs) cudaFree(q);
+        fused_bufs.clear();
+        f_tab = nullptr; f_rng = nullptr; f_off = nullptr; f_coef = nullptr; f_pt = nullptr; f_gm = nullptr;
+        s_tab = nullptr; s_rng = nullptr; s_hidx = nullptr; s_w = nullptr; s_pt = nullptr; s_acc = nullptr;
+        fb_n = 0; fb_off = nullptr; fb_w = nullptr; fb_pt = nullptr;
     }
+    template <class T>
+    T* upload(const std::vector<T>& v, cudaStream_t st);
 };
 
 }  // namespace
@@ -299,6 +312,7 @@ void create(const sfdb200_desc& d, sfdb200_plan& p) {
     ck(cudaStreamCreateWithFlags(&p.own_stream, cudaStreamNonBlocking), "cudaStreamCreate");
     p.stream = p.own_stream;
 
+
     p.field = dalloc<float>(static_cast<size_t>(p.rows * g.slot));
     p.c1 = dalloc<float>(static_cast<size_t>(g.slot));
     p.c2 = dalloc<float>(static_cast<size_t>(g.slot));
@@ -322,66 +336,162 @@ void create(const sfdb200_desc& d, sfdb200_plan& p) {
     ck(cudaStreamSynchronize(p.stream), "plan setup");
 }
 
-// Injection entries grouped by the sweep CTA that stores their corner (tile
-// of the corner's (y, x), z chunk of its z), sorted by (z, point, corner) so a
-// CTA applies them plane by plane in the reference's (p, c) order.  Corners
-// the sweep never writes (halo cells) go to CTA 0's first plane.
-void build_fused(sfdb200_plan& p, SparseDev& s, const long* idx,
-                 const std::vector<long long>& off, const std::vector<float>& coef,
-                 const std::vector<unsigned char>& mask) {
+template <class T>
+T* SparseDev::upload(const std::vector<T>& v, cudaStream_t st) {
+    if (v.empty()) return nullptr;
+    T* d = dalloc<T>(v.size());
+    fused_bufs.push_back(d);
+    ck(cudaMemcpyAsync(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st), "H2D");
+    return d;
+}
+
+// Sweep CTA (static grid: x tiles fastest, then y tiles, then z chunks) and
+// its local plane index for a point of the updated region.
+struct Owner {
+    int cta, plane;
+};
+
+Owner owner_of(const sfdb200_plan& p, long z, long y, long x) {
     const SweepConfig& c = p.cfg;
-    const int R = p.g.R, C = p.corners, TY = c.ty();
-    const int ctas = c.tiles_x * c.tiles_y * c.zchunks;
-    struct E { int cta, z; size_t i; };
+    const int R = p.g.R;
+    const int bx = static_cast<int>(x / 32), by = static_cast<int>((y - R) / c.ty()),
+              bz = static_cast<int>((z - R) / c.zlen);
+    return {bx + c.tiles_x * (by + c.tiles_y * bz), static_cast<int>(z - R - bz * c.zlen)};
+}
+
+// Per CTA, the plane range [lo, hi + extra) holding entries (extra = 1 for
+// samples, whose second half comes one plane later); empty ranges are (0, 0).
+std::vector<int2> plane_ranges(const sfdb200_plan& p, const std::vector<int>& tab, int extra) {
+    const int ctas = p.cfg.tiles_x * p.cfg.tiles_y * p.cfg.zchunks, L = p.cfg.zlen + 1;
+    std::vector<int2> r(static_cast<size_t>(ctas), make_int2(0, 0));
+    for (int c = 0; c < ctas; ++c) {
+        const int* t = tab.data() + static_cast<size_t>(c) * L;
+        int lo = -1, hi = -1;
+        for (int i = 0; i + 1 < L; ++i)
+            if (t[i + 1] > t[i]) {
+                if (lo < 0) lo = i;
+                hi = i;
+            }
+        if (lo >= 0) r[static_cast<size_t>(c)] = make_int2(lo, std::min(hi + 1 + extra, L - 1));
+    }
+    return r;
+}
+
+// Per-CTA plane table over entries sorted by (cta, plane).
+std::vector<int> plane_table(const sfdb200_plan& p, const std::vector<Owner>& keys) {
+    const int ctas = p.cfg.tiles_x * p.cfg.tiles_y * p.cfg.zchunks, L = p.cfg.zlen + 1;
+    std::vector<int> tab(static_cast<size_t>(ctas) * L, 0);
+    size_t e = 0;
+    for (int c = 0; c < ctas; ++c)
+        for (int i = 0; i < L; ++i) {
+            while (e < keys.size() &&
+                   (keys[e].cta < c || (keys[e].cta == c && keys[e].plane < i)))
+                ++e;
+            tab[static_cast<size_t>(c) * L + i] = static_cast<int>(e);
+        }
+    return tab;
+}
+
+// Injection entries grouped by the sweep CTA that stores their corner, in
+// (plane, point, corner) order so each plane's injections follow the
+// reference's (p, c) order.  Corners the sweep never writes (halo cells) go to
+// CTA 0's first plane.
+void build_inject(sfdb200_plan& p, SparseDev& s, const long* idx,
+                  const std::vector<long long>& off, const std::vector<float>& coef,
+                  const std::vector<unsigned char>& mask) {
+    const int R = p.g.R, C = p.corners;
+    struct E { Owner o; size_t i; };
     std::vector<E> es;
-    es.reserve(off.size());
     for (long q = 0; q < s.n; ++q)
         for (int k = 0; k < C; ++k) {
             const long z = idx[q * 3] + ((k >> 2) & 1), y = idx[q * 3 + 1] + ((k >> 1) & 1),
                        x = idx[q * 3 + 2] + (k & 1);
-            const size_t i = static_cast<size_t>(q) * C + k;
             const bool inside = z >= R && z < p.g.Pz - R && y >= R && y < p.g.Py - R &&
                                 x >= R && x < p.g.Px - R;
-            if (!inside) {
-                es.push_back({0, R, i});
-                continue;
-            }
-            const int bx = static_cast<int>(x / 32), by = static_cast<int>((y - R) / TY),
-                      bz = static_cast<int>((z - R) / c.zlen);
-            es.push_back({bx + c.tiles_x * (by + c.tiles_y * bz), static_cast<int>(z), i});
+            es.push_back({inside ? owner_of(p, z, y, x) : Owner{0, 0},
+                          static_cast<size_t>(q) * C + k});
         }
     std::stable_sort(es.begin(), es.end(), [](const E& a, const E& b) {
-        return a.cta != b.cta ? a.cta < b.cta : a.z < b.z;
+        return a.o.cta != b.o.cta ? a.o.cta < b.o.cta : a.o.plane < b.o.plane;
     });
-    std::vector<int> begin(static_cast<size_t>(ctas) + 1, 0), ez(es.size()), ept(es.size());
-    std::vector<long long> eoff(es.size());
-    std::vector<float> ecoef(es.size());
-    std::vector<unsigned char> egm(es.size());
-    for (size_t j = 0; j < es.size(); ++j) {
-        ++begin[static_cast<size_t>(es[j].cta) + 1];
-        ez[j] = es[j].z;
-        eoff[j] = off[es[j].i];
-        ecoef[j] = coef[es[j].i];
-        ept[j] = static_cast<int>(es[j].i / C);
-        egm[j] = mask[es[j].i];
+    std::vector<Owner> keys;
+    std::vector<long long> eoff;
+    std::vector<float> ecoef;
+    std::vector<int> ept;
+    std::vector<unsigned char> egm;
+    for (const E& e : es) {
+        keys.push_back(e.o);
+        eoff.push_back(off[e.i]);
+        ecoef.push_back(coef[e.i]);
+        ept.push_back(static_cast<int>(e.i / C));
+        egm.push_back(mask[e.i]);
     }
-    for (int j = 0; j < ctas; ++j) begin[static_cast<size_t>(j) + 1] += begin[static_cast<size_t>(j)];
-    s.free_fused();
-    s.f_ctas = ctas;
-    s.f_begin = dalloc<int>(begin.size());
-    s.f_z = dalloc<int>(ez.size());
-    s.f_off = dalloc<long long>(eoff.size());
-    s.f_coef = dalloc<float>(ecoef.size());
-    s.f_pt = dalloc<int>(ept.size());
-    s.f_gm = dalloc<unsigned char>(egm.size());
     cudaStream_t st = p.stream;
-    ck(cudaMemcpyAsync(s.f_begin, begin.data(), begin.size() * 4, cudaMemcpyHostToDevice, st), "H2D");
-    ck(cudaMemcpyAsync(s.f_z, ez.data(), ez.size() * 4, cudaMemcpyHostToDevice, st), "H2D");
-    ck(cudaMemcpyAsync(s.f_off, eoff.data(), eoff.size() * 8, cudaMemcpyHostToDevice, st), "H2D");
-    ck(cudaMemcpyAsync(s.f_coef, ecoef.data(), ecoef.size() * 4, cudaMemcpyHostToDevice, st), "H2D");
-    ck(cudaMemcpyAsync(s.f_pt, ept.data(), ept.size() * 4, cudaMemcpyHostToDevice, st), "H2D");
-    ck(cudaMemcpyAsync(s.f_gm, egm.data(), egm.size(), cudaMemcpyHostToDevice, st), "H2D");
-    ck(cudaStreamSynchronize(st), "fused sparse upload");
+    const std::vector<int> tab = plane_table(p, keys);
+    s.f_tab = s.upload(tab, st);
+    s.f_rng = s.upload(plane_ranges(p, tab, 0), st);
+    s.f_off = s.upload(eoff, st);
+    s.f_coef = s.upload(ecoef, st);
+    s.f_pt = s.upload(ept, st);
+    s.f_gm = s.upload(egm, st);
+}
+
+// Sample entries: a receiver whose base corner (z0, y, x) lies in a sweep
+// CTA's tile with both planes z0, z0+1 in that CTA's z chunk is read from the
+// staged halo plane (all its x/y corners are inside tile + halo).
+void build_sample(sfdb200_plan& p, SparseDev& s, const long* idx,
+                  const std::vector<long long>& off, const std::vector<float>& w32) {
+    const int R = p.g.R, RA = (R + 3) & ~3, BW = p.cfg.bw(R), C = p.corners;
+    struct E { Owner o; int hidx; long q; };
+    std::vector<E> es;
+    std::vector<long long> fb_off;
+    std::vector<float> fb_w;
+    std::vector<int> fb_pt;
+    for (long q = 0; q < s.n; ++q) {
+        const long z = idx[q * 3], y = idx[q * 3 + 1], x = idx[q * 3 + 2];
+        bool ok = z >= R && z + 1 < p.g.Pz - R && y >= R && y < p.g.Py - R && x >= 0 &&
+                  x < 32L * p.cfg.tiles_x;
+        Owner o{0, 0};
+        if (ok) {
+            o = owner_of(p, z, y, x);
+            ok = o.plane + 1 < p.cfg.zlen && z + 1 < p.g.Pz - R;  // z0 + 1 in the same chunk
+        }
+        if (ok) {
+            const int y0 = R + ((static_cast<int>(y) - R) / p.cfg.ty()) * p.cfg.ty();
+            const int x0 = (static_cast<int>(x) / 32) * 32;
+            es.push_back({o, (static_cast<int>(y) - y0 + R) * BW + (static_cast<int>(x) - x0 + RA), q});
+        } else {
+            for (int k = 0; k < C; ++k) {
+                fb_off.push_back(off[static_cast<size_t>(q) * C + k]);
+                fb_w.push_back(w32[static_cast<size_t>(q) * C + k]);
+            }
+            fb_pt.push_back(static_cast<int>(q));
+        }
+    }
+    std::stable_sort(es.begin(), es.end(), [](const E& a, const E& b) {
+        return a.o.cta != b.o.cta ? a.o.cta < b.o.cta : a.o.plane < b.o.plane;
+    });
+    std::vector<Owner> keys;
+    std::vector<int> hidx, pt;
+    std::vector<float> w8;
+    for (const E& e : es) {
+        keys.push_back(e.o);
+        hidx.push_back(e.hidx);
+        pt.push_back(static_cast<int>(e.q));
+        for (int k = 0; k < C; ++k) w8.push_back(w32[static_cast<size_t>(e.q) * C + k]);
+    }
+    cudaStream_t st = p.stream;
+    const std::vector<int> tab = plane_table(p, keys);
+    s.s_tab = s.upload(tab, st);
+    s.s_rng = s.upload(plane_ranges(p, tab, 1), st);
+    s.s_hidx = s.upload(hidx, st);
+    s.s_w = s.upload(w8, st);
+    s.s_pt = s.upload(pt, st);
+    s.s_acc = s.upload(std::vector<float>(es.size(), 0.0f), st);
+    s.fb_n = static_cast<long>(fb_pt.size());
+    s.fb_off = s.upload(fb_off, st);
+    s.fb_w = s.upload(fb_w, st);
+    s.fb_pt = s.upload(fb_pt, st);
 }
 
 // Host-side sparse tables: corner offsets in the device layout, inject
@@ -421,7 +531,11 @@ void upload_sparse(sfdb200_plan& p, SparseDev& s, const long* idx, const double*
     ck(cudaMemcpyAsync(s.coef, coef.data(), coef.size() * 4, cudaMemcpyHostToDevice, p.stream), "H2D");
     ck(cudaMemcpyAsync(s.w, w32.data(), w32.size() * 4, cudaMemcpyHostToDevice, p.stream), "H2D");
     ck(cudaMemcpyAsync(s.gmask, mask.data(), mask.size(), cudaMemcpyHostToDevice, p.stream), "H2D");
-    if (nd == 3) build_fused(p, s, idx, off, coef, mask);
+    if (nd == 3) {
+        s.free_fused();
+        if (&s == &p.injected()) build_inject(p, s, idx, off, coef, mask);
+        if (&s == p.sampled()) build_sample(p, s, idx, off, w32);
+    }
     ck(cudaStreamSynchronize(p.stream), "sparse upload");
     p.h2d += static_cast<long>(s.n) * (nd * 8 + C * 8);
 }
@@ -543,11 +657,13 @@ void do_execute(sfdb200_plan& p) {
 
     SparseDev& inj = p.injected();
     SparseDev* smp = p.sampled();
+    if (smp && smp->n == 0) smp = nullptr;
     const bool fwd = d.kind == SFDB200_FORWARD;
     const bool save = fwd && d.save;
-    const bool fused = g.ndim == 3;  // 3-D: sparse ops ride inside the sweep launches
-    const int ctas = fused ? p.cfg.tiles_x * p.cfg.tiles_y * p.cfg.zchunks : 0;
-    long prev_srow = -1;             // sample row still owed by the previous step
+    // 3-D: the sparse operators ride inside the sweep launches;
+    // SFDB200_UNFUSED=1 runs them as their own kernels (A/B measurements).
+    const bool fused = g.ndim == 3 && !env_int("SFDB200_UNFUSED", 0);
+    long prev_srow = -1;
     const float* prev_out = nullptr;
     for (long i = 0; i < nsteps; ++i) {
         const long t = fwd ? 2 + i : d.nt - 1 - i;
@@ -574,29 +690,29 @@ void do_execute(sfdb200_plan& p) {
             a.row_ut = static_cast<int>(t);
         }
         a.zchunk = p.cfg.zlen;
-        a.corners = p.corners;
+
         // Sparse section in list order, inject then sample (codegen.cpp:426-462):
         // inject trace row t-1 (forward, trace_offset -1) or t (adjoint, gradient);
         // sample rec row t (forward) or src row t-1 (adjoint).
         const long irow = fwd ? t - 1 : t;
         const long srow = fwd ? t : t - 1;
-        if (fused) {
-            if (inj.n) {
-                a.inj_begin = inj.f_begin;
-                a.inj_z = inj.f_z;
-                a.inj_off = inj.f_off;
-                a.inj_coef = inj.f_coef;
-                a.inj_pt = inj.f_pt;
-                a.inj_gm = inj.f_gm;
-                a.inj_row = inj.trace + irow * inj.n;
-            }
-            if (smp && smp->n && prev_srow >= 0) {  // previous step's row == this u1
-                a.smp_off = smp->off;
-                a.smp_w = smp->w;
-                a.smp_row = smp->trace + prev_srow * smp->n;
-                a.smp_n = static_cast<int>(smp->n);
-                a.smp_per_cta = static_cast<int>((smp->n + ctas - 1) / ctas);
-            }
+        if (fused && inj.n) {
+            a.inj_tab = inj.f_tab;
+            a.inj_rng = inj.f_rng;
+            a.inj_off = inj.f_off;
+            a.inj_coef = inj.f_coef;
+            a.inj_pt = inj.f_pt;
+            a.inj_gm = inj.f_gm;
+            a.inj_row = inj.trace + irow * inj.n;
+        }
+        if (fused && smp && prev_srow >= 0 && smp->s_tab) {  // previous row == this u1
+            a.smp_tab = smp->s_tab;
+            a.smp_rng = smp->s_rng;
+            a.smp_hidx = smp->s_hidx;
+            a.smp_w = smp->s_w;
+            a.smp_pt = smp->s_pt;
+            a.smp_acc = smp->s_acc;
+            a.smp_row = smp->trace + prev_srow * smp->n;
         }
         if (p.timing) ck(cudaEventRecord(p.events[2 * i], s), "event");
         sweep(p, a);
@@ -608,18 +724,22 @@ void do_execute(sfdb200_plan& p) {
                                  p.corners, p.grad, p.grad_kind() ? a.ut : nullptr, inj.gmask,
                                  p.base.nidt2, s),
                    "inject");
-            if (smp && smp->n)
-                ck(launch_sample(a.out, smp->off, smp->w, smp->trace + srow * smp->n, smp->n,
-                                 p.corners, s),
+            if (smp)
+                ck(launch_sample(a.out, smp->off, smp->w, nullptr, smp->trace + srow * smp->n,
+                                 smp->n, p.corners, s),
                    "sample");
+        } else if (smp && smp->fb_n) {  // receivers no sweep CTA can sample
+            ck(launch_sample(a.out, smp->fb_off, smp->fb_w, smp->fb_pt,
+                             smp->trace + srow * smp->n, smp->fb_n, p.corners, s),
+               "sample");
         }
         prev_srow = srow;
         prev_out = a.out;
     }
-    // The last step's samples have no following sweep to ride on.
-    if (fused && smp && smp->n && prev_out)
-        ck(launch_sample(prev_out, smp->off, smp->w, smp->trace + prev_srow * smp->n, smp->n,
-                         p.corners, s),
+    // The last step's row has no following sweep to be sampled in.
+    if (fused && smp && prev_out && smp->s_tab)
+        ck(launch_sample(prev_out, smp->off, smp->w, nullptr, smp->trace + prev_srow * smp->n,
+                         smp->n, p.corners, s),
            "sample");
     ck(cudaGetLastError(), "execute");
 }
@@ -798,8 +918,9 @@ long sfdb200_launches_per_execute(const sfdb200_plan* p) {
     const SparseDev* smp = p->d.kind == SFDB200_FORWARD ? &p->rec
                            : p->d.kind == SFDB200_ADJOINT ? &p->src : nullptr;
     const bool has_smp = smp && smp->n;
-    if (p->g.ndim == 3)  // sparse ops fused into the sweep; one trailing sample
-        return p->steps() + (has_smp && p->steps() ? 1 : 0);
+    if (p->g.ndim == 3)  // sparse ops fused into the sweeps (+ fallback and final sample)
+        return p->steps() * (1 + (has_smp && smp->fb_n ? 1 : 0)) +
+               (has_smp && p->steps() ? 1 : 0);
     return (1 + (inj.n ? 1 : 0) + (has_smp ? 1 : 0)) * p->steps();
 }
 

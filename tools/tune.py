@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--tiles", default="4,2,4,1;4,2,4,0;4,1,4,1;8,1,3,1")
     ap.add_argument("--zchunks", default="0")
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--no-rec", action="store_true")
     args = ap.parse_args()
 
     import torch
@@ -27,6 +28,8 @@ def main():
     from paper_1608_08658_b200 import _lib as L
 
     w = bench.make_workload(args.workload, args.time_steps)
+    if args.no_rec:
+        w.rec_coords = w.rec_coords[:0]
     model, src, rec = bench.problem(w)
     argv = [np.empty((3, *model.padded)), L.f64(model.m), L.f64(model.damp), L.i64(src.idx),
             L.f64(src.w), L.f64(w.wavelet), L.i64(rec.idx), L.f64(rec.w),
@@ -50,9 +53,15 @@ def main():
                 ms, n = plan.stencil_time()
                 best = ms / n if best is None else min(best, ms / n)
             plan.set_timing(False)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            plan.execute()
+            e1.record()
+            torch.cuda.synchronize()
+            step_ms = e0.elapsed_time(e1) / plan.steps
             gbs = 20 * plan.points_per_step / (best / 1e3) / 1e9
             print(json.dumps({"workload": w.name, "tile": tile, "zchunks": zc,
-                              "sweep_ms": best, "gpts": plan.points_per_step / best / 1e6,
+                              "sweep_ms": best, "step_ms": step_ms, "env_unfused": os.environ.get("SFDB200_UNFUSED", "0"), "gpts": plan.points_per_step / best / 1e6,
                               "alg_GBps": gbs}), flush=True)
             plan.close()
 
