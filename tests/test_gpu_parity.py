@@ -107,3 +107,86 @@ def test_scattered_points_forward_and_adjoint():
                      src.idx, src.w, rec.idx, rec.w, resid)
     assert O.rel_l2(a.v, v) <= TOL
     assert O.rel_l2(a.src_samples.data, s) <= TOL
+
+
+GOLD = O.os.path.join(O.ROOT, "tests", "golden")
+
+
+@pytest.mark.parametrize("name", ["ref_2d_so4.npz", "ref_3d_so8.npz"])
+def test_operators_match_reference_fixtures(name):
+    """Direct comparison with the unmodified reference's outputs."""
+    g = np.load(O.os.path.join(GOLD, name))
+    nt, dt = int(g["nt"]), float(g["dt"])
+    model = S.make_model(list(g["interior"]), float(g["h"]), int(g["nbpml"]), int(g["so"]),
+                         g["m_interior"])
+    src = S.locate_points(model, g["src_coords"])
+    rec = S.locate_points(model, g["rec_coords"])
+    f = S.forward(model, src, g["wavelet"], rec, nt, dt, False)
+    assert O.rel_l2(f.record.data, g["rec"]) <= TOL
+    if "u" in g:
+        assert O.rel_l2(f.u, g["u"]) <= TOL
+    else:
+        assert O.rel_l2(f.u[(nt - 1) % 3], g["u_last"]) <= TOL
+    res = S.ShotRecord(nt, dt, rec.npoints, g["residual"])
+    a = S.adjoint(model, rec, res, src, nt, dt)
+    assert O.rel_l2(a.src_samples.data, g["src_samples"]) <= TOL
+    fs = S.forward(model, src, g["wavelet"], rec, nt, dt, True)
+    gr = S.gradient(model, rec, res, fs.u, nt, dt)
+    assert O.rel_l2(gr.grad, g["grad"]) <= TOL
+
+
+def test_adjoint_dot_product_fp32():
+    """verify.cpp:123-177 with the fp64 1e-10 bar relaxed for fp32."""
+    w = configs.cfg2(n=40, nt=202, nbpml=12, nrec_side=6)
+    model, src, rec = _setup(w)
+    rng = np.random.default_rng(1)
+    x = O._f64(rng.standard_normal((w.nt, 1)).astype(np.float32))
+    y = O._f64(rng.standard_normal((w.nt, rec.npoints)).astype(np.float32))
+    f = S.forward(model, src, x, rec, w.nt, w.dt, False)
+    a = S.adjoint(model, rec, S.ShotRecord(w.nt, w.dt, rec.npoints, y), src, w.nt, w.dt)
+    lhs, rhs = float((f.record.data * y).sum()), float((x * a.src_samples.data).sum())
+    assert abs(lhs - rhs) / abs(lhs) < 1e-5
+
+
+def test_zero_source_and_saved_vs_rolling():
+    """test_seismic.cpp:173-188, :220-241 on the device."""
+    w = configs.cfg2(n=32, nt=92, nbpml=10, nrec_side=6)
+    model, src, rec = _setup(w)
+    z = S.forward(model, src, np.zeros_like(w.wavelet), rec, w.nt, w.dt, False)
+    assert not z.u.any() and not z.record.data.any()
+    za = S.adjoint(model, rec, S.zero_record(w.nt, w.dt, rec.npoints), src, w.nt, w.dt)
+    assert not za.v.any() and not za.src_samples.data.any()
+    roll = S.forward(model, src, w.wavelet, rec, w.nt, w.dt, False)
+    sav = S.forward(model, src, w.wavelet, rec, w.nt, w.dt, True)
+    assert np.array_equal(roll.record.data, sav.record.data)
+    for t in range(w.nt - 3, w.nt):
+        assert np.array_equal(sav.u[t], roll.u[t % 3])
+    gz = S.gradient(model, rec, S.zero_record(w.nt, w.dt, rec.npoints), sav.u, w.nt, w.dt)
+    assert not gz.grad.any()
+
+
+def test_reference_abi_call_with_argv():
+    """sfdb200_call(desc, argv): the `<Name>_call(void **argv)` drop-in with the
+    reference's argv order (codegen.cpp:247-265), trailing block sizes ignored."""
+    from paper_1608_08658_b200 import _lib as L
+    w = configs.cfg2(n=24, nt=62, nbpml=8, nrec_side=4)
+    model, src, rec = _setup(w)
+    u = np.full((3, *model.padded), 7.0)  # garbage: first touch must zero it
+    rec_data = np.full((w.nt, rec.npoints), 3.0)
+    blocks = np.array([8, 8], dtype=np.int64)
+    argv = [u, model.m, model.damp, src.idx, src.w, O._f64(w.wavelet), rec.idx, rec.w, rec_data,
+            blocks[:1], blocks[1:]]
+    L.call(L.FORWARD, 3, model.padded, w.space_order, w.nt, w.dt, w.h, src.npoints,
+           rec.npoints, False, argv)
+    uo, ro = _oracle_forward(w, model, src, rec)
+    assert O.rel_l2(u, uo) <= TOL and O.rel_l2(rec_data, ro) <= TOL
+    # a second call reuses the cached plan
+    L.call(L.FORWARD, 3, model.padded, w.space_order, w.nt, w.dt, w.h, src.npoints,
+           rec.npoints, False, argv)
+    assert O.rel_l2(rec_data, ro) <= TOL
+    bad = src.idx.copy()
+    bad[0, 0] = model.padded[0]  # corner outside the padded grid
+    with pytest.raises(ValueError):
+        L.call(L.FORWARD, 3, model.padded, w.space_order, w.nt, w.dt, w.h, src.npoints,
+               rec.npoints, False, [u, model.m, model.damp, bad, src.w, O._f64(w.wavelet),
+                                    rec.idx, rec.w, rec_data])
