@@ -92,7 +92,9 @@ def config_of(w, n, extra=None):
                      f"{len(w.src_coords)} src, {len(w.rec_coords)} rec",
          "padded": w.padded, "space_order": w.space_order, "time_steps": w.steps,
          "points_per_step": w.points_per_step, "nsrc": len(w.src_coords),
-         "nrec": len(w.rec_coords), "parallelism": f"replicas x{n}" if n > 1 else "1 GPU",
+         "nrec": len(w.rec_coords),
+         "parallelism": f"z-slab x{n} (NCCL ghost exchange overlapped with the interior sweep)"
+                        if n > 1 else "1 GPU",
          "l2": "inputs larger than L2 (each fp32 field 4*prod(padded) B > 126 MB)"
                if 4 * int(np.prod(w.padded)) > 126e6 else "working set fits L2"}
     if extra:
@@ -225,16 +227,22 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dist = None
+    comm = None
     if world > 1:
+        # torch.distributed is the plumbing (rendezvous, barriers, the max over
+        # ranks); the ghost exchange runs on libsfdb200's own NCCL communicator.
         import torch.distributed as dist
-        dist.init_process_group("nccl")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        uid = [L.Comm.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = L.Comm(uid[0], world, rank, local)
 
     w = make_workload(args.workload, args.time_steps)
     model, src, rec = problem(w)
     S.check_dt(model, w.dt)
     nd = model.ndim()
     plan = L.Plan(L.FORWARD, nd, model.padded, w.space_order, w.nt, w.dt, w.h, src.npoints,
-                  rec.npoints, False, local)
+                  rec.npoints, False, local, comm=comm)
     stream = torch.cuda.Stream()
     plan.set_stream(stream.cuda_stream)
 
@@ -275,8 +283,8 @@ def run_ours(args):
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    pts = plan.points_per_step * plan.steps
-    value = pts * args.steps * world / (ms / 1e3) / 1e9
+    pts = w.points_per_step * plan.steps  # the global problem (strong scaling over z slabs)
+    value = pts * args.steps / (ms / 1e3) / 1e9
     launches = plan.launches_per_execute * args.steps
 
     # ---- end to end through the C ABI with host buffers (e2e)
@@ -294,14 +302,20 @@ def run_ours(args):
             t = torch.tensor([el], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             el = float(t.item())
-        e2e = {"value": pts * args.steps * world / el / 1e9, "unit": "Gpts/s",
+        e2e = {"value": pts * args.steps / el / 1e9, "unit": "Gpts/s",
                "h2d_bytes_per_step": plan.h2d_bytes, "d2h_bytes_per_step": plan.d2h_bytes,
                "ms_per_step": el / args.steps * 1e3,
                "path": "sfdb200_run(plan, argv): reference argv, pinned fp64 host buffers"}
 
     peak, peak_src = measured_peak()
     per_launch_ms = sweep_ms / max(1, sweep_n)
-    alg = BYTES_PER_POINT["forward"] * plan.points_per_step
+    # the timed launch is the (interior) sweep over this rank's slab
+    zb, ze, _ = plan.slab()
+    interior = plan.points_per_step
+    if world > 1:
+        R = w.space_order // 2
+        interior = plan.points_per_step // (ze - zb) * ((ze - zb) - R * ((rank > 0) + (rank < world - 1)))
+    alg = BYTES_PER_POINT["forward"] * interior
     achieved = alg / (per_launch_ms / 1e3) / 1e9
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": ncu_traffic(w.name),
@@ -317,12 +331,15 @@ def run_ours(args):
     if rank == 0:
         line = {"metric": "Gpts/s (grid-point updates/sec) 3D acoustic so-8", "value": value,
                 "unit": "Gpts/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-                "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+                "ms_per_step": ms / args.steps, "higher_is_better": True,
+                "scaling": "strong" if world > 1 else "weak",
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic",
                 "config": config_of(w, world), "roofline": roof, "cpu_baseline": cb,
                 "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary}
         print(json.dumps(line))
     plan.close()
+    if comm:
+        comm.close()
     if dist:
         dist.destroy_process_group()
 

@@ -104,6 +104,43 @@ SFDB200_API long sfdb200_steps(const sfdb200_plan* plan);
 SFDB200_API long sfdb200_h2d_bytes(const sfdb200_plan* plan);
 SFDB200_API long sfdb200_d2h_bytes(const sfdb200_plan* plan);
 
+/* ---- multi-GPU: z-slab decomposition -------------------
+ * One process per GPU.  Every rank creates a communicator from the same
+ * 128-byte unique id (made by rank 0, shared by the caller, e.g. through
+ * torch.distributed), then a plan for the GLOBAL problem: the rank keeps the
+ * planes [z_begin, z_end) of the updated z range (sfdb200_slab) plus so/2
+ * ghost planes a side, sweeps the so/2 planes next to each neighbour first and
+ * exchanges them (NCCL send/recv on its own stream) while the interior runs.
+ * upload() takes the global host arrays; download() writes the rank's owned
+ * planes of u / v / grad and its owned receivers' trace columns (others are
+ * left zero: summing the traces over ranks assembles the record). */
+typedef struct sfdb200_comm sfdb200_comm;
+SFDB200_API int sfdb200_comm_unique_id(void* id128);
+SFDB200_API int sfdb200_comm_create(const void* id128, int world, int rank, int device,
+                                    sfdb200_comm** out);
+SFDB200_API int sfdb200_comm_destroy(sfdb200_comm* comm);
+/* Test harness for one GPU: `world` emulated ranks in one process (no NCCL).
+ * Their plans must share one stream (sfdb200_set_stream) and run together
+ * through sfdb200_execute_group, which does the ghost exchange as device
+ * copies between the plans, phase by phase in lockstep. */
+SFDB200_API int sfdb200_comm_create_loopback(int world, int rank, int device,
+                                             sfdb200_comm** out);
+SFDB200_API int sfdb200_execute_group(sfdb200_plan** plans, int n);
+SFDB200_API int sfdb200_plan_create_dist(const sfdb200_desc* global_desc, sfdb200_comm* comm,
+                                         sfdb200_plan** out);
+/* Owned updated global planes of `rank`: an even split of [so/2, Pz - so/2). */
+SFDB200_API int sfdb200_slab(long padded_z, int space_order, int world, int rank, long* z_begin,
+                             long* z_end);
+/* Which sparse corners (injection) and points (sampling, by base plane) the
+ * plan of `rank` owns, for global indices idx [npoints][ndim]; either output
+ * may be NULL.  Every corner / point is owned by exactly one rank. */
+SFDB200_API int sfdb200_slab_owns(long padded_z, int space_order, int world, int rank,
+                                  long npoints, int ndim, const long* idx,
+                                  unsigned char* corner_owned, unsigned char* point_owned);
+/* The plan's owned planes and the global index of its local plane 0. */
+SFDB200_API int sfdb200_plan_slab(const sfdb200_plan* plan, long* z_begin, long* z_end,
+                                  long* zoff);
+
 /* ---- host helpers mirroring sfd::seismic (bit-exact with the reference) -- */
 
 /* fd_coefficients(2, so) as doubles, w[0..so] for offsets -so/2..so/2 (fd.cpp:8-60). */

@@ -334,3 +334,66 @@ int sfdo_gradient(const sfdo_problem* p, double* v, const double* u, const doubl
             }
     return 0;
 }
+
+/* Masked variants of inject / sample for the decomposition harness. */
+static void inject_masked(const geom* g, double* field, const double* m, long npts,
+                          const long* idx, const double* w, const double* row, double scale,
+                          const unsigned char* cmask) {
+    const int corners = 1 << g->nd;
+    for (long p = 0; p < npts; ++p)
+        for (int c = 0; c < corners; ++c) {
+            if (cmask && !cmask[p * corners + c]) continue;
+            const long a = corner_offset(g, idx + p * g->nd, c);
+            double v = w[p * corners + c];
+            v *= scale;
+            v *= row[p];
+            v /= m[a];
+            field[a] += v;
+        }
+}
+
+int sfdo_forward_steps(const sfdo_problem* p, double* u, const double* m, const double* damp,
+                       const long* src_idx, const double* src_w, const double* src_data,
+                       const unsigned char* src_cmask, const long* rec_idx, const double* rec_w,
+                       double* rec_data, const unsigned char* rec_mask, long t_begin,
+                       long t_end) {
+    geom g;
+    if (make_geom(p, &g)) return 1;
+    const int corners = 1 << g.nd;
+    for (long t = t_begin; t < t_end; ++t) {
+        double* out = u + (t % 3) * g.cells;
+        sweep(&g, p->dt, out, u + ((t - 1) % 3) * g.cells, u + ((t - 2) % 3) * g.cells, m, damp);
+        inject_masked(&g, out, m, p->nsrc, src_idx, src_w, src_data + (t - 1) * p->nsrc,
+                      p->dt * p->dt, src_cmask);
+        if (!rec_data) continue;
+        for (long q = 0; q < p->nrec; ++q) {
+            if (rec_mask && !rec_mask[q]) continue;
+            double acc = 0.0;
+            for (int c = 0; c < corners; ++c) {
+                const double term =
+                    rec_w[q * corners + c] * out[corner_offset(&g, rec_idx + q * g.nd, c)];
+                acc = c == 0 ? term : acc + term;
+            }
+            rec_data[t * p->nrec + q] = acc;
+        }
+    }
+    return 0;
+}
+
+int sfdo_sample_row(const sfdo_problem* p, const double* u, long t, const long* rec_idx,
+                    const double* rec_w, double* rec_data, const unsigned char* rec_mask) {
+    geom g;
+    if (make_geom(p, &g)) return 1;
+    const int corners = 1 << g.nd;
+    const double* f = u + (t % 3) * g.cells;
+    for (long q = 0; q < p->nrec; ++q) {
+        if (rec_mask && !rec_mask[q]) continue;
+        double acc = 0.0;
+        for (int c = 0; c < corners; ++c) {
+            const double term = rec_w[q * corners + c] * f[corner_offset(&g, rec_idx + q * g.nd, c)];
+            acc = c == 0 ? term : acc + term;
+        }
+        rec_data[t * p->nrec + q] = acc;
+    }
+    return 0;
+}

@@ -61,6 +61,21 @@ int sfdo_gradient(const sfdo_problem* p, double* v, const double* u, const doubl
                   const double* damp, double* grad, const long* rec_idx, const double* rec_w,
                   const double* rec_data);
 
+/* Forward time steps t in [t_begin, t_end) on an already initialised rolling
+ * field (no zeroing), with optional per-corner injection masks and
+ * per-receiver sampling masks (NULL = all); rec_data NULL skips sampling.
+ * Test harness for the z-slab decomposition: ranks step their slabs and
+ * exchange ghost planes between calls. */
+int sfdo_forward_steps(const sfdo_problem* p, double* u, const double* m, const double* damp,
+                       const long* src_idx, const double* src_w, const double* src_data,
+                       const unsigned char* src_cmask, const long* rec_idx, const double* rec_w,
+                       double* rec_data, const unsigned char* rec_mask, long t_begin,
+                       long t_end);
+
+/* rec_data[t][q] = sum_c w u[t%3][corner] for receivers with rec_mask[q]. */
+int sfdo_sample_row(const sfdo_problem* p, const double* u, long t, const long* rec_idx,
+                    const double* rec_w, double* rec_data, const unsigned char* rec_mask);
+
 #ifdef __cplusplus
 }
 #endif

@@ -54,6 +54,15 @@ _SIGS = {
     "sfdb200_steps": (_L, [_P]),
     "sfdb200_h2d_bytes": (_L, [_P]),
     "sfdb200_d2h_bytes": (_L, [_P]),
+    "sfdb200_comm_unique_id": (_i, [_P]),
+    "sfdb200_comm_create": (_i, [_P, _i, _i, _i, _P]),
+    "sfdb200_comm_destroy": (_i, [_P]),
+    "sfdb200_comm_create_loopback": (_i, [_i, _i, _i, _P]),
+    "sfdb200_execute_group": (_i, [_P, _i]),
+    "sfdb200_plan_create_dist": (_i, [_P, _P, _P]),
+    "sfdb200_slab": (_i, [_L, _i, _i, _i, _lp, _lp]),
+    "sfdb200_plan_slab": (_i, [_P, _lp, _lp, _lp]),
+    "sfdb200_slab_owns": (_i, [_L, _i, _i, _i, _L, _i, _lp, _P, _P]),
     "sfdb200_fd2": (_i, [_i, _dp]),
     "sfdb200_make_model": (_i, [_i, _lp, _D, _L, _i, _dp, _lp, _dp, _dp]),
     "sfdb200_build_damping": (_i, [_i, _lp, _L, _L, _D, _dp]),
@@ -112,7 +121,7 @@ class Plan:
     """Owning handle of an sfdb200_plan."""
 
     def __init__(self, kind, ndim, padded, space_order, nt, dt, h, nsrc, nrec, save=False,
-                 device=0):
+                 device=0, comm=None):
         d = Desc()
         d.kind, d.ndim, d.space_order = kind, ndim, space_order
         for i in range(3):
@@ -121,8 +130,12 @@ class Plan:
         d.save, d.device = int(bool(save)), int(device)
         self.desc = d
         h_ = C.c_void_p()
-        check(lib().sfdb200_plan_create(C.byref(d), C.byref(h_)))
+        if comm is None:
+            check(lib().sfdb200_plan_create(C.byref(d), C.byref(h_)))
+        else:
+            check(lib().sfdb200_plan_create_dist(C.byref(d), comm.handle, C.byref(h_)))
         self.handle = h_
+        self.comm = comm
         self._keep = None
 
     def close(self):
@@ -164,6 +177,11 @@ class Plan:
         check(lib().sfdb200_stencil_time(self.handle, C.byref(ms), C.byref(n)))
         return ms.value, n.value
 
+    def slab(self):
+        zb, ze, zo = C.c_long(), C.c_long(), C.c_long()
+        check(lib().sfdb200_plan_slab(self.handle, C.byref(zb), C.byref(ze), C.byref(zo)))
+        return zb.value, ze.value, zo.value
+
     @property
     def launches_per_execute(self):
         return lib().sfdb200_launches_per_execute(self.handle)
@@ -183,6 +201,58 @@ class Plan:
     @property
     def d2h_bytes(self):
         return lib().sfdb200_d2h_bytes(self.handle)
+
+
+class Comm:
+    """sfdb200_comm: the z-slab ranks' NCCL communicator (one per GPU process)."""
+
+    def __init__(self, unique_id: bytes, world: int, rank: int, device: int):
+        buf = C.create_string_buffer(bytes(unique_id), 128)
+        h = C.c_void_p()
+        check(lib().sfdb200_comm_create(buf, world, rank, device, C.byref(h)))
+        self.handle, self.world, self.rank, self.device = h, world, rank, device
+
+    @classmethod
+    def loopback(cls, world: int, rank: int, device: int = 0):
+        """An emulated rank for the one-GPU harness (execute_group)."""
+        c = cls.__new__(cls)
+        h = C.c_void_p()
+        check(lib().sfdb200_comm_create_loopback(world, rank, device, C.byref(h)))
+        c.handle, c.world, c.rank, c.device = h, world, rank, device
+        return c
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        check(lib().sfdb200_comm_unique_id(buf))
+        return buf.raw
+
+    def close(self):
+        if self.handle:
+            lib().sfdb200_comm_destroy(self.handle)
+            self.handle = None
+
+
+def execute_group(plans):
+    arr = (C.c_void_p * len(plans))(*[p.handle.value for p in plans])
+    check(lib().sfdb200_execute_group(arr, len(plans)))
+
+
+def slab(padded_z, space_order, world, rank):
+    zb, ze = C.c_long(), C.c_long()
+    check(lib().sfdb200_slab(int(padded_z), int(space_order), int(world), int(rank),
+                             C.byref(zb), C.byref(ze)))
+    return zb.value, ze.value
+
+
+def slab_owns(padded_z, space_order, world, rank, idx):
+    idx = i64(idx)
+    n, nd = idx.shape
+    cm = np.zeros((n, 1 << nd), np.uint8)
+    pm = np.zeros(n, np.uint8)
+    check(lib().sfdb200_slab_owns(int(padded_z), int(space_order), int(world), int(rank), n, nd,
+                                  lptr(idx), cm.ctypes.data, pm.ctypes.data))
+    return cm.astype(bool), pm.astype(bool)
 
 
 def call(kind, ndim, padded, space_order, nt, dt, h, nsrc, nrec, save, arrays, device=0):

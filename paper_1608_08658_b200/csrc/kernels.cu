@@ -400,15 +400,14 @@ __global__ void __launch_bounds__(256) sweep2d_kernel(const SweepArgs a, const i
 // ---------------------------------------------------------------- sparse ops
 
 __global__ void inject_kernel(float* __restrict__ field, const long long* __restrict__ off,
-                              const float* __restrict__ coef, const float* __restrict__ row,
-                              long total, int corners_log2, float* __restrict__ grad,
+                              const float* __restrict__ coef, const int* __restrict__ pt,
+                              const float* __restrict__ row, long n, float* __restrict__ grad,
                               const float* __restrict__ ut,
                               const unsigned char* __restrict__ gmask, float nidt2) {
     const long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
-    if (i >= total) return;
-    const long p = i >> corners_log2;
+    if (i >= n) return;
     const long long o = off[i];
-    const float delta = coef[i] * row[p];
+    const float delta = coef[i] * row[pt[i]];
     atomicAdd(field + o, delta);
     if (grad && gmask[i]) atomicAdd(grad + o, nidt2 * ut[o] * delta);
 }
@@ -535,16 +534,12 @@ cudaError_t launch_sweep2d(const FieldGeom& g, const SweepArgs& a, bool grad, cu
     return cudaGetLastError();
 }
 
-cudaError_t launch_inject(float* field, const long long* off, const float* coef,
-                          const float* row, long npoints, int corners, float* grad,
-                          const float* ut, const unsigned char* gmask, float nidt2,
-                          cudaStream_t s) {
-    const long total = npoints * corners;
-    if (total == 0) return cudaSuccess;
-    int lg = 0;
-    while ((1 << lg) < corners) ++lg;
-    inject_kernel<<<grid_for(total, 128), 128, 0, s>>>(field, off, coef, row, total, lg, grad,
-                                                       ut, gmask, nidt2);
+cudaError_t launch_inject(float* field, const long long* off, const float* coef, const int* pt,
+                          const float* row, long n, float* grad, const float* ut,
+                          const unsigned char* gmask, float nidt2, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    inject_kernel<<<grid_for(n, 128), 128, 0, s>>>(field, off, coef, pt, row, n, grad, ut, gmask,
+                                                   nidt2);
     return cudaGetLastError();
 }
 

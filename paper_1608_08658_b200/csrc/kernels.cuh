@@ -94,15 +94,15 @@ cudaError_t launch_sweep3d(const FieldGeom& g, const SweepConfig& cfg, const Swe
                            const SweepArgs& a, bool grad, cudaStream_t s);
 cudaError_t launch_sweep2d(const FieldGeom& g, const SweepArgs& a, bool grad, cudaStream_t s);
 
-// Sparse operators.  off[p][c] = element offset of corner c of point p inside
-// one row; coef = w dt^2 / m[corner] (inject) or w (sample), fp32.
+// Sparse operators over flat entry lists: off = element offset of a corner
+// inside one row, coef = w dt^2 / m[corner] (inject), pt = the entry's point
+// (trace column).
 // GRAD: the imaging condition of the row just finalised also sees the
 // injected increment, grad[c] += -(1/dt^2) u_t[c] delta, for corners inside
 // the updated region (gmask[p][c] != 0).
-cudaError_t launch_inject(float* field, const long long* off, const float* coef,
-                          const float* row, long npoints, int corners, float* grad,
-                          const float* ut, const unsigned char* gmask, float nidt2,
-                          cudaStream_t s);
+cudaError_t launch_inject(float* field, const long long* off, const float* coef, const int* pt,
+                          const float* row, long n, float* grad, const float* ut,
+                          const unsigned char* gmask, float nidt2, cudaStream_t s);
 // pt (optional): output index of each sampled point (a subset of the set).
 cudaError_t launch_sample(const float* field, const long long* off, const float* w,
                           const int* pt, float* row, long npoints, int corners, cudaStream_t s);

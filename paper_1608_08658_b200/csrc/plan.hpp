@@ -1,0 +1,211 @@
+// Internal host-side structures of the B200 backend (not installed).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/sfdb200.h"
+#include "kernels.cuh"
+
+namespace sfdb200 {
+
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void fail(int code, const std::string& msg) { throw Error(code, msg); }
+
+inline void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        fail(e == cudaErrorMemoryAllocation ? SFDB200_ENOMEM : SFDB200_ECUDA,
+             std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class T>
+T* dalloc(size_t n) {
+    if (n == 0) return nullptr;
+    void* p = nullptr;
+    ck(cudaMalloc(&p, n * sizeof(T)), "cudaMalloc");
+    return static_cast<T*>(p);
+}
+
+int env_int(const char* name, int dflt);
+
+// A flat list of (point, corner) entries for the inject kernel.
+struct InjectList {
+    long n = 0;
+    long long* off = nullptr;
+    float* coef = nullptr;
+    int* pt = nullptr;
+    unsigned char* gm = nullptr;
+};
+
+// A flat list of sampled points for the sample kernel.
+struct SampleList {
+    long n = 0;
+    long long* off = nullptr;  // [n][corners]
+    float* w = nullptr;        // [n][corners]
+    int* pt = nullptr;         // receiver index
+};
+
+// One sparse set on the device.
+struct SparseDev {
+    long n = 0;                // points in the (global) set
+    float* trace = nullptr;    // [nt][n]
+    std::vector<void*> bufs;   // device buffers owned by the tables below
+
+    // Injection: entries of the interior sweep launch, per (CTA, plane)
+    // (fused into the sweep), and the rest (boundary / halo planes, or every
+    // entry when the sweep is not fused) as a flat list.
+    int* f_tab = nullptr;
+    int2* f_rng = nullptr;
+    long long* f_off = nullptr;
+    float* f_coef = nullptr;
+    int* f_pt = nullptr;
+    unsigned char* f_gm = nullptr;
+    InjectList inj_rest;
+    // Sampling: receivers read from the staged plane by the interior sweep
+    // (previous row), the rest (fallback) sampled after the step, and every
+    // owned receiver (last row).
+    int* s_tab = nullptr;
+    int2* s_rng = nullptr;
+    int* s_hidx = nullptr;
+    float* s_w = nullptr;
+    int* s_pt = nullptr;
+    float* s_acc = nullptr;
+    SampleList smp_rest, smp_all;
+
+    template <class T>
+    T* upload(const std::vector<T>& v, cudaStream_t st) {
+        if (v.empty()) return nullptr;
+        T* d = dalloc<T>(v.size());
+        bufs.push_back(d);
+        ck(cudaMemcpyAsync(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st),
+           "H2D");
+        return d;
+    }
+    void free_tables() {
+        for (void* q : bufs) cudaFree(q);
+        bufs.clear();
+        f_tab = nullptr; f_rng = nullptr; f_off = nullptr; f_coef = nullptr; f_pt = nullptr;
+        f_gm = nullptr;
+        s_tab = nullptr; s_rng = nullptr; s_hidx = nullptr; s_w = nullptr; s_pt = nullptr;
+        s_acc = nullptr;
+        inj_rest = InjectList{};
+        smp_rest = SampleList{};
+        smp_all = SampleList{};
+    }
+};
+
+struct Comm;  // comm.cpp
+
+// Local plane zl of a slab with Pl planes (R ghost / halo planes a side) is
+// stored and updated by this rank: its updated planes, plus the global halo
+// planes on the first / last rank (ghost planes belong to the neighbours).
+inline bool owns_plane(long zl, int R, long Pl, int rank, int world) {
+    if (zl < 0 || zl >= Pl) return false;
+    if (zl >= R && zl < Pl - R) return true;
+    return zl < R ? rank == 0 : rank == world - 1;
+}
+
+}  // namespace sfdb200
+
+struct sfdb200_comm {
+    sfdb200::Comm* impl = nullptr;
+};
+
+struct sfdb200_plan {
+    sfdb200_desc gd{};  // the global problem
+    sfdb200_desc d{};   // this rank's slab (padded[0] = local planes)
+    sfdb200::FieldGeom g{};
+    int corners = 0;
+    long long rows = 3;
+    long long hist_rows = 0;
+
+    // z-slab decomposition: local plane zl <-> global plane zl + zoff.
+    int world = 1, rank = 0;
+    long zoff = 0;
+    int zint_lo = 0, zint_hi = 0;  // interior sweep launch (local planes)
+    sfdb200::Comm* comm = nullptr;
+    cudaStream_t cstream = nullptr;
+    cudaEvent_t ev_b = nullptr, ev_x = nullptr;
+
+    float* field = nullptr;  // u (forward) / v (adjoint, gradient), `rows` rows
+    float* c1 = nullptr;
+    float* c2 = nullptr;
+    float* hist = nullptr;   // gradient: u history
+    bool own_hist = false;
+    float* grad = nullptr;
+    sfdb200::SparseDev src, rec;
+    double* staging = nullptr;
+    size_t staging_elems = 0;
+    unsigned long long* counter = nullptr;
+
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;
+    sfdb200::SweepConfig cfg;
+    sfdb200::SweepMaps maps{};
+    sfdb200::SweepArgs base{};
+    bool maps_ready = false;
+    bool fused = true;
+
+    bool timing = false;
+    std::vector<cudaEvent_t> events;
+    long timed_launches = 0;
+    long launches = 0;
+    long h2d = 0, d2h = 0;
+    int sms = 148;
+
+    ~sfdb200_plan();
+
+    long steps() const { return d.nt > 2 ? d.nt - 2 : 0; }
+    long long cells() const { return static_cast<long long>(g.Pz) * g.Py * g.Px; }
+    long long plane_cells() const { return static_cast<long long>(g.Py) * g.Px; }
+    bool grad_kind() const { return d.kind == SFDB200_GRADIENT; }
+    bool dist() const { return world > 1; }
+    // Planes this rank stores and updates: its updated slab, plus the global
+    // halo planes on the first / last rank (ghost planes belong to neighbours).
+    bool owns_plane(long zl) const { return sfdb200::owns_plane(zl, g.R, g.Pz, rank, world); }
+    sfdb200::SparseDev& injected() { return d.kind == SFDB200_FORWARD ? src : rec; }
+    sfdb200::SparseDev* sampled() {
+        if (d.kind == SFDB200_FORWARD) return &rec;
+        if (d.kind == SFDB200_ADJOINT) return &src;
+        return nullptr;
+    }
+    void ensure_staging(size_t elems) {
+        if (elems <= staging_elems) return;
+        cudaFree(staging);
+        staging = nullptr;
+        staging = sfdb200::dalloc<double>(elems);
+        staging_elems = elems;
+    }
+};
+
+namespace sfdb200 {
+
+// sparse.cpp: host-side sparse tables for one set (corner offsets in the
+// local device layout, ownership by rank, fused per-CTA tables).
+void upload_sparse(sfdb200_plan& p, SparseDev& s, const long* idx, const double* w,
+                   const double* m_global);
+
+// comm.cpp: NCCL (loaded at run time) for the ghost-plane exchange.
+Comm* comm_create(const void* id128, int world, int rank, int device);
+// Emulated rank (one-GPU test harness): no NCCL; see sfdb200_execute_group.
+Comm* comm_create_loopback(int world, int rank, int device);
+bool comm_loopback(const Comm* c);
+void comm_destroy(Comm* c);
+void comm_unique_id(void* id128);
+// Sends/receives R ghost planes of one field row with the z neighbours.
+void comm_exchange(Comm* c, sfdb200_plan& p, float* row, cudaStream_t s);
+int comm_world(const Comm* c);
+int comm_rank(const Comm* c);
+int comm_device(const Comm* c);
+
+// Owned global updated planes [z_begin, z_end) of `rank` (even split).
+void slab_of(long pz_global, int R, int world, int rank, long* z_begin, long* z_end);
+
+}  // namespace sfdb200

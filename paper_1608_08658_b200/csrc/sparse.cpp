@@ -1,0 +1,247 @@
+// Host-side preparation of the sparse operators (source injection, receiver
+// sampling) for one plan: corner offsets in the device layout, ownership by
+// z-slab rank, and the per-(CTA, plane) tables that let the 3-D sweep apply
+// them inside its own launch.
+//
+// Reference semantics: codegen.cpp:419-462 (corner bit order: bit ndim-1-d of
+// c -> +1 along dim d; inject w * scale * data / m[corner]; sample
+// sum_c w_c u[corner_c] in order c = 0..2^d-1), interpreter.cpp:118-160.
+#include <algorithm>
+#include <vector>
+
+#include "plan.hpp"
+
+namespace sfdb200 {
+namespace {
+
+struct Owner {
+    int cta, plane;
+};
+
+// Sweep CTA of the interior launch (x tiles fastest, then y tiles, then z
+// chunks) and its local plane index for a point of the interior range.
+Owner owner_of(const sfdb200_plan& p, long zl, long y, long x) {
+    const SweepConfig& c = p.cfg;
+    const int R = p.g.R;
+    const long zr = zl - p.zint_lo;
+    const int bx = static_cast<int>(x / 32), by = static_cast<int>((y - R) / c.ty()),
+              bz = static_cast<int>(zr / c.zlen);
+    return {bx + c.tiles_x * (by + c.tiles_y * bz), static_cast<int>(zr - bz * c.zlen)};
+}
+
+bool in_interior(const sfdb200_plan& p, long zl, long y, long x) {
+    const int R = p.g.R;
+    return zl >= p.zint_lo && zl < p.zint_hi && y >= R && y < p.g.Py - R && x >= R &&
+           x < p.g.Px - R;
+}
+
+int ctas_of(const sfdb200_plan& p) { return p.cfg.tiles_x * p.cfg.tiles_y * p.cfg.zchunks; }
+
+// Per-CTA plane table over keys sorted by (cta, plane): entries of CTA c at
+// plane i are [tab[c*L + i], tab[c*L + i + 1]), L = zlen + 1.
+std::vector<int> plane_table(const sfdb200_plan& p, const std::vector<Owner>& keys) {
+    const int ctas = ctas_of(p), L = p.cfg.zlen + 1;
+    std::vector<int> tab(static_cast<size_t>(ctas) * L, 0);
+    size_t e = 0;
+    for (int c = 0; c < ctas; ++c)
+        for (int i = 0; i < L; ++i) {
+            while (e < keys.size() &&
+                   (keys[e].cta < c || (keys[e].cta == c && keys[e].plane < i)))
+                ++e;
+            tab[static_cast<size_t>(c) * L + i] = static_cast<int>(e);
+        }
+    return tab;
+}
+
+// Per CTA, the plane range [lo, hi + extra) holding entries (extra = 1 for
+// samples, whose second half is read one plane later); empty: (0, 0).
+std::vector<int2> plane_ranges(const sfdb200_plan& p, const std::vector<int>& tab, int extra) {
+    const int ctas = ctas_of(p), L = p.cfg.zlen + 1;
+    std::vector<int2> r(static_cast<size_t>(ctas), make_int2(0, 0));
+    for (int c = 0; c < ctas; ++c) {
+        const int* t = tab.data() + static_cast<size_t>(c) * L;
+        int lo = -1, hi = -1;
+        for (int i = 0; i + 1 < L; ++i)
+            if (t[i + 1] > t[i]) {
+                if (lo < 0) lo = i;
+                hi = i;
+            }
+        if (lo >= 0) r[static_cast<size_t>(c)] = make_int2(lo, std::min(hi + 1 + extra, L - 1));
+    }
+    return r;
+}
+
+struct Corner {
+    long long off;     // element offset in one local row
+    long zl, y, x;     // local position
+    long long dense;   // global dense index (for m)
+    bool owned;        // this rank stores and updates the cell
+    bool updated;      // inside the updated region (the gradient accumulates there)
+};
+
+}  // namespace
+
+void upload_sparse(sfdb200_plan& p, SparseDev& s, const long* idx, const double* w,
+                   const double* m) {
+    s.free_tables();
+    if (s.n == 0) return;
+    const sfdb200_desc& gd = p.gd;
+    const FieldGeom& g = p.g;
+    const int nd = gd.ndim, C = p.corners, R = g.R;
+    const cudaStream_t st = p.stream;
+    const bool is_inj = &s == &p.injected();
+    const bool is_smp = &s == p.sampled();
+    const bool fused3d = nd == 3 && p.fused;
+
+    std::vector<Corner> cs(static_cast<size_t>(s.n) * C);
+    for (long q = 0; q < s.n; ++q)
+        for (int c = 0; c < C; ++c) {
+            long pos[3] = {0, 0, 0};
+            long long dense = 0;
+            for (int k = 0; k < nd; ++k) {
+                pos[k] = idx[q * nd + k] + ((c >> (nd - 1 - k)) & 1);
+                if (pos[k] < 0 || pos[k] >= gd.padded[k])
+                    fail(SFDB200_EINVAL, "sparse point corner lies outside the padded grid");
+                dense = dense * gd.padded[k] + pos[k];
+            }
+            Corner& k = cs[static_cast<size_t>(q) * C + c];
+            k.zl = pos[0] - p.zoff;
+            k.y = nd == 3 ? pos[1] : 0;
+            k.x = pos[nd - 1];
+            k.dense = dense;
+            k.owned = p.owns_plane(k.zl);
+            k.off = k.zl * g.pz + k.y * g.py + k.x;
+            k.updated = k.zl >= R && k.zl < g.Pz - R && k.x >= R && k.x < g.Px - R &&
+                        (nd == 2 || (k.y >= R && k.y < g.Py - R));
+        }
+
+    if (is_inj) {
+        // coef = w * dt^2 / m[corner]: the reference's v = w; v *= scale;
+        // v /= m with the data factor applied on the device (interpreter.cpp:144-147).
+        struct E { Owner o; size_t i; };
+        std::vector<E> fused;
+        std::vector<long long> r_off;
+        std::vector<float> r_coef;
+        std::vector<int> r_pt;
+        std::vector<unsigned char> r_gm;
+        for (size_t i = 0; i < cs.size(); ++i) {
+            const Corner& k = cs[i];
+            if (!k.owned) continue;
+            if (fused3d && in_interior(p, k.zl, k.y, k.x)) {
+                fused.push_back({owner_of(p, k.zl, k.y, k.x), i});
+                continue;
+            }
+            r_off.push_back(k.off);
+            r_coef.push_back(static_cast<float>(w[i] * (gd.dt * gd.dt) / m[k.dense]));
+            r_pt.push_back(static_cast<int>(i / C));
+            r_gm.push_back(k.updated ? 1 : 0);
+        }
+        s.inj_rest.n = static_cast<long>(r_off.size());
+        s.inj_rest.off = s.upload(r_off, st);
+        s.inj_rest.coef = s.upload(r_coef, st);
+        s.inj_rest.pt = s.upload(r_pt, st);
+        s.inj_rest.gm = s.upload(r_gm, st);
+        if (!fused.empty()) {
+            // (plane, point, corner) order: each plane's injections follow the
+            // reference's (p, c) order.
+            std::stable_sort(fused.begin(), fused.end(), [](const E& a, const E& b) {
+                return a.o.cta != b.o.cta ? a.o.cta < b.o.cta : a.o.plane < b.o.plane;
+            });
+            std::vector<Owner> keys;
+            std::vector<long long> eoff;
+            std::vector<float> ecoef;
+            std::vector<int> ept;
+            std::vector<unsigned char> egm;
+            for (const E& e : fused) {
+                const Corner& k = cs[e.i];
+                keys.push_back(e.o);
+                eoff.push_back(k.off);
+                ecoef.push_back(static_cast<float>(w[e.i] * (gd.dt * gd.dt) / m[k.dense]));
+                ept.push_back(static_cast<int>(e.i / C));
+                egm.push_back(1);
+            }
+            const std::vector<int> tab = plane_table(p, keys);
+            s.f_tab = s.upload(tab, st);
+            s.f_rng = s.upload(plane_ranges(p, tab, 0), st);
+            s.f_off = s.upload(eoff, st);
+            s.f_coef = s.upload(ecoef, st);
+            s.f_pt = s.upload(ept, st);
+            s.f_gm = s.upload(egm, st);
+        }
+    }
+
+    if (is_smp) {
+        // A receiver belongs to the rank owning its base plane z0.  The sweep
+        // reads it from the staged halo plane when the base (y, x) lies in a
+        // tile and z0, z0 + 1 lie in one z chunk of the interior launch (all
+        // x/y corners are then inside tile + halo); the rest is sampled by
+        // sample_kernel after the step (after the ghost exchange).
+        const int RA = (R + 3) & ~3, BW = p.cfg.bw(R);
+        struct E { Owner o; int hidx; long q; };
+        std::vector<E> fused;
+        std::vector<long long> a_off, r_off;
+        std::vector<float> a_w, r_w;
+        std::vector<int> a_pt, r_pt;
+        for (long q = 0; q < s.n; ++q) {
+            const Corner& b = cs[static_cast<size_t>(q) * C];  // corner 0: the base
+            if (!b.owned) continue;
+            for (int c = 0; c < C; ++c) {
+                a_off.push_back(cs[static_cast<size_t>(q) * C + c].off);
+                a_w.push_back(static_cast<float>(w[static_cast<size_t>(q) * C + c]));
+            }
+            a_pt.push_back(static_cast<int>(q));
+            bool ok = fused3d && b.zl >= p.zint_lo && b.zl + 1 < p.zint_hi && b.y >= R &&
+                      b.y < g.Py - R && b.x >= 0 && b.x < 32L * p.cfg.tiles_x;
+            Owner o{0, 0};
+            if (ok) {
+                o = owner_of(p, b.zl, b.y, b.x);
+                ok = o.plane + 1 < p.cfg.zlen;  // z0 + 1 in the same chunk
+            }
+            if (ok) {
+                const long y0 = R + ((b.y - R) / p.cfg.ty()) * p.cfg.ty();
+                const long x0 = (b.x / 32) * 32;
+                fused.push_back({o, static_cast<int>((b.y - y0 + R) * BW + (b.x - x0 + RA)), q});
+            } else {
+                for (int c = 0; c < C; ++c) {
+                    r_off.push_back(cs[static_cast<size_t>(q) * C + c].off);
+                    r_w.push_back(static_cast<float>(w[static_cast<size_t>(q) * C + c]));
+                }
+                r_pt.push_back(static_cast<int>(q));
+            }
+        }
+        s.smp_all.n = static_cast<long>(a_pt.size());
+        s.smp_all.off = s.upload(a_off, st);
+        s.smp_all.w = s.upload(a_w, st);
+        s.smp_all.pt = s.upload(a_pt, st);
+        s.smp_rest.n = static_cast<long>(r_pt.size());
+        s.smp_rest.off = s.upload(r_off, st);
+        s.smp_rest.w = s.upload(r_w, st);
+        s.smp_rest.pt = s.upload(r_pt, st);
+        if (!fused.empty()) {
+            std::stable_sort(fused.begin(), fused.end(), [](const E& a, const E& b) {
+                return a.o.cta != b.o.cta ? a.o.cta < b.o.cta : a.o.plane < b.o.plane;
+            });
+            std::vector<Owner> keys;
+            std::vector<int> hidx, pt;
+            std::vector<float> w8;
+            for (const E& e : fused) {
+                keys.push_back(e.o);
+                hidx.push_back(e.hidx);
+                pt.push_back(static_cast<int>(e.q));
+                for (int c = 0; c < C; ++c)
+                    w8.push_back(static_cast<float>(w[static_cast<size_t>(e.q) * C + c]));
+            }
+            const std::vector<int> tab = plane_table(p, keys);
+            s.s_tab = s.upload(tab, st);
+            s.s_rng = s.upload(plane_ranges(p, tab, 1), st);
+            s.s_hidx = s.upload(hidx, st);
+            s.s_w = s.upload(w8, st);
+            s.s_pt = s.upload(pt, st);
+            s.s_acc = s.upload(std::vector<float>(fused.size(), 0.0f), st);
+        }
+    }
+    ck(cudaStreamSynchronize(st), "sparse upload");
+    p.h2d += static_cast<long>(s.n) * (nd * 8 + C * 8);
+}
+
+}  // namespace sfdb200

@@ -47,6 +47,9 @@ _ORACLE_SIGS = {
     "sfdo_forward": (_i, [_P, _i, _dp, _dp, _dp, _lp, _dp, _dp, _lp, _dp, _dp]),
     "sfdo_adjoint": (_i, [_P, _dp, _dp, _dp, _lp, _dp, _dp, _lp, _dp, _dp]),
     "sfdo_gradient": (_i, [_P, _dp, _dp, _dp, _dp, _dp, _lp, _dp, _dp]),
+    "sfdo_forward_steps": (_i, [_P, _dp, _dp, _dp, _lp, _dp, _dp, _P, _lp, _dp, _dp, _P, _L,
+                                _L]),
+    "sfdo_sample_row": (_i, [_P, _dp, _L, _lp, _dp, _dp, _P]),
 }
 _REF_SIGS = {
     "sfdref_fd2": (_i, [_i, _dp]),
@@ -200,6 +203,27 @@ def gradient(padded, so, h, dt, nt, m, damp, u_history, rec_idx, rec_w, rec_data
                                 _d(_f64(rec_data)))
     assert rc == 0
     return grad.reshape(padded), v.reshape(3, *padded)
+
+
+def forward_steps(padded, so, h, dt, nt, u, m, damp, src_idx, src_w, src_data, src_cmask,
+                  t_begin, t_end):
+    """Sweep + masked injection for t in [t_begin, t_end) on u (3 slots, in place)."""
+    p = _problem(padded, so, nt, dt, h, len(src_idx), 0)
+    cm = None if src_cmask is None else np.ascontiguousarray(src_cmask, np.uint8)
+    rc = oracle().sfdo_forward_steps(C.cast(C.pointer(p), C.c_void_p), _d(u), _d(_f64(m)),
+                                     _d(_f64(damp)), _l(_i64(src_idx)), _d(_f64(src_w)),
+                                     _d(_f64(src_data)), cm.ctypes.data if cm is not None
+                                     else None, None, None, None, None, t_begin, t_end)
+    assert rc == 0
+
+
+def sample_row(padded, so, h, dt, nt, u, t, rec_idx, rec_w, rec_data, rec_mask):
+    p = _problem(padded, so, nt, dt, h, 0, len(rec_idx))
+    pm = None if rec_mask is None else np.ascontiguousarray(rec_mask, np.uint8)
+    rc = oracle().sfdo_sample_row(C.cast(C.pointer(p), C.c_void_p), _d(u), t, _l(_i64(rec_idx)),
+                                  _d(_f64(rec_w)), _d(rec_data),
+                                  pm.ctypes.data if pm is not None else None)
+    assert rc == 0
 
 
 # ---------------------------------------------------------------- reference
