@@ -331,7 +331,9 @@ def ref_gradient(interior, h, nbpml, so, m_interior, rec_coords, residual, u_his
 
 
 def rel_l2(a, b):
-    a = np.asarray(a, np.float64)
-    b = np.asarray(b, np.float64)
+    a = np.asarray(a, np.float64).ravel()
+    b = np.asarray(b, np.float64).ravel()
+    if a.size != b.size:
+        raise ValueError(f"size mismatch {a.size} vs {b.size}")
     den = np.linalg.norm(b)
     return float(np.linalg.norm(a - b) / den) if den > 0 else float(np.linalg.norm(a - b))
