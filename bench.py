@@ -334,7 +334,7 @@ def run_ours(args):
                 "ms_per_step": ms / args.steps, "higher_is_better": True,
                 "scaling": "strong" if world > 1 else "weak",
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "config": config_of(w, world), "roofline": roof, "cpu_baseline": cb,
+                "config": config_of(w, world, {"sweep": plan.info()}), "roofline": roof, "cpu_baseline": cb,
                 "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary}
         print(json.dumps(line))
     plan.close()

@@ -100,6 +100,8 @@ SFDB200_API long sfdb200_launches_per_execute(const sfdb200_plan* plan);
 /* Updated points per step ((n + 2 nbpml)^ndim, lowering.cpp:111-121) and steps (nt-2). */
 SFDB200_API long sfdb200_points_per_step(const sfdb200_plan* plan);
 SFDB200_API long sfdb200_steps(const sfdb200_plan* plan);
+/* The 3-D sweep configuration chosen for this plan, as a JSON object. */
+SFDB200_API int sfdb200_plan_info(const sfdb200_plan* plan, char* buf, long len);
 /* Host<->device bytes moved by upload()/download() for this plan. */
 SFDB200_API long sfdb200_h2d_bytes(const sfdb200_plan* plan);
 SFDB200_API long sfdb200_d2h_bytes(const sfdb200_plan* plan);

@@ -53,6 +53,7 @@ _SIGS = {
     "sfdb200_points_per_step": (_L, [_P]),
     "sfdb200_steps": (_L, [_P]),
     "sfdb200_h2d_bytes": (_L, [_P]),
+    "sfdb200_plan_info": (_i, [_P, C.c_char_p, _L]),
     "sfdb200_d2h_bytes": (_L, [_P]),
     "sfdb200_comm_unique_id": (_i, [_P]),
     "sfdb200_comm_create": (_i, [_P, _i, _i, _i, _P]),
@@ -176,6 +177,12 @@ class Plan:
         n = C.c_long()
         check(lib().sfdb200_stencil_time(self.handle, C.byref(ms), C.byref(n)))
         return ms.value, n.value
+
+    def info(self):
+        import json
+        buf = C.create_string_buffer(1024)
+        check(lib().sfdb200_plan_info(self.handle, buf, 1024))
+        return json.loads(buf.value.decode())
 
     def slab(self):
         zb, ze, zo = C.c_long(), C.c_long(), C.c_long()

@@ -25,352 +25,6 @@
 namespace sfdb200 {
 namespace {
 
-// ---------------------------------------------------------------- PTX helpers
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-
-__device__ __forceinline__ void fence_barrier_init() {
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-
-__device__ __forceinline__ void fence_proxy_async() {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                 "r"(bytes)
-                 : "memory");
-}
-
-__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
-    uint32_t ok;
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-        "selp.u32 %0, 1, 0, p;\n"
-        "}\n"
-        : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-    return ok != 0;
-}
-
-// Spins on the stage barrier; a transaction count that can never complete
-// (a bug) traps instead of hanging the GPU.
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    uint32_t spins = 0;
-    while (!mbar_try_wait(bar, parity))
-        if (++spins == (1u << 26)) __trap();
-}
-
-__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1,
-                                            int c2, int c3, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
-        "r"(smem_u32(bar))
-        : "memory");
-}
-
-template <int R, int BY, int NY, bool GRAD>
-struct Tile {
-    static constexpr int TX = 32;
-    static constexpr int HALF = BY * NY;  // rows per tile half
-    static constexpr int TY = 2 * HALF;
-    // TMA box starts must be 16-byte aligned in x: tiles start at multiples of
-    // 32 columns and the x halo is widened to RA = roundup(R, 4).
-    static constexpr int RA = (R + 3) & ~3;
-    static constexpr int BW = TX + 2 * RA;                     // halo row pitch
-    static constexpr int HF = ((TY + 2 * R) * BW + 31) & ~31;  // halo floats, 128 B multiple
-    static constexpr int CF = TY * TX;                         // centre box floats
-    static constexpr int NC = GRAD ? 5 : 4;                    // u1c, u2, c1, c2, [ut]
-    static constexpr int SF = HF + NC * CF;                    // floats per stage
-    // Bytes the TMA boxes of one stage deliver (the mbarrier transaction count).
-    static constexpr uint32_t BYTES = static_cast<uint32_t>((TY + 2 * R) * BW + NC * CF) * 4u;
-    static constexpr int Q = 2 * R + 1;                        // z-queue length
-};
-
-__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
-__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
-__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
-__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
-
-template <int V>
-struct IC {
-    static constexpr int value = V;
-};
-
-// ---------------------------------------------------------------- 3-D sweep
-//
-// Thread (lx, wy) owns column x = x0 + lx and NY rows in EACH half of the
-// tile: rows ly0 + j (top) and HALF + ly0 + j (bottom), j < NY.  Every value
-// is a float2 {top, bottom}, so the whole update runs on the packed fp32x2
-// pipe (FADD2/FFMA2/FMUL2, sm_100): per k and per point pair, 5 FADD2 for the
-// six neighbours and 2 FFMA2 for
-//     lap += w_k * ((sum of the 2*ndim neighbours at distance k) - 2*ndim*u0)
-// (the centred per-k form keeps the fp32 error ~1e-6).  The z
-// neighbours live in a register queue of Q = 2R+1 planes; with ROT the z loop
-// is unrolled by Q so the queue rotates by renaming (no moves).
-
-template <int R, int BY, int NY, int S, bool GRAD, bool ROT>
-__global__ void __launch_bounds__(32 * BY)
-    sweep3d_kernel(const __grid_constant__ CUtensorMap tm_uh,
-                   const __grid_constant__ CUtensorMap tm_uc,
-                   const __grid_constant__ CUtensorMap tm_c1,
-                   const __grid_constant__ CUtensorMap tm_c2,
-                   const __grid_constant__ CUtensorMap tm_ut, const SweepArgs a, const int Px,
-                   const int Py, const long long py, const long long pz) {
-    using T = Tile<R, BY, NY, GRAD>;
-    constexpr int Q = T::Q;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    float* smem = reinterpret_cast<float*>(smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u));
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * T::SF);
-
-    const int lx = threadIdx.x;
-    const int ly0 = threadIdx.y * NY;
-    const int tid = threadIdx.y * 32 + lx;
-    const int x0 = blockIdx.x * T::TX;
-    const int y0 = R + blockIdx.y * T::TY;
-    const int zb = a.zlo + blockIdx.z * a.zchunk;
-    const int ze = min(zb + a.zchunk, a.zhi);
-    if (zb >= ze) return;
-    const int n = ze - zb;
-    const int x = x0 + lx;
-
-    auto issue = [&](int stage, int z) {
-        float* sb = smem + stage * T::SF;
-        uint64_t* bar = &bars[stage];
-        mbar_arrive_expect_tx(bar, T::BYTES);
-        tma_load_4d(sb, &tm_uh, x0 - T::RA, y0 - R, z, a.row_u1, bar);
-        tma_load_4d(sb + T::HF, &tm_uc, x0, y0, z + R, a.row_u1, bar);
-        tma_load_4d(sb + T::HF + T::CF, &tm_uc, x0, y0, z, a.row_u2, bar);
-        tma_load_4d(sb + T::HF + 2 * T::CF, &tm_c1, x0, y0, z, 0, bar);
-        tma_load_4d(sb + T::HF + 3 * T::CF, &tm_c2, x0, y0, z, 0, bar);
-        if constexpr (GRAD) tma_load_4d(sb + T::HF + 4 * T::CF, &tm_ut, x0, y0, z, a.row_ut, bar);
-    };
-
-    if (tid == 0) {
-#pragma unroll
-        for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
-        fence_barrier_init();
-    }
-    __syncthreads();
-    if (tid == 0) {
-        for (int s = 0; s < S && s < n; ++s) issue(s, zb + s);
-    }
-
-    const int cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
-    // Plane ranges with fused sparse work: loaded once, so planes without
-    // sparse work (nearly all) never touch the tables.
-    const int* stab = a.smp_tab ? a.smp_tab + static_cast<long long>(cta) * (a.zchunk + 1) : nullptr;
-    const int* itab = a.inj_tab ? a.inj_tab + static_cast<long long>(cta) * (a.zchunk + 1) : nullptr;
-    const int2 srng = stab ? a.smp_rng[cta] : make_int2(0, 0);
-    const int2 irng = itab ? a.inj_rng[cta] : make_int2(0, 0);
-    // Warm L2 with this CTA's entry records so the planes that use them do
-    // not stall on DRAM latency.
-    auto prefetch = [&](const void* base, long long bytes) {
-        const char* b = static_cast<const char*>(base);
-        for (long long o = tid * 128LL; o < bytes; o += 32LL * BY * 128)
-            asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(b + o));
-    };
-    if (srng.y > srng.x) {
-        const int e0 = stab[srng.x], e1 = stab[srng.y];
-        prefetch(a.smp_hidx + e0, 4LL * (e1 - e0));
-        prefetch(a.smp_pt + e0, 4LL * (e1 - e0));
-        prefetch(a.smp_w + 8LL * e0, 32LL * (e1 - e0));
-    }
-    if (irng.y > irng.x) {
-        const int e0 = itab[irng.x], e1 = itab[irng.y];
-        prefetch(a.inj_off + e0, 8LL * (e1 - e0));
-        prefetch(a.inj_coef + e0, 4LL * (e1 - e0));
-        prefetch(a.inj_pt + e0, 4LL * (e1 - e0));
-    }
-
-    // Queue slot of plane zb - R + t is t mod Q.
-    float2 q[NY][Q];
-    bool va[NY], vb[NY];
-    const bool xin = x >= R && x < Px - R;
-#pragma unroll
-    for (int j = 0; j < NY; ++j) {
-        const int ya_ = y0 + ly0 + j, yb_ = ya_ + T::HALF;
-        va[j] = xin && ya_ < Py - R;
-        vb[j] = xin && yb_ < Py - R;
-        const float* ca = a.u1 + static_cast<long long>(ya_) * py + x;
-        const float* cb = a.u1 + static_cast<long long>(yb_) * py + x;
-#pragma unroll
-        for (int t = 0; t < 2 * R; ++t) {
-            const long long o = static_cast<long long>(zb - R + t) * pz;
-            q[j][t] = f2(va[j] ? __ldg(ca + o) : 0.0f, vb[j] ? __ldg(cb + o) : 0.0f);
-        }
-    }
-
-    const float2 neg2nd = f2(a.neg2nd, a.neg2nd);
-    const float2 mone = f2(-1.0f, -1.0f);
-    float2 wk[R + 1];
-#pragma unroll
-    for (int k = 0; k <= R; ++k) wk[k] = f2(a.w[k], a.w[k]);
-    const float2 nidt2 = f2(a.nidt2, a.nidt2);
-
-    float* outa = a.out + static_cast<long long>(y0 + ly0) * py + x;
-    float* outb = outa + T::HALF * py;
-    float* ga = GRAD ? a.grad + static_cast<long long>(y0 + ly0) * py + x : nullptr;
-    float* gb = GRAD ? ga + T::HALF * py : nullptr;
-
-    // One z plane.  PH is the compile-time phase of plane i within the queue
-    // rotation (always 0 without ROT, where the queue is shifted instead).
-    auto plane = [&](auto ph_c, const int i) {
-        constexpr int PH = decltype(ph_c)::value;
-        auto slot = [](int off) { return ((PH + off + R) % Q + Q) % Q; };
-        const int st = i % S;
-        mbar_wait(&bars[st], static_cast<uint32_t>((i / S) & 1));
-        const float* H = smem + st * T::SF;
-        const float* Cq = H + T::HF;
-        const float* U2 = Cq + T::CF;
-        const float* C1 = U2 + T::CF;
-        const float* C2 = C1 + T::CF;
-        const float* UT = C2 + T::CF;
-        const int ca = ly0 * T::TX + lx, cb = ca + T::HALF * T::TX;
-
-#pragma unroll
-        for (int j = 0; j < NY; ++j)
-            q[j][slot(R)] = f2(Cq[ca + j * T::TX], Cq[cb + j * T::TX]);
-
-        // y neighbours outside this thread's NY rows (both halves).
-        float2 ya[R], yb[R];
-        const float* hA = H + ly0 * T::BW + lx + T::RA;   // smem row ly0 <-> tile row ly0 - R
-        const float* hB = hA + T::HALF * T::BW;
-#pragma unroll
-        for (int k = 0; k < R; ++k) {
-            ya[k] = f2(hA[k * T::BW], hB[k * T::BW]);
-            yb[k] = f2(hA[(NY + R + k) * T::BW], hB[(NY + R + k) * T::BW]);
-        }
-        const long long zoff = static_cast<long long>(zb + i) * pz;
-
-#pragma unroll
-        for (int j = 0; j < NY; ++j) {
-            const float2 c0 = q[j][slot(0)];
-            const float* ra = hA + (j + R) * T::BW;
-            const float* rb = hB + (j + R) * T::BW;
-            float2 lap = f2(0.0f, 0.0f);
-#pragma unroll
-            for (int k = 1; k <= R; ++k) {
-                const int rm = j + R - k, rp = j + R + k;  // smem rows of the y neighbours
-                const float2 ym = rm < R ? ya[rm] : (rm < R + NY ? q[rm - R][slot(0)] : yb[rm - R - NY]);
-                const float2 yp = rp < R ? ya[rp] : (rp < R + NY ? q[rp - R][slot(0)] : yb[rp - R - NY]);
-                const float2 xs = add2(f2(ra[-k], rb[-k]), f2(ra[k], rb[k]));
-                const float2 zs = add2(q[j][slot(-k)], q[j][slot(k)]);
-                float2 sk = add2(add2(xs, add2(ym, yp)), zs);
-                sk = fma2(neg2nd, c0, sk);
-                lap = fma2(wk[k], sk, lap);
-            }
-            const int ia = ca + j * T::TX, ib = cb + j * T::TX;
-            const float2 d = fma2(f2(U2[ia], U2[ib]), mone, c0);           // c0 - u2, exact form
-            const float2 inc = fma2(f2(C1[ia], C1[ib]), d, mul2(f2(C2[ia], C2[ib]), lap));
-            const float2 o = add2(c0, inc);
-            const long long off = zoff + j * py;
-            if (va[j]) outa[off] = o.x;
-            if (vb[j]) outb[off] = o.y;
-            if constexpr (GRAD) {
-                // grad += -(1/dt^2) u_t (v_t - 2 v_{t+1} + v_{t+2}) = nidt2 * u_t * (inc - d)
-                const float2 vtt = fma2(d, mone, inc);
-                const float2 coef = mul2(nidt2, f2(UT[ia], UT[ib]));
-                if (va[j]) ga[off] = fmaf(coef.x, vtt.x, ga[off]);
-                if (vb[j]) gb[off] = fmaf(coef.y, vtt.y, gb[off]);
-            }
-        }
-
-        if constexpr (!ROT) {
-#pragma unroll
-            for (int j = 0; j < NY; ++j)
-#pragma unroll
-                for (int t = 0; t < 2 * R; ++t) q[j][t] = q[j][t + 1];
-        }
-        // Fused Sample from the staged u1 plane (see SweepArgs): second halves
-        // of receivers based on the previous plane, first halves of those based here.
-        if (i >= srng.x && i < srng.y) {
-            const int e0 = i > 0 ? stab[i - 1] : stab[0], e1 = stab[i], e2 = stab[i + 1];
-            for (int e = e0 + tid; e < e2; e += 32 * BY) {
-                const float* hp = H + a.smp_hidx[e];
-                const float* w = a.smp_w + 8LL * e;
-                const int c0 = e < e1 ? 4 : 0;
-                float acc = e < e1 ? a.smp_acc[e] : 0.0f;
-                acc = fmaf(__ldg(w + c0 + 0), hp[0], acc);
-                acc = fmaf(__ldg(w + c0 + 1), hp[1], acc);
-                acc = fmaf(__ldg(w + c0 + 2), hp[T::BW], acc);
-                acc = fmaf(__ldg(w + c0 + 3), hp[T::BW + 1], acc);
-                if (e < e1) a.smp_row[a.smp_pt[e]] = acc;
-                else a.smp_acc[e] = acc;
-            }
-        }
-        __syncthreads();
-        if (tid == 0 && i + S < n) {
-            fence_proxy_async();
-            issue(st, zb + i + S);
-        }
-        // Fused Inject (see SweepArgs): the barrier above made the plane's
-        // stores visible to the whole CTA.
-        if (i >= irng.x && i < irng.y) {
-            const int e0 = itab[i], e1 = itab[i + 1];
-            for (int e = e0 + tid; e < e1; e += 32 * BY) {
-                const long long o = a.inj_off[e];
-                const float delta = a.inj_coef[e] * __ldg(a.inj_row + a.inj_pt[e]);
-                atomicAdd(a.out + o, delta);
-                if constexpr (GRAD)
-                    if (a.inj_gm[e]) atomicAdd(a.grad + o, a.nidt2 * __ldg(a.ut + o) * delta);
-            }
-        }
-    };
-
-    if constexpr (ROT) {
-        for (int base = 0; base < n; base += Q) {
-            [&]<int... P>(std::integer_sequence<int, P...>) {
-                ((base + P < n ? (plane(IC<P>{}, base + P), true) : false) && ...);
-            }(std::make_integer_sequence<int, Q>{});
-        }
-    } else {
-        for (int i = 0; i < n; ++i) plane(IC<0>{}, i);
-    }
-}
-
-template <int R, int BY, int NY, int S, bool GRAD, bool ROT>
-cudaError_t launch3d_t(const FieldGeom& g, const SweepConfig& cfg, const SweepMaps& m,
-                       const SweepArgs& a, cudaStream_t s) {
-    auto kern = sweep3d_kernel<R, BY, NY, S, GRAD, ROT>;
-    const size_t smem = sweep3d_smem_bytes(R, cfg, GRAD);
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-    dim3 grid(cfg.tiles_x, cfg.tiles_y, cfg.zchunks);
-    dim3 block(32, BY);
-    kern<<<grid, block, smem, s>>>(m.uh, m.uc, m.c1, m.c2, m.ut, a, g.Px, g.Py, g.py, g.pz);
-    return cudaGetLastError();
-}
-
-template <int R, bool GRAD>
-cudaError_t launch3d_r(const FieldGeom& g, const SweepConfig& cfg, const SweepMaps& m,
-                       const SweepArgs& a, cudaStream_t s) {
-    // (by, ny, stages, rot) variants compiled for every radius.
-    if (cfg.by == 4 && cfg.ny == 2 && cfg.stages == 4)
-        return cfg.rot ? launch3d_t<R, 4, 2, 4, GRAD, true>(g, cfg, m, a, s)
-                       : launch3d_t<R, 4, 2, 4, GRAD, false>(g, cfg, m, a, s);
-    if (cfg.by == 4 && cfg.ny == 1 && cfg.stages == 4)
-        return cfg.rot ? launch3d_t<R, 4, 1, 4, GRAD, true>(g, cfg, m, a, s)
-                       : launch3d_t<R, 4, 1, 4, GRAD, false>(g, cfg, m, a, s);
-    if (cfg.by == 8 && cfg.ny == 1 && cfg.stages == 3)
-        return cfg.rot ? launch3d_t<R, 8, 1, 3, GRAD, true>(g, cfg, m, a, s)
-                       : launch3d_t<R, 8, 1, 3, GRAD, false>(g, cfg, m, a, s);
-    return cudaErrorInvalidConfiguration;
-}
-
 // ---------------------------------------------------------------- 2-D sweep
 // 2-D fields are small (cfg1: 285^2 cells = 0.3 MB per row, L2-resident):
 // one thread per point, neighbours through L1.
@@ -484,15 +138,14 @@ size_t sweep3d_smem_bytes(int R, const SweepConfig& cfg, bool grad) {
     const int HF = ((TY + 2 * R) * BW + 31) & ~31;
     const int CF = TY * 32;
     const int SF = HF + (grad ? 5 : 4) * CF;
-    return static_cast<size_t>(cfg.stages) * SF * 4 + cfg.stages * 8 + 128;
+    return static_cast<size_t>(cfg.stages) * SF * 4 + cfg.stages * 16 + 128;
 }
 
-cudaError_t launch_sweep3d(const FieldGeom& g, const SweepConfig& cfg, const SweepMaps& m,
-                           const SweepArgs& a, bool grad, cudaStream_t s) {
+static cudaError_t dispatch3d(const FieldGeom& g, const SweepConfig& cfg, const SweepMaps& m,
+                              const SweepArgs& a, bool grad, cudaStream_t s, int* occ) {
 #define SFDB_R_CASE(RR)                                                   \
     case RR:                                                              \
-        return grad ? launch3d_r<RR, true>(g, cfg, m, a, s)               \
-                    : launch3d_r<RR, false>(g, cfg, m, a, s);
+        return sweep3d_r##RR(g, cfg, m, a, grad, s, occ);
     switch (g.R) {
         SFDB_R_CASE(1)
         SFDB_R_CASE(2)
@@ -506,6 +159,18 @@ cudaError_t launch_sweep3d(const FieldGeom& g, const SweepConfig& cfg, const Swe
             return cudaErrorInvalidValue;
     }
 #undef SFDB_R_CASE
+}
+
+cudaError_t launch_sweep3d(const FieldGeom& g, const SweepConfig& cfg, const SweepMaps& m,
+                           const SweepArgs& a, bool grad, cudaStream_t s) {
+    return dispatch3d(g, cfg, m, a, grad, s, nullptr);
+}
+
+cudaError_t sweep3d_occupancy(const FieldGeom& g, const SweepConfig& cfg, bool grad,
+                              int* blocks_per_sm) {
+    SweepMaps m{};
+    SweepArgs a{};
+    return dispatch3d(g, cfg, m, a, grad, nullptr, blocks_per_sm);
 }
 
 cudaError_t launch_sweep2d(const FieldGeom& g, const SweepArgs& a, bool grad, cudaStream_t s) {

@@ -92,6 +92,25 @@ struct SweepConfig {        // 3-D tiling, chosen by choose_config()
 size_t sweep3d_smem_bytes(int R, const SweepConfig& cfg, bool grad);
 cudaError_t launch_sweep3d(const FieldGeom& g, const SweepConfig& cfg, const SweepMaps& maps,
                            const SweepArgs& a, bool grad, cudaStream_t s);
+// Per-radius instantiations (sweep3d_r<R>.cu); occ != nullptr queries the
+// resident CTAs per SM instead of launching.
+#define SFDB_DECL_R(RR)                                                                  \
+    cudaError_t sweep3d_r##RR(const FieldGeom& g, const SweepConfig& cfg,                \
+                              const SweepMaps& m, const SweepArgs& a, bool grad,          \
+                              cudaStream_t s, int* occ);
+SFDB_DECL_R(1)
+SFDB_DECL_R(2)
+SFDB_DECL_R(3)
+SFDB_DECL_R(4)
+SFDB_DECL_R(5)
+SFDB_DECL_R(6)
+SFDB_DECL_R(7)
+SFDB_DECL_R(8)
+#undef SFDB_DECL_R
+
+// Resident CTAs per SM of the variant cfg selects (registers + shared memory).
+cudaError_t sweep3d_occupancy(const FieldGeom& g, const SweepConfig& cfg, bool grad,
+                              int* blocks_per_sm);
 cudaError_t launch_sweep2d(const FieldGeom& g, const SweepArgs& a, bool grad, cudaStream_t s);
 
 // Sparse operators over flat entry lists: off = element offset of a corner

@@ -126,27 +126,71 @@ void validate(const sfdb200_desc& d) {
 
 // 3-D tiling of the interior launch [zint_lo, zint_hi): 32-column x tiles,
 // TY-row y tiles, and z chunks sized so the grid fills the CTA slots.
+//
+// The grid must fit in ONE wave (all CTAs co-resident: they then march through
+// z in lockstep fronts, so neighbouring tiles' halo planes are still in L2 when
+// read) and spread evenly over the SMs.  Among the compiled variants (rows per
+// thread, pipeline depth) and z-chunk counts, take the best
+//   score = SM balance (avg / max CTAs per SM) * latency cover (CTAs per SM,
+//           saturating at 3) * z efficiency (chunk / (chunk + R): the queue
+//           prologue re-reads R planes a side per chunk).
 void choose_config(sfdb200_plan& p) {
-    SweepConfig& c = p.cfg;
     const int R = p.g.R;
-    if (R >= 6) c.ny = 1;  // keeps the 2R+1 float2 queue within the register budget
-    if (const char* t = std::getenv("SFDB200_TILE"))
-        std::sscanf(t, "%d,%d,%d,%d", &c.by, &c.ny, &c.stages, &c.rot);
-    c.tiles_x = static_cast<int>((p.g.Px - R + 31) / 32);  // tiles start at x = 0 (TMA alignment)
-    c.tiles_y = static_cast<int>((p.g.Py - 2 * R + c.ty() - 1) / c.ty());
-    c.smem_bytes = sweep3d_smem_bytes(R, c, p.grad_kind());
-    const int by_smem = static_cast<int>((227 * 1024) / (c.smem_bytes + 1024));
-    const int by_threads = 2048 / (32 * c.by);
-    const int per_sm = std::max(1, std::min({by_smem, by_threads, 32}));
-    const long long slots = static_cast<long long>(p.sms) * per_sm;
-    const long long tiles = static_cast<long long>(c.tiles_x) * c.tiles_y;
     const int zupd = std::max(1, p.zint_hi - p.zint_lo);
-    int zc = static_cast<int>(std::max<long long>(1, slots / std::max<long long>(1, tiles)));
-    zc = std::min(zc, std::max(1, zupd / (4 * R + 8)));
-    c.zchunks = env_int("SFDB200_ZCHUNKS", zc);
-    c.zchunks = std::max(1, std::min(c.zchunks, zupd));
-    c.zlen = (zupd + c.zchunks - 1) / c.zchunks;
-    c.zchunks = (zupd + c.zlen - 1) / c.zlen;  // no empty chunks
+    struct V { int by, ny, stages; };
+    std::vector<V> variants = {{4, 2, 4}, {4, 2, 3}, {4, 1, 4}, {4, 1, 3}};
+    if (R >= 6) variants = {{4, 1, 4}, {4, 1, 3}};  // the 2R+1 float2 queue of ny = 2 spills
+    if (const char* t = std::getenv("SFDB200_TILE")) {
+        V v{4, 2, 4};
+        int rot = 1;
+        std::sscanf(t, "%d,%d,%d,%d", &v.by, &v.ny, &v.stages, &rot);
+        variants = {v};
+    }
+    const int zc_env = env_int("SFDB200_ZCHUNKS", 0);
+    double best = -1;
+    SweepConfig pick;
+    for (const V& v : variants) {
+        SweepConfig c;
+        c.by = v.by;
+        c.ny = v.ny;
+        c.stages = v.stages;
+        c.tiles_x = static_cast<int>((p.g.Px - R + 31) / 32);  // tiles start at x = 0 (TMA alignment)
+        c.tiles_y = static_cast<int>((p.g.Py - 2 * R + c.ty() - 1) / c.ty());
+        c.smem_bytes = sweep3d_smem_bytes(R, c, p.grad_kind());
+        int occ = 0;
+        if (sweep3d_occupancy(p.g, c, p.grad_kind(), &occ) != cudaSuccess || occ < 1) continue;
+        const long long tiles = static_cast<long long>(c.tiles_x) * c.tiles_y;
+        const long long slots = static_cast<long long>(p.sms) * occ;
+        // Throughput model (calibrated on B200 with cfg2 / cfg4 at so 8): a
+        // wave of `a` resident CTAs advances each CTA by min(r_max, B / a)
+        // planes per microsecond, B = the HBM-bound tile-plane rate and r_max
+        // a lone CTA's latency-bound rate; a chunk costs its planes plus a
+        // queue/pipeline prologue of ~R + 2 planes.  A small last wave runs at
+        // r_max and is what makes some chunk counts slow.
+        const double bpp = p.grad_kind() ? 32.0 : 20.0;
+        const double B = 5.7e6 / (32.0 * c.ty() * bpp);
+        const double r_max = 2.0 * 8.0 / (R + 4.0) * (16.0 / c.ty());
+        for (int zc = 1; zc <= std::max(1, zupd / (2 * R + 4)); ++zc) {
+            if (zc_env && zc != zc_env) continue;
+            const int zlen = (zupd + zc - 1) / zc;
+            const int zcs = (zupd + zlen - 1) / zlen;
+            const long long ctas = tiles * zcs;
+            double t = 0;
+            for (long long left = ctas; left > 0; left -= slots) {
+                const double act = static_cast<double>(std::min(left, slots));
+                t += (zlen + R + 2.0) / std::min(r_max, B / act);
+            }
+            const double score = 1.0 / t;
+            if (score > best) {
+                best = score;
+                pick = c;
+                pick.zchunks = zcs;
+                pick.zlen = zlen;
+            }
+        }
+    }
+    if (best < 0) fail(SFDB200_ECUDA, "no sweep variant fits this device");
+    p.cfg = pick;
 }
 
 void build_maps(sfdb200_plan& p) {
@@ -290,6 +334,80 @@ void download_rows(sfdb200_plan& p, const float* src, double* dst, long long row
     }
 }
 
+// Measured choice of the interior launch's tiling, once per plan (the role of
+// the reference's runtime::autotune, runtime.cpp:396-423, for CPU blocks):
+// every compiled variant x z-chunk count is timed on this problem (the rows
+// are scratch here; execute() zeroes them), minimum of 3 launches wins.
+// SFDB200_AUTOTUNE=0 keeps the model's choice (choose_config).
+void autotune(sfdb200_plan& p) {
+    if (p.g.ndim != 3 || p.tuned || !env_int("SFDB200_AUTOTUNE", 1) ||
+        std::getenv("SFDB200_TILE") || std::getenv("SFDB200_ZCHUNKS"))
+        return;
+    p.tuned = true;
+    const int R = p.g.R;
+    const int zupd = std::max(1, p.zint_hi - p.zint_lo);
+    std::vector<std::pair<int, int>> variants = {{2, 4}, {2, 3}, {1, 4}};  // (ny, stages)
+    if (R >= 6) variants = {{1, 4}, {1, 3}};
+    const SweepConfig start = p.cfg;
+    SweepArgs a = p.base;
+    a.out = p.field;
+    a.u1 = p.field + p.g.slot;
+    a.u2 = p.field + 2 * p.g.slot;
+    a.c1 = p.c1;
+    a.c2 = p.c2;
+    a.row_out = 0;
+    a.row_u1 = 1;
+    a.row_u2 = 2;
+    if (p.grad_kind()) {
+        a.ut = p.hist;
+        a.grad = p.grad;
+        a.row_ut = 0;
+    }
+    a.zlo = p.zint_lo;
+    a.zhi = p.zint_hi;
+    cudaEvent_t e0, e1;
+    ck(cudaEventCreate(&e0), "cudaEventCreate");
+    ck(cudaEventCreate(&e1), "cudaEventCreate");
+    float best = 1e30f;
+    SweepConfig pick = start;
+    for (auto [ny, stages] : variants) {
+        for (int zc = 1; zc <= std::min(8, std::max(1, zupd / (2 * R + 4))); ++zc) {
+            SweepConfig c = start;
+            c.by = 4;
+            c.ny = ny;
+            c.stages = stages;
+            c.tiles_y = static_cast<int>((p.g.Py - 2 * R + c.ty() - 1) / c.ty());
+            c.smem_bytes = sweep3d_smem_bytes(R, c, p.grad_kind());
+            c.zlen = (zupd + zc - 1) / zc;
+            c.zchunks = (zupd + c.zlen - 1) / c.zlen;
+            if (c.zchunks != zc) continue;
+            int occ = 0;
+            if (sweep3d_occupancy(p.g, c, p.grad_kind(), &occ) != cudaSuccess || occ < 1) continue;
+            p.cfg = c;
+            build_maps(p);
+            a.zchunk = c.zlen;
+            float t = 1e30f;
+            for (int rep = 0; rep < 4; ++rep) {
+                ck(cudaEventRecord(e0, p.stream), "event");
+                ck(launch_sweep3d(p.g, c, p.maps, a, p.grad_kind(), p.stream), "autotune");
+                ck(cudaEventRecord(e1, p.stream), "event");
+                ck(cudaEventSynchronize(e1), "autotune");
+                float ms = 0;
+                ck(cudaEventElapsedTime(&ms, e0, e1), "elapsed");
+                if (rep > 0) t = std::min(t, ms);
+            }
+            if (t < best) {
+                best = t;
+                pick = c;
+            }
+        }
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    p.cfg = pick;
+    build_maps(p);
+}
+
 void do_upload(sfdb200_plan& p, void** argv) {
     const sfdb200_desc& d = p.d;
     const bool grad = p.grad_kind();
@@ -309,9 +427,6 @@ void do_upload(sfdb200_plan& p, void** argv) {
     p.h2d += 2 * cells * 8;
 
     if (grad) {
-        upload_sparse(p, p.rec, static_cast<const long*>(argv[5]),
-                      static_cast<const double*>(argv[6]), m);
-        upload_trace(p, p.rec, static_cast<const double*>(argv[7]));
         if (!p.hist || p.own_hist) {
             if (!p.hist) {
                 p.hist_rows = d.nt + 1;
@@ -322,7 +437,12 @@ void do_upload(sfdb200_plan& p, void** argv) {
             upload_rows(p, static_cast<const double*>(argv[1]), p.hist, p.hist_rows);
         }
         build_maps(p);
+        autotune(p);  // before the fused sparse tables, which depend on the tiling
+        upload_sparse(p, p.rec, static_cast<const long*>(argv[5]),
+                      static_cast<const double*>(argv[6]), m);
+        upload_trace(p, p.rec, static_cast<const double*>(argv[7]));
     } else {
+        autotune(p);
         upload_sparse(p, p.src, static_cast<const long*>(argv[3]),
                       static_cast<const double*>(argv[4]), m);
         upload_sparse(p, p.rec, static_cast<const long*>(argv[6]),
@@ -827,6 +947,21 @@ int sfdb200_slab_owns(long padded_z, int space_order, int world, int rank, long 
             }
             if (point_owned) point_owned[q] = owns_plane(idx[q * ndim] - zoff, R, Pl, rank, world);
         }
+    });
+}
+
+int sfdb200_plan_info(const sfdb200_plan* p, char* buf, long len) {
+    return guarded([&] {
+        if (!p || !buf || len < 1) fail(SFDB200_EINVAL, "null argument");
+        const SweepConfig& c = p->cfg;
+        std::snprintf(buf, static_cast<size_t>(len),
+                      "{\"tile\": [32, %d], \"warps\": %d, \"rows_per_thread\": %d, "
+                      "\"stages\": %d, \"tiles\": [%d, %d], \"zchunks\": %d, \"zlen\": %d, "
+                      "\"smem_bytes\": %zu, \"fused_sparse\": %s, \"slab\": [%ld, %ld], "
+                      "\"x_pitch\": %d}",
+                      c.ty(), c.by + 1, 2 * c.ny, c.stages, c.tiles_x, c.tiles_y, c.zchunks,
+                      c.zlen, c.smem_bytes, p->fused ? "true" : "false", p->zoff + p->g.R,
+                      p->zoff + p->g.Pz - p->g.R, p->g.XP);
     });
 }
 

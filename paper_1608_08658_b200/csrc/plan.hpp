@@ -152,6 +152,7 @@ struct sfdb200_plan {
     sfdb200::SweepArgs base{};
     bool maps_ready = false;
     bool fused = true;
+    bool tuned = false;
 
     bool timing = false;
     std::vector<cudaEvent_t> events;

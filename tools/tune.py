@@ -61,7 +61,7 @@ def main():
             step_ms = e0.elapsed_time(e1) / plan.steps
             gbs = 20 * plan.points_per_step / (best / 1e3) / 1e9
             print(json.dumps({"workload": w.name, "tile": tile, "zchunks": zc,
-                              "sweep_ms": best, "step_ms": step_ms, "env_unfused": os.environ.get("SFDB200_UNFUSED", "0"), "gpts": plan.points_per_step / best / 1e6,
+                              "sweep_ms": best, "cfg": plan.info(), "gpts": plan.points_per_step / best / 1e6,
                               "alg_GBps": gbs}), flush=True)
             plan.close()
 
