@@ -48,7 +48,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="cfg2",
-                    help="cfg1 | cfg2 | cfg4-so{2,4,8,12,16} | cfg5")
+                    help="cfg1 | cfg2 | cfg3 (FWI gradient) | cfg4-so{2,4,8,12,16} | cfg5")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=0, help="reference sample steps (0: auto)")
@@ -62,6 +62,7 @@ def make_workload(name, time_steps=0):
     if time_steps:
         w.nt = time_steps + 2
         w.wavelet = np.ascontiguousarray(w.wavelet[:w.nt])
+    w.wavelet = np.ascontiguousarray(w.wavelet.reshape(w.nt, -1))
     return w
 
 
@@ -71,6 +72,8 @@ def _make_workload(name):
         return configs.cfg1()
     if name == "cfg2":
         return configs.cfg2()
+    if name == "cfg3":
+        return configs.cfg3()
     if name.startswith("cfg4-so"):
         return configs.cfg4(int(name[len("cfg4-so"):]))
     if name == "cfg5":
@@ -344,10 +347,118 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def run_fwi(args):
+    """cfg3 (BASELINE configs[2]): FWI gradient.  Observed traces from the true
+    model, a saved forward on the smooth background (history stays in HBM),
+    the residual, then the timed gradient operator (fused adjoint + imaging
+    condition, 32 B/pt).  One GPU."""
+    import torch
+    from paper_1608_08658_b200 import _lib as L
+    from paper_1608_08658_b200 import seismic as S
+
+    torch.cuda.set_device(0)
+    w = make_workload(args.workload, args.time_steps)
+    true = S.make_model(w.interior, w.h, w.nbpml, w.space_order, w.m_interior)
+    bg = S.make_model(w.interior, w.h, w.nbpml, w.space_order, w.extra["m_background"])
+    S.check_dt(true, w.dt)
+    S.check_dt(bg, w.dt)
+    src = S.locate_points(bg, w.src_coords)
+    rec = S.locate_points(bg, w.rec_coords)
+    P, nt = bg.padded, w.nt
+    stream = torch.cuda.Stream()
+
+    def plan(kind, save=False):
+        p = L.Plan(kind, 3, P, w.space_order, nt, w.dt, w.h, src.npoints, rec.npoints, save, 0)
+        p.set_stream(stream.cuda_stream)
+        return p
+
+    obs = np.zeros((nt, rec.npoints))
+    f_true = plan(L.FORWARD)
+    f_true.run([None, true.m, true.damp, src.idx, src.w, w.wavelet, rec.idx, rec.w, obs])
+    f_true.close()
+    syn = np.zeros((nt, rec.npoints))
+    fwd = plan(L.FORWARD, save=True)
+    fargv = [None, bg.m, bg.damp, src.idx, src.w, w.wavelet, rec.idx, rec.w, syn]
+    fwd.upload(fargv)
+    fwd.execute()
+    fwd.download(fargv)  # traces only (argv[0] = NULL skips the 77 GB history)
+    resid = syn - obs
+    grad = np.zeros(P)
+    g = plan(L.GRADIENT)
+    g.bind_history(fwd)
+    gargv = [None, None, bg.m, bg.damp, grad, rec.idx, rec.w, resid]
+    g.upload(gargv)
+    for _ in range(args.warmup):
+        g.execute()
+    torch.cuda.synchronize()
+    g.set_timing(True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(0) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            g.execute()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    sweep_ms, sweep_n = g.stencil_time()
+    g.set_timing(False)
+    pts = w.points_per_step * g.steps
+    value = pts * args.steps / (ms / 1e3) / 1e9
+    # e2e: the gradient through the C ABI with host buffers (residual in, grad out;
+    # the history stays device-resident from the saved forward, as the design intends)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        g.run(gargv)
+    el = time.perf_counter() - t0
+    e2e = {"value": pts * args.steps / el / 1e9, "unit": "Gpts/s",
+           "h2d_bytes_per_step": g.h2d_bytes, "d2h_bytes_per_step": g.d2h_bytes,
+           "ms_per_step": el / args.steps * 1e3,
+           "path": "sfdb200_run(gradient plan bound to the saved forward's device history)"}
+    peak, peak_src = measured_peak()
+    per_launch_ms = sweep_ms / max(1, sweep_n)
+    alg = BYTES_PER_POINT["gradient"] * w.points_per_step
+    achieved = alg / (per_launch_ms / 1e3) / 1e9
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": ncu_traffic(w.name),
+            "kernel": "sweep3d_kernel<GRAD>", "alg_bytes_per_launch": alg,
+            "mean_launch_ms": per_launch_ms, "kernel_share_of_step": sweep_ms / (ms / args.steps),
+            "peak_source": peak_src}
+    cb = None
+    if not args.no_cpu:
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        import oracle_lib as O
+        if O.have_ref():
+            steps = args.cpu_steps or 20
+            ntc = steps + 2
+            tr = np.ascontiguousarray(w.wavelet[:ntc])
+            uh, r, _ = O.ref_forward(w.interior, w.h, w.nbpml, w.space_order,
+                                     w.extra["m_background"], w.src_coords, tr, w.rec_coords,
+                                     ntc, w.dt, save=True)
+            _, secs = O.ref_gradient(w.interior, w.h, w.nbpml, w.space_order,
+                                     w.extra["m_background"], w.rec_coords, r, uh, ntc, w.dt)
+            cb = {"value": w.points_per_step * steps / secs / 1e9, "unit": "Gpts/s",
+                  "cores": int(os.environ["STENCILFD_THREADS"]), "kind": "reference",
+                  "sample": f"seismic::gradient on the full {'x'.join(map(str, P))} grid, "
+                            f"{steps} of {w.steps} steps (RunStats.seconds)"}
+    line = {"metric": "Gpts/s (grid-point updates/sec) 3D acoustic so-8 FWI gradient",
+            "value": value, "unit": "Gpts/s", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": config_of(w, 1, {"sweep": g.info(), "objective": 0.5 * float((resid ** 2).sum()),
+                                       "history_GB": 4.0 * (nt + 1) * np.prod(P) / 1e9}),
+            "roofline": roof, "cpu_baseline": cb, "e2e": e2e,
+            "gpu_launches": g.launches_per_execute * args.steps, "clocks": clk.summary}
+    print(json.dumps(line))
+    for p in (g, fwd):
+        p.close()
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.workload == "cfg3":
+        run_fwi(args)
     else:
         run_ours(args)
 

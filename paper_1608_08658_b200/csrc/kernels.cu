@@ -137,7 +137,7 @@ size_t sweep3d_smem_bytes(int R, const SweepConfig& cfg, bool grad) {
     const int BW = cfg.bw(R);
     const int HF = ((TY + 2 * R) * BW + 31) & ~31;
     const int CF = TY * 32;
-    const int SF = HF + (grad ? 5 : 4) * CF;
+    const int SF = HF + (grad ? 6 : 4) * CF;
     return static_cast<size_t>(cfg.stages) * SF * 4 + cfg.stages * 16 + 128;
 }
 

@@ -74,6 +74,7 @@ struct SweepMaps {          // TMA descriptors (3-D only)
     CUtensorMap uc;         // u1/u2 rows, centre box (32, TY, 1, 1)
     CUtensorMap c1, c2;     // coefficient fields, centre box
     CUtensorMap ut;         // GRAD: history rows, centre box
+    CUtensorMap gr;         // GRAD: the gradient field, centre box
 };
 
 struct SweepConfig {        // 3-D tiling, chosen by choose_config()

@@ -203,6 +203,7 @@ void build_maps(sfdb200_plan& p) {
     p.maps.c2 = make_map(p.c2, p.g, 1, 32, TY);
     if (p.grad_kind() && p.hist) p.maps.ut = make_map(p.hist, p.g, p.hist_rows, 32, TY);
     else p.maps.ut = p.maps.uc;
+    p.maps.gr = p.grad ? make_map(p.grad, p.g, 1, 32, TY) : p.maps.uc;
     p.maps_ready = true;
 }
 

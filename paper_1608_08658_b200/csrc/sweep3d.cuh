@@ -86,7 +86,7 @@ struct Tile {
     static constexpr int BW = TX + 2 * RA;                     // halo row pitch
     static constexpr int HF = ((TY + 2 * R) * BW + 31) & ~31;  // halo floats, 128 B multiple
     static constexpr int CF = TY * TX;                         // centre box floats
-    static constexpr int NC = GRAD ? 5 : 4;                    // u1c, u2, c1, c2, [ut]
+    static constexpr int NC = GRAD ? 6 : 4;                    // u1c, u2, c1, c2, [ut, grad]
     static constexpr int SF = HF + NC * CF;                    // floats per stage
     // Bytes the TMA boxes of one stage deliver (the mbarrier transaction count).
     static constexpr uint32_t BYTES = static_cast<uint32_t>((TY + 2 * R) * BW + NC * CF) * 4u;
@@ -126,7 +126,8 @@ __global__ void __launch_bounds__(32 * (BY + 1), 4)
                    const __grid_constant__ CUtensorMap tm_uc,
                    const __grid_constant__ CUtensorMap tm_c1,
                    const __grid_constant__ CUtensorMap tm_c2,
-                   const __grid_constant__ CUtensorMap tm_ut, const SweepArgs a, const int Px,
+                   const __grid_constant__ CUtensorMap tm_ut,
+                   const __grid_constant__ CUtensorMap tm_gr, const SweepArgs a, const int Px,
                    const int Py, const long long py, const long long pz) {
     using T = Tile<R, BY, NY, GRAD>;
     constexpr int Q = T::Q;
@@ -156,7 +157,10 @@ __global__ void __launch_bounds__(32 * (BY + 1), 4)
         tma_load_4d(sb + T::HF + T::CF, &tm_uc, x0, y0, z, a.row_u2, bar);
         tma_load_4d(sb + T::HF + 2 * T::CF, &tm_c1, x0, y0, z, 0, bar);
         tma_load_4d(sb + T::HF + 3 * T::CF, &tm_c2, x0, y0, z, 0, bar);
-        if constexpr (GRAD) tma_load_4d(sb + T::HF + 4 * T::CF, &tm_ut, x0, y0, z, a.row_ut, bar);
+        if constexpr (GRAD) {
+            tma_load_4d(sb + T::HF + 4 * T::CF, &tm_ut, x0, y0, z, a.row_ut, bar);
+            tma_load_4d(sb + T::HF + 5 * T::CF, &tm_gr, x0, y0, z, 0, bar);
+        }
     };
 
     if (tid == 0) {
@@ -248,6 +252,7 @@ __global__ void __launch_bounds__(32 * (BY + 1), 4)
         const float* C1 = U2 + T::CF;
         const float* C2 = C1 + T::CF;
         const float* UT = C2 + T::CF;
+        const float* GR = UT + T::CF;  // the gradient plane, staged like the rest
         const int ca = ly0 * T::TX + lx, cb = ca + T::HALF * T::TX;
 
 #pragma unroll
@@ -293,8 +298,8 @@ __global__ void __launch_bounds__(32 * (BY + 1), 4)
                 // grad += -(1/dt^2) u_t (v_t - 2 v_{t+1} + v_{t+2}) = nidt2 * u_t * (inc - d)
                 const float2 vtt = fma2(d, mone, inc);
                 const float2 coef = mul2(nidt2, f2(UT[ia], UT[ib]));
-                if (va[j]) ga[off] = fmaf(coef.x, vtt.x, ga[off]);
-                if (vb[j]) gb[off] = fmaf(coef.y, vtt.y, gb[off]);
+                if (va[j]) ga[off] = fmaf(coef.x, vtt.x, GR[ia]);
+                if (vb[j]) gb[off] = fmaf(coef.y, vtt.y, GR[ib]);
             }
         }
 
@@ -372,7 +377,7 @@ cudaError_t launch3d_t(const FieldGeom& g, const SweepConfig& cfg, const SweepMa
     if (occ) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, kern, 32 * (BY + 1), smem);
     dim3 grid(cfg.tiles_x, cfg.tiles_y, cfg.zchunks);
     dim3 block(32, BY + 1);  // BY consumer warps + the TMA producer warp
-    kern<<<grid, block, smem, s>>>(m.uh, m.uc, m.c1, m.c2, m.ut, a, g.Px, g.Py, g.py, g.pz);
+    kern<<<grid, block, smem, s>>>(m.uh, m.uc, m.c1, m.c2, m.ut, m.gr, a, g.Px, g.Py, g.py, g.pz);
     return cudaGetLastError();
 }
 
