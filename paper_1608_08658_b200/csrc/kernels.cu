@@ -19,8 +19,12 @@
 // straight from registers with 128-byte coalesced rows.
 #include "kernels.cuh"
 
+#include <cooperative_groups.h>
+
 #include <cmath>
 #include <utility>
+
+namespace cg = cooperative_groups;
 
 namespace sfdb200 {
 namespace {
@@ -49,6 +53,93 @@ __global__ void __launch_bounds__(256) sweep2d_kernel(const SweepArgs a, const i
     const float inc = fmaf(__ldg(a.c1 + o), d, __ldg(a.c2 + o) * lap);
     a.out[o] = c0 + inc;
     if constexpr (GRAD) a.grad[o] = fmaf(a.nidt2 * __ldg(a.ut + o), inc - d, a.grad[o]);
+}
+
+// ---------------------------------------------------------------- 2-D time loop
+// 2-D problems are small (cfg1: 78,961 updated points, 0.3 MB per row, all in
+// L2), so a launch per step would be launch-bound.  One cooperative launch
+// runs every step: each CTA owns a contiguous range of updated points; per
+// step it samples its share of the previous row's receivers, sweeps its
+// points, applies the injections whose corner it owns (after a CTA barrier,
+// in the reference's (p, c) order, atomics for collisions) and meets the rest
+// of the grid at grid.sync().  Field rows are written inside the launch, so
+// they are read with ld.global.cg (L2, never a stale L1 line); c1, c2 and the
+// history are read-only.
+
+template <int R, bool GRAD>
+__global__ void __launch_bounds__(256) loop2d_kernel(const Loop2dArgs a) {
+    cg::grid_group grid = cg::this_grid();
+    const int cta = blockIdx.x;
+    const int tid = threadIdx.x;
+    const int nth = blockDim.x;
+    const int nx = a.Px - 2 * R;
+    const long long p0 = static_cast<long long>(cta) * a.per_cta;
+    const long long p1 = min(p0 + a.per_cta, a.npts);
+    const bool fwd = a.kind == 0;
+    const long steps = a.nt > 2 ? a.nt - 2 : 0;
+    const int e_begin = a.inj_n ? a.inj_begin[cta] : 0;
+    const int e_end = a.inj_n ? a.inj_begin[cta + 1] : 0;
+    auto sample = [&](const float* field, long row) {
+        const long q0 = static_cast<long>(cta) * a.smp_per_cta;
+        const long q1 = min(q0 + a.smp_per_cta, a.smp_cnt);
+        for (long q = q0 + tid; q < q1; q += nth) {
+            float acc = 0.0f;
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+                acc = fmaf(__ldg(a.smp_w + 4 * q + c), __ldcg(field + a.smp_off[4 * q + c]), acc);
+            a.smp_trace[row * a.smp_n + a.smp_pt[q]] = acc;
+        }
+    };
+    long prev_row = -1;
+    const float* prev_out = nullptr;
+    for (long i = 0; i < steps; ++i) {
+        const long t = fwd ? 2 + i : a.nt - 1 - i;
+        long r0, r1, r2;
+        if (fwd && a.save) {
+            r0 = t; r1 = t - 1; r2 = t - 2;
+        } else if (fwd) {
+            r0 = t % 3; r1 = (t - 1) % 3; r2 = (t - 2) % 3;
+        } else {
+            r0 = t % 3; r1 = (t + 1) % 3; r2 = (t + 2) % 3;
+        }
+        float* out = a.field + r0 * a.slot;
+        const float* u1 = a.field + r1 * a.slot;
+        const float* u2 = a.field + r2 * a.slot;
+        const float* ut = GRAD ? a.hist + t * a.slot : nullptr;
+        if (prev_out && a.smp_cnt) sample(prev_out, prev_row);
+        for (long long p = p0 + tid; p < p1; p += nth) {
+            const long long z = R + p / nx, x = R + p % nx;
+            const long long o = z * a.pz + x;
+            const float c0 = __ldcg(u1 + o);
+            float lap = 0.0f;
+#pragma unroll
+            for (int k = 1; k <= R; ++k) {
+                float s = (__ldcg(u1 + o - k) + __ldcg(u1 + o + k)) +
+                          (__ldcg(u1 + o - k * a.pz) + __ldcg(u1 + o + k * a.pz));
+                s = fmaf(a.neg2nd, c0, s);
+                lap = fmaf(a.w[k], s, lap);
+            }
+            const float d = c0 - __ldcg(u2 + o);
+            const float inc = fmaf(__ldg(a.c1 + o), d, __ldg(a.c2 + o) * lap);
+            out[o] = c0 + inc;
+            if constexpr (GRAD) a.grad[o] = fmaf(a.nidt2 * __ldg(ut + o), inc - d, a.grad[o]);
+        }
+        if (e_end > e_begin) {
+            __syncthreads();
+            const long irow = fwd ? t - 1 : t;
+            for (int e = e_begin + tid; e < e_end; e += nth) {
+                const long long o = a.inj_off[e];
+                const float delta = a.inj_coef[e] * __ldg(a.inj_trace + irow * a.inj_n + a.inj_pt[e]);
+                atomicAdd(out + o, delta);
+                if constexpr (GRAD)
+                    if (a.inj_gm[e]) atomicAdd(a.grad + o, a.nidt2 * __ldg(ut + o) * delta);
+            }
+        }
+        grid.sync();
+        prev_row = fwd ? t : t - 1;
+        prev_out = out;
+    }
+    if (prev_out && a.smp_cnt) sample(prev_out, prev_row);
 }
 
 // ---------------------------------------------------------------- sparse ops
@@ -197,6 +288,60 @@ cudaError_t launch_sweep2d(const FieldGeom& g, const SweepArgs& a, bool grad, cu
     }
 #undef SFDB_R_CASE
     return cudaGetLastError();
+}
+
+cudaError_t launch_loop2d(const Loop2dArgs& a, int R, bool grad, int ctas, cudaStream_t s) {
+    void* args[] = {const_cast<Loop2dArgs*>(&a)};
+    void* fn = nullptr;
+#define SFDB_R_CASE(RR)                                                                     \
+    case RR:                                                                                \
+        fn = grad ? reinterpret_cast<void*>(loop2d_kernel<RR, true>)                        \
+                  : reinterpret_cast<void*>(loop2d_kernel<RR, false>);                      \
+        break;
+    switch (R) {
+        SFDB_R_CASE(1)
+        SFDB_R_CASE(2)
+        SFDB_R_CASE(3)
+        SFDB_R_CASE(4)
+        SFDB_R_CASE(5)
+        SFDB_R_CASE(6)
+        SFDB_R_CASE(7)
+        SFDB_R_CASE(8)
+        default:
+            return cudaErrorInvalidValue;
+    }
+#undef SFDB_R_CASE
+    if (ctas < 0) {  // query: co-resident CTAs per SM
+        int occ = 0;
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 256, 0);
+        return e != cudaSuccess ? e : (occ > 0 ? cudaSuccess : cudaErrorInvalidConfiguration);
+    }
+    return cudaLaunchCooperativeKernel(fn, dim3(ctas), dim3(256), args, 0, s);
+}
+
+int loop2d_blocks_per_sm(int R, bool grad) {
+    void* fn = nullptr;
+#define SFDB_R_CASE(RR)                                                                     \
+    case RR:                                                                                \
+        fn = grad ? reinterpret_cast<void*>(loop2d_kernel<RR, true>)                        \
+                  : reinterpret_cast<void*>(loop2d_kernel<RR, false>);                      \
+        break;
+    switch (R) {
+        SFDB_R_CASE(1)
+        SFDB_R_CASE(2)
+        SFDB_R_CASE(3)
+        SFDB_R_CASE(4)
+        SFDB_R_CASE(5)
+        SFDB_R_CASE(6)
+        SFDB_R_CASE(7)
+        SFDB_R_CASE(8)
+        default:
+            return 0;
+    }
+#undef SFDB_R_CASE
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 256, 0) != cudaSuccess) return 0;
+    return occ;
 }
 
 cudaError_t launch_inject(float* field, const long long* off, const float* coef, const int* pt,

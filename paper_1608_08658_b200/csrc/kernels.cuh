@@ -114,6 +114,40 @@ cudaError_t sweep3d_occupancy(const FieldGeom& g, const SweepConfig& cfg, bool g
                               int* blocks_per_sm);
 cudaError_t launch_sweep2d(const FieldGeom& g, const SweepArgs& a, bool grad, cudaStream_t s);
 
+// 2-D: the whole time loop in one cooperative launch (see kernels.cu).
+struct Loop2dArgs {
+    float* field;              // wavefield rows
+    long long slot, pz;        // elements per row, per z line
+    const float* c1;
+    const float* c2;
+    const float* hist;         // GRAD: u history rows
+    float* grad;               // GRAD
+    int kind, save;            // 0 forward, 1 adjoint, 2 gradient; forward history rows
+    long nt;
+    float w[kMaxRadius + 1];
+    float neg2nd, nidt2;
+    int Px;
+    long long npts;            // updated points (Pz - 2R) * (Px - 2R)
+    long long per_cta;         // updated points per CTA
+    // injections owned by each CTA (CSR over CTAs), trace [nt][inj_n]
+    const int* inj_begin;
+    const long long* inj_off;
+    const float* inj_coef;
+    const int* inj_pt;
+    const unsigned char* inj_gm;
+    const float* inj_trace;
+    long inj_n;
+    // sampling: smp_cnt points [n][4] spread over the CTAs, trace [nt][smp_n]
+    const long long* smp_off;
+    const float* smp_w;
+    const int* smp_pt;
+    long smp_cnt, smp_per_cta;
+    float* smp_trace;
+    long smp_n;
+};
+cudaError_t launch_loop2d(const Loop2dArgs& a, int R, bool grad, int ctas, cudaStream_t s);
+int loop2d_blocks_per_sm(int R, bool grad);
+
 // Sparse operators over flat entry lists: off = element offset of a corner
 // inside one row, coef = w dt^2 / m[corner] (inject), pt = the entry's point
 // (trace column).

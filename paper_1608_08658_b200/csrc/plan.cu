@@ -283,6 +283,14 @@ void create(const sfdb200_desc& gd, Comm* comm, sfdb200_plan& p) {
     for (SparseDev* s : {&p.src, &p.rec})
         s->trace = dalloc<float>(static_cast<size_t>(d.nt * s->n));
     if (g.ndim == 3) choose_config(p);
+    if (g.ndim == 2) {  // cooperative time loop: all CTAs co-resident, ~1 point per thread
+        const long long npts = static_cast<long long>(g.Pz - 2 * R) * (g.Px - 2 * R);
+        const int occ = loop2d_blocks_per_sm(R, p.grad_kind());
+        if (occ < 1) fail(SFDB200_ECUDA, "2-D time loop kernel cannot be resident");
+        p.ctas2d = static_cast<int>(std::max<long long>(
+            1, std::min<long long>(static_cast<long long>(occ) * p.sms, (npts + 255) / 256)));
+        p.per_cta2d = (npts + p.ctas2d - 1) / p.ctas2d;
+    }
     if (!p.grad_kind()) build_maps(p);
     ck(cudaStreamSynchronize(p.stream), "plan setup");
 }
@@ -626,10 +634,63 @@ void exec_end(sfdb200_plan& p, StepState& st) {
     ck(cudaGetLastError(), "execute");
 }
 
+// 2-D: the whole time loop is one cooperative launch (kernels.cu loop2d_kernel).
+void execute_2d(sfdb200_plan& p) {
+    const sfdb200_desc& d = p.d;
+    const FieldGeom& g = p.g;
+    SparseDev& inj = p.injected();
+    SparseDev* smp = sampled_nonempty(p);
+    Loop2dArgs a{};
+    a.field = p.field;
+    a.slot = g.slot;
+    a.pz = g.pz;
+    a.c1 = p.c1;
+    a.c2 = p.c2;
+    a.hist = p.hist;
+    a.grad = p.grad;
+    a.kind = d.kind;
+    a.save = d.save;
+    a.nt = d.nt;
+    for (int k = 0; k <= g.R; ++k) a.w[k] = p.base.w[k];
+    a.neg2nd = p.base.neg2nd;
+    a.nidt2 = p.base.nidt2;
+    a.Px = g.Px;
+    a.npts = static_cast<long long>(g.Pz - 2 * g.R) * (g.Px - 2 * g.R);
+    a.per_cta = p.per_cta2d;
+    if (inj.n && inj.f_tab) {
+        a.inj_begin = inj.f_tab;
+        a.inj_off = inj.f_off;
+        a.inj_coef = inj.f_coef;
+        a.inj_pt = inj.f_pt;
+        a.inj_gm = inj.f_gm;
+        a.inj_trace = inj.trace;
+        a.inj_n = inj.n;
+    }
+    if (smp) {
+        a.smp_off = smp->smp_all.off;
+        a.smp_w = smp->smp_all.w;
+        a.smp_pt = smp->smp_all.pt;
+        a.smp_cnt = smp->smp_all.n;
+        a.smp_per_cta = (smp->smp_all.n + p.ctas2d - 1) / p.ctas2d;
+        a.smp_trace = smp->trace;
+        a.smp_n = smp->n;
+    }
+    if (p.steps() == 0) return;
+    if (p.timing) ck(cudaEventRecord(p.events[0], p.stream), "event");
+    ck(launch_loop2d(a, g.R, p.grad_kind(), p.ctas2d, p.stream), "loop2d");
+    if (p.timing) ck(cudaEventRecord(p.events[1], p.stream), "event");
+    p.timed_launches = 1;
+    p.launches = 1;
+}
+
 void do_execute(sfdb200_plan& p) {
     if (p.dist() && comm_loopback(p.comm))
         fail(SFDB200_EINVAL, "loopback ranks run through sfdb200_execute_group");
     exec_begin(p);
+    if (p.g.ndim == 2) {
+        execute_2d(p);
+        return;
+    }
     StepState st;
     for (long i = 0; i < p.steps(); ++i) {
         step_setup(p, i, st);

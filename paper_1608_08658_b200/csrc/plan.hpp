@@ -130,6 +130,8 @@ struct sfdb200_plan {
     int world = 1, rank = 0;
     long zoff = 0;
     int zint_lo = 0, zint_hi = 0;  // interior sweep launch (local planes)
+    int ctas2d = 0;                // 2-D: cooperative time-loop grid
+    long long per_cta2d = 0;       // 2-D: updated points per CTA
     sfdb200::Comm* comm = nullptr;
     cudaStream_t cstream = nullptr;
     cudaEvent_t ev_b = nullptr, ev_x = nullptr;

@@ -115,7 +115,39 @@ void upload_sparse(sfdb200_plan& p, SparseDev& s, const long* idx, const double*
                         (nd == 2 || (k.y >= R && k.y < g.Py - R));
         }
 
-    if (is_inj) {
+    if (is_inj && nd == 2) {
+        // 2-D time loop: entries grouped by the CTA owning the corner's point
+        // (CSR in f_tab), reference (p, c) order within a CTA; halo corners
+        // (never swept) go to CTA 0.
+        const long nx = g.Px - 2L * R;
+        struct E { int cta; size_t i; };
+        std::vector<E> es;
+        for (size_t i = 0; i < cs.size(); ++i) {
+            const Corner& k = cs[i];
+            int cta = 0;
+            if (k.updated) cta = static_cast<int>(((k.zl - R) * nx + (k.x - R)) / p.per_cta2d);
+            es.push_back({cta, i});
+        }
+        std::stable_sort(es.begin(), es.end(), [](const E& a, const E& b) { return a.cta < b.cta; });
+        std::vector<int> begin(static_cast<size_t>(p.ctas2d) + 1, 0), ept;
+        std::vector<long long> eoff;
+        std::vector<float> ecoef;
+        std::vector<unsigned char> egm;
+        for (const E& e : es) {
+            const Corner& k = cs[e.i];
+            ++begin[static_cast<size_t>(e.cta) + 1];
+            eoff.push_back(k.off);
+            ecoef.push_back(static_cast<float>(w[e.i] * (gd.dt * gd.dt) / m[k.dense]));
+            ept.push_back(static_cast<int>(e.i / C));
+            egm.push_back(k.updated ? 1 : 0);
+        }
+        for (int c = 0; c < p.ctas2d; ++c) begin[static_cast<size_t>(c) + 1] += begin[static_cast<size_t>(c)];
+        s.f_tab = s.upload(begin, st);
+        s.f_off = s.upload(eoff, st);
+        s.f_coef = s.upload(ecoef, st);
+        s.f_pt = s.upload(ept, st);
+        s.f_gm = s.upload(egm, st);
+    } else if (is_inj) {
         // coef = w * dt^2 / m[corner]: the reference's v = w; v *= scale;
         // v /= m with the data factor applied on the device (interpreter.cpp:144-147).
         struct E { Owner o; size_t i; };
