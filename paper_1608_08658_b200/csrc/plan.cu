@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -49,7 +50,10 @@ sfdb200_plan::~sfdb200_plan() {
         s->free_tables();
     }
     cudaFree(staging);
+    cudaFree(xstaging);
     cudaFree(counter);
+    if (ev_flush) cudaEventDestroy(ev_flush);
+    if (xstream) cudaStreamDestroy(xstream);
     for (cudaEvent_t e : events) cudaEventDestroy(e);
     if (ev_b) cudaEventDestroy(ev_b);
     if (ev_x) cudaEventDestroy(ev_x);
@@ -125,15 +129,9 @@ void validate(const sfdb200_desc& d) {
 }
 
 // 3-D tiling of the interior launch [zint_lo, zint_hi): 32-column x tiles,
-// TY-row y tiles, and z chunks sized so the grid fills the CTA slots.
-//
-// The grid must fit in ONE wave (all CTAs co-resident: they then march through
-// z in lockstep fronts, so neighbouring tiles' halo planes are still in L2 when
-// read) and spread evenly over the SMs.  Among the compiled variants (rows per
-// thread, pipeline depth) and z-chunk counts, take the best
-//   score = SM balance (avg / max CTAs per SM) * latency cover (CTAs per SM,
-//           saturating at 3) * z efficiency (chunk / (chunk + R): the queue
-//           prologue re-reads R planes a side per chunk).
+// TY-row y tiles, and z chunks.  Among the compiled variants (rows per thread,
+// pipeline depth) and z-chunk counts, take the one a wave model predicts
+// fastest (below); autotune() then measures the candidates on the device.
 void choose_config(sfdb200_plan& p) {
     const int R = p.g.R;
     const int zupd = std::max(1, p.zint_hi - p.zint_lo);
@@ -683,10 +681,40 @@ void execute_2d(sfdb200_plan& p) {
     p.launches = 1;
 }
 
+// Forward run(): trace rows [p.flushed, upto) are final; convert and copy them
+// to the caller's record on the copy stream while the time loop goes on.
+void flush_rows(sfdb200_plan& p, long upto) {
+    SparseDev& s = p.rec;
+    if (!p.host_rec || upto <= p.flushed || !s.n) return;
+    const long long n = (upto - p.flushed) * s.n;
+    if (static_cast<size_t>(n) > p.xstaging_elems) {  // sized for the whole record once
+        ck(cudaStreamSynchronize(p.xstream), "flush");
+        cudaFree(p.xstaging);
+        p.xstaging = nullptr;
+        p.xstaging_elems = static_cast<size_t>(p.d.nt * s.n);
+        p.xstaging = dalloc<double>(p.xstaging_elems);
+    }
+    ck(cudaEventRecord(p.ev_flush, p.stream), "event");
+    ck(cudaStreamWaitEvent(p.xstream, p.ev_flush, 0), "wait");
+    const long long off = p.flushed * s.n;
+    ck(launch_dense_to_f64(s.trace + off, p.xstaging + off, n, p.xstream), "convert");
+    ck(cudaMemcpyAsync(p.host_rec + off, p.xstaging + off, n * 8, cudaMemcpyDeviceToHost,
+                       p.xstream), "D2H");
+    p.d2h += n * 8;
+    p.flushed = upto;
+}
+
 void do_execute(sfdb200_plan& p) {
     if (p.dist() && comm_loopback(p.comm))
         fail(SFDB200_EINVAL, "loopback ranks run through sfdb200_execute_group");
     exec_begin(p);
+    p.flushed = 0;
+    const bool stream_out = p.host_rec && p.g.ndim == 3 && p.d.kind == SFDB200_FORWARD &&
+                            p.fused && !p.dist() && p.rec.n;
+    if (stream_out && !p.xstream) {
+        ck(cudaStreamCreateWithFlags(&p.xstream, cudaStreamNonBlocking), "cudaStreamCreate");
+        ck(cudaEventCreateWithFlags(&p.ev_flush, cudaEventDisableTiming), "cudaEventCreate");
+    }
     if (p.g.ndim == 2) {
         execute_2d(p);
         return;
@@ -704,6 +732,8 @@ void do_execute(sfdb200_plan& p) {
         phase_interior(p, i, st);
         if (p.dist()) ck(cudaStreamWaitEvent(p.stream, p.ev_x, 0), "wait");
         phase_samples(p, st);
+        // forward: rows < t are final once step t's sweep sampled row t-1
+        if (stream_out && i % 64 == 63) flush_rows(p, 2 + i);
     }
     exec_end(p, st);
 }
@@ -768,7 +798,14 @@ void do_download(sfdb200_plan& p, void** argv) {
         check_finite(p, s->trace, d.nt * s->n,
                      d.kind == SFDB200_FORWARD ? "the receiver record" : "the source samples");
     if (argv[0]) download_rows(p, p.field, static_cast<double*>(argv[0]), p.rows);
-    if (d.kind == SFDB200_FORWARD && argv[8]) download_trace(p, p.rec, static_cast<double*>(argv[8]));
+    if (d.kind == SFDB200_FORWARD && argv[8]) {
+        if (p.host_rec == argv[8] && p.flushed > 0) {  // rows streamed during the run
+            flush_rows(p, d.nt);
+            ck(cudaStreamSynchronize(p.xstream), "D2H");
+        } else {
+            download_trace(p, p.rec, static_cast<double*>(argv[8]));
+        }
+    }
     if (d.kind == SFDB200_ADJOINT && argv[5]) download_trace(p, p.src, static_cast<double*>(argv[5]));
     if (d.kind == SFDB200_GRADIENT && argv[4])
         download_rows(p, p.grad, static_cast<double*>(argv[4]), 1);
@@ -853,9 +890,33 @@ int sfdb200_run(sfdb200_plan* p, void** argv) {
     return guarded([&] {
         if (!p || !argv) fail(SFDB200_EINVAL, "null argument");
         ck(cudaSetDevice(p->d.device), "cudaSetDevice");
+        const bool prof = env_int("SFDB200_PROFILE", 0) != 0;
+        auto now = [&] {
+            if (prof) cudaStreamSynchronize(p->stream);
+            return std::chrono::steady_clock::now();
+        };
+        const auto t0 = now();
         do_upload(*p, argv);
-        do_execute(*p);
+        const auto t1 = now();
+        p->host_rec = p->d.kind == SFDB200_FORWARD ? static_cast<double*>(argv[8]) : nullptr;
+        p->d2h = 0;
+        try {
+            do_execute(*p);
+        } catch (...) {
+            p->host_rec = nullptr;
+            throw;
+        }
+        const auto t2 = now();
+        const long streamed = p->d2h;
         do_download(*p, argv);
+        p->d2h += streamed;
+        p->host_rec = nullptr;
+        const auto t3 = now();
+        if (prof) {
+            auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+            std::fprintf(stderr, "sfdb200_run: upload %.2f ms (%ld B), execute %.2f ms, download %.2f ms (%ld B)\n",
+                         ms(t0, t1), p->h2d, ms(t1, t2), ms(t2, t3), p->d2h);
+        }
     });
 }
 

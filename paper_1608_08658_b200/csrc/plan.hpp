@@ -57,6 +57,7 @@ struct SparseDev {
     long n = 0;                // points in the (global) set
     float* trace = nullptr;    // [nt][n]
     std::vector<void*> bufs;   // device buffers owned by the tables below
+    unsigned long long key = 0;  // fingerprint of the inputs the tables were built from
 
     // Injection: entries of the interior sweep launch, per (CTA, plane)
     // (fused into the sweep), and the rest (boundary / halo planes, or every
@@ -91,6 +92,7 @@ struct SparseDev {
     void free_tables() {
         for (void* q : bufs) cudaFree(q);
         bufs.clear();
+        key = 0;
         f_tab = nullptr; f_rng = nullptr; f_off = nullptr; f_coef = nullptr; f_pt = nullptr;
         f_gm = nullptr;
         s_tab = nullptr; s_rng = nullptr; s_hidx = nullptr; s_w = nullptr; s_pt = nullptr;
@@ -155,6 +157,15 @@ struct sfdb200_plan {
     bool maps_ready = false;
     bool fused = true;
     bool tuned = false;
+
+    // run(): completed receiver rows stream to the caller's host record during
+    // the time loop (copy stream + its own staging), the rest at download.
+    double* host_rec = nullptr;
+    long flushed = 0;
+    double* xstaging = nullptr;
+    size_t xstaging_elems = 0;
+    cudaStream_t xstream = nullptr;
+    cudaEvent_t ev_flush = nullptr;
 
     bool timing = false;
     std::vector<cudaEvent_t> events;
