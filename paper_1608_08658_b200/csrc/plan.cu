@@ -353,8 +353,8 @@ void autotune(sfdb200_plan& p) {
     p.tuned = true;
     const int R = p.g.R;
     const int zupd = std::max(1, p.zint_hi - p.zint_lo);
-    std::vector<std::pair<int, int>> variants = {{2, 4}, {2, 3}, {1, 4}};  // (ny, stages)
-    if (R >= 6) variants = {{1, 4}, {1, 3}};
+    std::vector<std::pair<int, int>> variants = {{2, 3}, {2, 4}, {2, 6}, {1, 4}, {1, 6}};
+    if (R >= 6) variants = {{1, 3}, {1, 4}, {1, 6}};  // (ny, stages)
     const SweepConfig start = p.cfg;
     SweepArgs a = p.base;
     a.out = p.field;

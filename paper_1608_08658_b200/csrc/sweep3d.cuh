@@ -120,6 +120,47 @@ struct IC {
 // transaction bytes) and an "empty" one (one arrival per consumer warp once
 // it is done reading the stage), so no CTA-wide barrier runs per plane.
 
+// The fused sparse work of one plane, kept out of line: it runs on a handful
+// of planes, and inlined into every phase of the unrolled plane loop it would
+// only crowd the instruction cache.
+template <int BW, int NT>
+__device__ __noinline__ void sample_plane(const SweepArgs& a, const float* H, const int* stab,
+                                          int i, int tid) {
+    const int e1 = stab[i], e2 = stab[i + 1];
+    if (i > 0)
+        for (int e = stab[i - 1] + tid; e < e1; e += NT) {
+            const float* hp = H + a.smp_hidx[e];
+            const float* w = a.smp_w + 8LL * e + 4;
+            float acc = a.smp_acc[e];
+            acc = fmaf(__ldg(w + 0), hp[0], acc);
+            acc = fmaf(__ldg(w + 1), hp[1], acc);
+            acc = fmaf(__ldg(w + 2), hp[BW], acc);
+            acc = fmaf(__ldg(w + 3), hp[BW + 1], acc);
+            a.smp_row[a.smp_pt[e]] = acc;
+        }
+    for (int e = e1 + tid; e < e2; e += NT) {
+        const float* hp = H + a.smp_hidx[e];
+        const float* w = a.smp_w + 8LL * e;
+        float acc = __ldg(w + 0) * hp[0];
+        acc = fmaf(__ldg(w + 1), hp[1], acc);
+        acc = fmaf(__ldg(w + 2), hp[BW], acc);
+        acc = fmaf(__ldg(w + 3), hp[BW + 1], acc);
+        a.smp_acc[e] = acc;
+    }
+}
+
+template <bool GRAD, int NT>
+__device__ __noinline__ void inject_plane(const SweepArgs& a, const int* itab, int i, int tid) {
+    const int e0 = itab[i], e1 = itab[i + 1];
+    for (int e = e0 + tid; e < e1; e += NT) {
+        const long long o = a.inj_off[e];
+        const float delta = a.inj_coef[e] * __ldg(a.inj_row + a.inj_pt[e]);
+        atomicAdd(a.out + o, delta);
+        if constexpr (GRAD)
+            if (a.inj_gm[e]) atomicAdd(a.grad + o, a.nidt2 * __ldg(a.ut + o) * delta);
+    }
+}
+
 template <int R, int BY, int NY, int S, bool GRAD, bool ROT>
 __global__ void __launch_bounds__(32 * (BY + 1), 4)
     sweep3d_kernel(const __grid_constant__ CUtensorMap tm_uh,
@@ -313,29 +354,7 @@ __global__ void __launch_bounds__(32 * (BY + 1), 4)
         // (corners 0..3) of receivers based on this plane, second halves
         // (4..7) of those based on the previous one.  Entry e is handled by
         // the same thread in both passes, so its half sum needs no barrier.
-        if (i >= srng.x && i < srng.y) {
-            const int e1 = stab[i], e2 = stab[i + 1];
-            if (i > 0)
-                for (int e = stab[i - 1] + tid; e < e1; e += NT) {
-                    const float* hp = H + a.smp_hidx[e];
-                    const float* w = a.smp_w + 8LL * e + 4;
-                    float acc = a.smp_acc[e];
-                    acc = fmaf(__ldg(w + 0), hp[0], acc);
-                    acc = fmaf(__ldg(w + 1), hp[1], acc);
-                    acc = fmaf(__ldg(w + 2), hp[T::BW], acc);
-                    acc = fmaf(__ldg(w + 3), hp[T::BW + 1], acc);
-                    a.smp_row[a.smp_pt[e]] = acc;
-                }
-            for (int e = e1 + tid; e < e2; e += NT) {
-                const float* hp = H + a.smp_hidx[e];
-                const float* w = a.smp_w + 8LL * e;
-                float acc = __ldg(w + 0) * hp[0];
-                acc = fmaf(__ldg(w + 1), hp[1], acc);
-                acc = fmaf(__ldg(w + 2), hp[T::BW], acc);
-                acc = fmaf(__ldg(w + 3), hp[T::BW + 1], acc);
-                a.smp_acc[e] = acc;
-            }
-        }
+        if (i >= srng.x && i < srng.y) sample_plane<T::BW, NT>(a, H, stab, i, tid);
         // Release the stage to the producer (one arrival per consumer warp).
         __syncwarp();
         if (lx == 0) mbar_arrive(&empty[st]);
@@ -343,14 +362,7 @@ __global__ void __launch_bounds__(32 * (BY + 1), 4)
         // plane (named barrier over the consumer warps only).
         if (i >= irng.x && i < irng.y) {
             named_barrier_sync(1, NT);
-            const int e0 = itab[i], e1 = itab[i + 1];
-            for (int e = e0 + tid; e < e1; e += NT) {
-                const long long o = a.inj_off[e];
-                const float delta = a.inj_coef[e] * __ldg(a.inj_row + a.inj_pt[e]);
-                atomicAdd(a.out + o, delta);
-                if constexpr (GRAD)
-                    if (a.inj_gm[e]) atomicAdd(a.grad + o, a.nidt2 * __ldg(a.ut + o) * delta);
-            }
+            inject_plane<GRAD, NT>(a, itab, i, tid);
         }
     };
 
@@ -390,8 +402,10 @@ cudaError_t launch3d_r(const FieldGeom& g, const SweepConfig& cfg, const SweepMa
         return launch3d_t<R, BY, NY, S, GRAD>(g, cfg, m, a, s, occ);
     SFDB_V(4, 2, 4)
     SFDB_V(4, 2, 3)
+    SFDB_V(4, 2, 6)
     SFDB_V(4, 1, 4)
     SFDB_V(4, 1, 3)
+    SFDB_V(4, 1, 6)
 #undef SFDB_V
     return cudaErrorInvalidConfiguration;
 }
