@@ -155,3 +155,20 @@ def test_synthetic_configs_have_the_baseline_shapes():
     w5 = configs.cfg4(16, n=16, nt=12, nbpml=4)
     m = S.make_model(w5.interior, w5.h, w5.nbpml, 16, w5.m_interior)
     assert w5.dt <= S.critical_dt(m)
+
+
+def test_cli_config_patch_and_refusal(tmp_path):
+    """sfd.cpp:58-78 (--set) and :555-565 (refusal -> exit 2 with a summary)."""
+    from paper_1608_08658_b200 import cli
+    p = cli.build_patch("", ["interior=[9,9]", "h=12.5", "source.0=3", "kernel=adjoint"])
+    assert p == {"interior": [9, 9], "h": 12.5, "source": {"0": 3}, "kernel": "adjoint"}
+    ex = cli.build_experiment({"interior": [20, 24], "nbpml": 4, "space_order": 4,
+                               "receivers": 3, "time": 0.05})
+    assert ex["rec"].npoints == 3 and ex["nt"] >= 4
+    assert ex["dt"] == 0.9 * S.critical_dt(ex["model"])
+    rc = cli.main(["--out", str(tmp_path), "--set", "dt=1.0", "--set", "interior=[9,9]",
+                   "run"])
+    assert rc == 2
+    import json as _json
+    summ = _json.load(open(tmp_path / "summary.json"))
+    assert summ["command"] == "error" and "CFL" in summ["error"]
