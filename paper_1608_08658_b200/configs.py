@@ -112,6 +112,18 @@ def cfg2(n=256, nt=1002, nbpml=40, nrec_side=256):
                     _carpet(nrec_side, span, 20.0), h, nbpml, 12.0)
 
 
+def cfg2_stacked(copies, n=256, nt=1002, nbpml=40, nrec_side=256):
+    """Weak-scaling form of cfg2 for N GPUs: the cfg2 model repeated `copies`
+    times along z (interior n*copies x n x n), same source, receivers and
+    steps, so every z-slab rank carries one cfg2-sized slab."""
+    w = cfg2(n, nt, nbpml, nrec_side)
+    if copies == 1:
+        return w
+    m = np.tile(w.m_interior.reshape(n, n, n), (copies, 1, 1)).ravel()
+    return Workload(f"cfg2-3d-so8-x{copies}", 3, [n * copies, n, n], 8, w.nt, w.dt, m,
+                    w.wavelet, w.src_coords, w.rec_coords, w.h, nbpml, w.f0)
+
+
 def cfg3(n=200, nt=802, nbpml=40, nrec_side=200):
     """3-D FWI gradient: background + Gaussian anomaly (BASELINE configs[2]).
     Returns (true workload, background m)."""
