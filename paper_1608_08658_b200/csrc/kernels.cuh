@@ -79,11 +79,14 @@ struct SweepMaps {          // TMA descriptors (3-D only)
 
 struct SweepConfig {        // 3-D tiling, chosen by choose_config()
     int by = 4;             // warps per CTA (each warp: 32 x-columns)
-    int ny = 2;             // y rows per thread in each tile half (tile is 2*by*ny rows)
+    int ny = 2;             // y rows per thread in each tile half (tile is 2*by*ny rows);
+                            // pair mapping: rows per thread (two row groups per warp)
     int stages = 4;         // TMA pipeline depth
     int rot = 1;            // z loop unrolled by 2R+1 (register queue rotates by renaming)
     int zchunks = 1;        // CTAs along z per (x, y) tile
     int zlen = 1;           // planes per z chunk
+    int pdl = 1;            // programmatic dependent launch (overlap launch + CTA setup)
+    int pair = 0;           // thread owns column pairs x, x+1 (sweep3d_pair_kernel)
     int tiles_x = 0, tiles_y = 0;
     size_t smem_bytes = 0;
     int ty() const { return 2 * by * ny; }

@@ -128,6 +128,16 @@ void validate(const sfdb200_desc& d) {
     if (d.nsrc < 0 || d.nrec < 0) fail(SFDB200_EINVAL, "negative sparse-set size");
 }
 
+// Compiled sweep variants worth timing for radius R, best-first (B200
+// measurements, profiles/r01): the half-tile mapping up to R = 4, the
+// column-pair mapping with a shifted (not renamed) z queue above, where the
+// fully unrolled queue rotation overflows the instruction cache.
+struct V { int by, ny, stages, pair = 0, rot = 1; };
+std::vector<V> sweep_variants(int R) {
+    if (R <= 4) return {{4, 2, 3}, {4, 2, 4}, {4, 2, 6}, {4, 1, 4}, {4, 1, 6}, {4, 2, 3, 1, 0}};
+    return {{4, 2, 4, 1, 0}, {4, 2, 3, 1, 0}, {8, 2, 3, 1, 1}, {4, 1, 4, 1, 0}, {4, 1, 4}, {4, 1, 3}};
+}
+
 // 3-D tiling of the interior launch [zint_lo, zint_hi): 32-column x tiles,
 // TY-row y tiles, and z chunks.  Among the compiled variants (rows per thread,
 // pipeline depth) and z-chunk counts, take the one a wave model predicts
@@ -135,13 +145,11 @@ void validate(const sfdb200_desc& d) {
 void choose_config(sfdb200_plan& p) {
     const int R = p.g.R;
     const int zupd = std::max(1, p.zint_hi - p.zint_lo);
-    struct V { int by, ny, stages; };
-    std::vector<V> variants = {{4, 2, 4}, {4, 2, 3}, {4, 1, 4}, {4, 1, 3}};
-    if (R >= 6) variants = {{4, 1, 4}, {4, 1, 3}};  // the 2R+1 float2 queue of ny = 2 spills
+    std::vector<V> variants = sweep_variants(R);
+    variants.resize(1);  // the measured best on B200 (autotune() times the rest)
     if (const char* t = std::getenv("SFDB200_TILE")) {
         V v{4, 2, 4};
-        int rot = 1;
-        std::sscanf(t, "%d,%d,%d,%d", &v.by, &v.ny, &v.stages, &rot);
+        std::sscanf(t, "%d,%d,%d,%d,%d", &v.by, &v.ny, &v.stages, &v.rot, &v.pair);
         variants = {v};
     }
     const int zc_env = env_int("SFDB200_ZCHUNKS", 0);
@@ -152,6 +160,8 @@ void choose_config(sfdb200_plan& p) {
         c.by = v.by;
         c.ny = v.ny;
         c.stages = v.stages;
+        c.pair = v.pair;
+        c.rot = v.pair ? v.rot : 1;
         c.tiles_x = static_cast<int>((p.g.Px - R + 31) / 32);  // tiles start at x = 0 (TMA alignment)
         c.tiles_y = static_cast<int>((p.g.Py - 2 * R + c.ty() - 1) / c.ty());
         c.smem_bytes = sweep3d_smem_bytes(R, c, p.grad_kind());
@@ -188,6 +198,7 @@ void choose_config(sfdb200_plan& p) {
         }
     }
     if (best < 0) fail(SFDB200_ECUDA, "no sweep variant fits this device");
+    pick.pdl = env_int("SFDB200_PDL", 1);
     p.cfg = pick;
 }
 
@@ -353,8 +364,7 @@ void autotune(sfdb200_plan& p) {
     p.tuned = true;
     const int R = p.g.R;
     const int zupd = std::max(1, p.zint_hi - p.zint_lo);
-    std::vector<std::pair<int, int>> variants = {{2, 3}, {2, 4}, {2, 6}, {1, 4}, {1, 6}};
-    if (R >= 6) variants = {{1, 3}, {1, 4}, {1, 6}};  // (ny, stages)
+    const std::vector<V> variants = sweep_variants(R);
     const SweepConfig start = p.cfg;
     SweepArgs a = p.base;
     a.out = p.field;
@@ -377,12 +387,14 @@ void autotune(sfdb200_plan& p) {
     ck(cudaEventCreate(&e1), "cudaEventCreate");
     float best = 1e30f;
     SweepConfig pick = start;
-    for (auto [ny, stages] : variants) {
+    for (const V& v : variants) {
         for (int zc = 1; zc <= std::min(8, std::max(1, zupd / (2 * R + 4))); ++zc) {
             SweepConfig c = start;
-            c.by = 4;
-            c.ny = ny;
-            c.stages = stages;
+            c.by = v.by;
+            c.ny = v.ny;
+            c.stages = v.stages;
+            c.pair = v.pair;
+            c.rot = v.rot;
             c.tiles_y = static_cast<int>((p.g.Py - 2 * R + c.ty() - 1) / c.ty());
             c.smem_bytes = sweep3d_smem_bytes(R, c, p.grad_kind());
             c.zlen = (zupd + zc - 1) / zc;
@@ -1081,10 +1093,12 @@ int sfdb200_plan_info(const sfdb200_plan* p, char* buf, long len) {
                       "{\"tile\": [32, %d], \"warps\": %d, \"rows_per_thread\": %d, "
                       "\"stages\": %d, \"tiles\": [%d, %d], \"zchunks\": %d, \"zlen\": %d, "
                       "\"smem_bytes\": %zu, \"fused_sparse\": %s, \"slab\": [%ld, %ld], "
-                      "\"x_pitch\": %d}",
+                      "\"x_pitch\": %d, \"mapping\": \"%s\", \"pdl\": %s}",
                       c.ty(), c.by + 1, 2 * c.ny, c.stages, c.tiles_x, c.tiles_y, c.zchunks,
                       c.zlen, c.smem_bytes, p->fused ? "true" : "false", p->zoff + p->g.R,
-                      p->zoff + p->g.Pz - p->g.R, p->g.XP);
+                      p->zoff + p->g.Pz - p->g.R, p->g.XP,
+                      c.pair ? "column pairs x ny rows" : "2 half-tiles x ny rows",
+                      c.pdl ? "true" : "false");
     });
 }
 

@@ -65,6 +65,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         if (++spins == (1u << 26)) __trap();
 }
 
+// Programmatic dependent launch: the next sweep may be scheduled once every
+// CTA of this one has started; it sets up its barriers and tables, then waits
+// here until this grid has completed and its stores are visible.
+__device__ __forceinline__ void pdl_trigger() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int c0, int c1,
                                             int c2, int c3, uint64_t* bar) {
     asm volatile(
@@ -204,6 +212,7 @@ __global__ void __launch_bounds__(32 * (BY + 1), 4)
         }
     };
 
+    pdl_trigger();
     if (tid == 0) {
 #pragma unroll
         for (int s = 0; s < S; ++s) {
@@ -214,6 +223,7 @@ __global__ void __launch_bounds__(32 * (BY + 1), 4)
     }
     __syncthreads();
     if (threadIdx.y == BY) {  // producer warp: one lane streams the planes
+        pdl_wait();
         if (lx == 0)
             for (int j = 0; j < n; ++j) {
                 const int st = j % S;
@@ -249,6 +259,9 @@ __global__ void __launch_bounds__(32 * (BY + 1), 4)
         prefetch(a.inj_coef + e0, 4LL * (e1 - e0));
         prefetch(a.inj_pt + e0, 4LL * (e1 - e0));
     }
+
+    // Everything below reads or writes rows the previous sweep touches.
+    pdl_wait();
 
     // Queue slot of plane zb - R + t is t mod Q.
     float2 q[NY][Q];
@@ -377,6 +390,234 @@ __global__ void __launch_bounds__(32 * (BY + 1), 4)
     }
 }
 
+// ---------------------------------------------------------------- pair mapping
+//
+// Same tile, TMA pipeline, fused sparse work and numerics as sweep3d_kernel,
+// but thread (px, gy) of warp wy owns the column PAIR x, x+1 (x = x0 + 2 px)
+// in NY consecutive rows r0 + j, r0 = (2 wy + gy) NY.  The float2 lanes are
+// the two columns, so every shared-memory read is an 8-byte LDS.64 (a
+// half-warp reads 128 contiguous bytes: conflict-free) and one x window of
+// 2R + 2 floats per row serves both points: per updated point the kernel
+// reads (2R + 2)/2 + 2R/NY + 4 floats of shared memory instead of
+// 2R + 2R/NY + 4, which is what bounds high space orders.  Odd
+// x offsets straddle two loaded pairs; the compiler pairs them with moves.
+__device__ __forceinline__ float2 ld2(const float* p) {
+    return *reinterpret_cast<const float2*>(p);
+}
+__device__ __forceinline__ void st2(float* p, float2 v) { *reinterpret_cast<float2*>(p) = v; }
+
+template <int R, int BY, int NY, int S, bool GRAD, int MINB, bool ROT>
+__global__ void __launch_bounds__(32 * (BY + 1), MINB)
+    sweep3d_pair_kernel(const __grid_constant__ CUtensorMap tm_uh,
+                        const __grid_constant__ CUtensorMap tm_uc,
+                        const __grid_constant__ CUtensorMap tm_c1,
+                        const __grid_constant__ CUtensorMap tm_c2,
+                        const __grid_constant__ CUtensorMap tm_ut,
+                        const __grid_constant__ CUtensorMap tm_gr, const SweepArgs a,
+                        const int Px, const int Py, const long long py, const long long pz) {
+    using T = Tile<R, BY, NY, GRAD>;
+    constexpr int Q = T::Q;
+    constexpr int WL = (R + 1) & ~1;  // x window [x - WL, x + 1 + WL], 8-byte aligned
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    float* smem = reinterpret_cast<float*>(smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * T::SF);
+    uint64_t* empty = full + S;
+    constexpr int NT = 32 * BY;
+
+    const int lx = threadIdx.x;
+    const int tid = threadIdx.y * 32 + lx;
+    const int x0 = blockIdx.x * T::TX;
+    const int y0 = R + blockIdx.y * T::TY;
+    const int zb = a.zlo + blockIdx.z * a.zchunk;
+    const int ze = min(zb + a.zchunk, a.zhi);
+    if (zb >= ze) return;
+    const int n = ze - zb;
+
+    auto issue = [&](int stage, int z) {
+        float* sb = smem + stage * T::SF;
+        uint64_t* bar = &full[stage];
+        mbar_arrive_expect_tx(bar, T::BYTES);
+        tma_load_4d(sb, &tm_uh, x0 - T::RA, y0 - R, z, a.row_u1, bar);
+        tma_load_4d(sb + T::HF, &tm_uc, x0, y0, z + R, a.row_u1, bar);
+        tma_load_4d(sb + T::HF + T::CF, &tm_uc, x0, y0, z, a.row_u2, bar);
+        tma_load_4d(sb + T::HF + 2 * T::CF, &tm_c1, x0, y0, z, 0, bar);
+        tma_load_4d(sb + T::HF + 3 * T::CF, &tm_c2, x0, y0, z, 0, bar);
+        if constexpr (GRAD) {
+            tma_load_4d(sb + T::HF + 4 * T::CF, &tm_ut, x0, y0, z, a.row_ut, bar);
+            tma_load_4d(sb + T::HF + 5 * T::CF, &tm_gr, x0, y0, z, 0, bar);
+        }
+    };
+
+    pdl_trigger();
+    if (tid == 0) {
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], BY);
+        }
+        fence_barrier_init();
+    }
+    __syncthreads();
+    if (threadIdx.y == BY) {
+        pdl_wait();
+        if (lx == 0)
+            for (int j = 0; j < n; ++j) {
+                const int st = j % S;
+                if (j >= S) mbar_wait(&empty[st], static_cast<uint32_t>((j / S - 1) & 1));
+                issue(st, zb + j);
+            }
+        return;
+    }
+
+    const int cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    const int* stab = a.smp_tab ? a.smp_tab + static_cast<long long>(cta) * (a.zchunk + 1) : nullptr;
+    const int* itab = a.inj_tab ? a.inj_tab + static_cast<long long>(cta) * (a.zchunk + 1) : nullptr;
+    const int2 srng = stab ? a.smp_rng[cta] : make_int2(0, 0);
+    const int2 irng = itab ? a.inj_rng[cta] : make_int2(0, 0);
+    auto prefetch = [&](const void* base, long long bytes) {
+        const char* b = static_cast<const char*>(base);
+        for (long long o = tid * 128LL; o < bytes; o += NT * 128LL)
+            asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(b + o));
+    };
+    if (srng.y > srng.x) {
+        const int e0 = stab[srng.x], e1 = stab[srng.y];
+        prefetch(a.smp_hidx + e0, 4LL * (e1 - e0));
+        prefetch(a.smp_pt + e0, 4LL * (e1 - e0));
+        prefetch(a.smp_w + 8LL * e0, 32LL * (e1 - e0));
+    }
+    if (irng.y > irng.x) {
+        const int e0 = itab[irng.x], e1 = itab[irng.y];
+        prefetch(a.inj_off + e0, 8LL * (e1 - e0));
+        prefetch(a.inj_coef + e0, 4LL * (e1 - e0));
+        prefetch(a.inj_pt + e0, 4LL * (e1 - e0));
+    }
+    pdl_wait();
+
+    const int px = lx & 15, gy = lx >> 4;
+    const int r0 = (threadIdx.y * 2 + gy) * NY;  // first tile row of this thread
+    const int x = x0 + 2 * px;
+    const bool vx0 = x >= R && x < Px - R, vx1 = x + 1 >= R && x + 1 < Px - R;
+    float2 q[NY][Q];
+    bool vy[NY];
+#pragma unroll
+    for (int j = 0; j < NY; ++j) {
+        const int y = y0 + r0 + j;
+        vy[j] = y < Py - R;
+        const float* c = a.u1 + static_cast<long long>(y) * py + x;
+#pragma unroll
+        for (int t = 0; t < 2 * R; ++t) {
+            const long long o = static_cast<long long>(zb - R + t) * pz;
+            q[j][t] = vy[j] ? __ldg(reinterpret_cast<const float2*>(c + o)) : f2(0.0f, 0.0f);
+        }
+    }
+
+    const float2 neg2nd = f2(a.neg2nd, a.neg2nd);
+    const float2 mone = f2(-1.0f, -1.0f);
+    float2 wk[R + 1];
+#pragma unroll
+    for (int k = 0; k <= R; ++k) wk[k] = f2(a.w[k], a.w[k]);
+    const float2 nidt2 = f2(a.nidt2, a.nidt2);
+    float* outp = a.out + static_cast<long long>(y0 + r0) * py + x;
+    float* gp = GRAD ? a.grad + static_cast<long long>(y0 + r0) * py + x : nullptr;
+    auto put = [&](float* p, float2 v) {
+        if (vx0 && vx1) {
+            st2(p, v);
+        } else {
+            if (vx0) p[0] = v.x;
+            if (vx1) p[1] = v.y;
+        }
+    };
+
+    auto plane = [&](auto ph_c, const int i) {
+        constexpr int PH = decltype(ph_c)::value;
+        auto slot = [](int off) { return ((PH + off + R) % Q + Q) % Q; };
+        const int st = i % S;
+        mbar_wait(&full[st], static_cast<uint32_t>((i / S) & 1));
+        const float* H = smem + st * T::SF;
+        const float* Cq = H + T::HF;
+        const float* U2 = Cq + T::CF;
+        const float* C1 = U2 + T::CF;
+        const float* C2 = C1 + T::CF;
+        const float* UT = C2 + T::CF;
+        const float* GR = UT + T::CF;
+        const int cidx = r0 * T::TX + 2 * px;
+#pragma unroll
+        for (int j = 0; j < NY; ++j) q[j][slot(R)] = ld2(Cq + cidx + j * T::TX);
+
+        const float* hp = H + (r0 + R) * T::BW + T::RA + 2 * px;  // (row r0, column x)
+        float2 yu[R], yd[R];  // rows r0 - k and r0 + NY - 1 + k
+#pragma unroll
+        for (int k = 1; k <= R; ++k) {
+            yu[k - 1] = ld2(hp - k * T::BW);
+            yd[k - 1] = ld2(hp + (NY - 1 + k) * T::BW);
+        }
+        const long long zoff = static_cast<long long>(zb + i) * pz;
+
+#pragma unroll
+        for (int j = 0; j < NY; ++j) {
+            float w[2 * WL + 2];
+#pragma unroll
+            for (int m = 0; m <= WL; ++m) {
+                const float2 v = ld2(hp + j * T::BW - WL + 2 * m);
+                w[2 * m] = v.x;
+                w[2 * m + 1] = v.y;
+            }
+            const float2 c0 = q[j][slot(0)];
+            // Two partial sums (odd / even k) halve the dependent FFMA2 chain.
+            float2 lap = f2(0.0f, 0.0f), lap2 = f2(0.0f, 0.0f);
+#pragma unroll
+            for (int k = 1; k <= R; ++k) {
+                const float2 ym = j - k >= 0 ? q[(j - k) >= 0 ? j - k : 0][slot(0)] : yu[k - j - 1];
+                const float2 yp = j + k < NY ? q[(j + k) < NY ? j + k : 0][slot(0)] : yd[j + k - NY];
+                const float2 xs = add2(f2(w[WL - k], w[WL - k + 1]), f2(w[WL + k], w[WL + k + 1]));
+                const float2 zs = add2(q[j][slot(-k)], q[j][slot(k)]);
+                float2 sk = add2(add2(xs, add2(ym, yp)), zs);
+                sk = fma2(neg2nd, c0, sk);
+                if (R >= 5 && (k & 1) == 0)
+                    lap2 = fma2(wk[k], sk, lap2);
+                else
+                    lap = fma2(wk[k], sk, lap);
+            }
+            if constexpr (R >= 5) lap = add2(lap, lap2);
+            const int ci = cidx + j * T::TX;
+            const float2 d = fma2(ld2(U2 + ci), mone, c0);
+            const float2 inc = fma2(ld2(C1 + ci), d, mul2(ld2(C2 + ci), lap));
+            const float2 o = add2(c0, inc);
+            const long long off = zoff + j * py;
+            if (vy[j]) put(outp + off, o);
+            if constexpr (GRAD) {
+                const float2 vtt = fma2(d, mone, inc);
+                const float2 coef = mul2(nidt2, ld2(UT + ci));
+                if (vy[j]) put(gp + off, fma2(coef, vtt, ld2(GR + ci)));
+            }
+        }
+
+        if constexpr (!ROT) {
+#pragma unroll
+            for (int j = 0; j < NY; ++j)
+#pragma unroll
+                for (int t = 0; t < 2 * R; ++t) q[j][t] = q[j][t + 1];
+        }
+        if (i >= srng.x && i < srng.y) sample_plane<T::BW, NT>(a, H, stab, i, tid);
+        __syncwarp();
+        if (lx == 0) mbar_arrive(&empty[st]);
+        if (i >= irng.x && i < irng.y) {
+            named_barrier_sync(1, NT);
+            inject_plane<GRAD, NT>(a, itab, i, tid);
+        }
+    };
+
+    if constexpr (ROT) {
+        for (int base = 0; base < n; base += Q) {
+            [&]<int... P>(std::integer_sequence<int, P...>) {
+                ((base + P < n ? (plane(IC<P>{}, base + P), true) : false) && ...);
+            }(std::make_integer_sequence<int, Q>{});
+        }
+    } else {
+        for (int i = 0; i < n; ++i) plane(IC<0>{}, i);
+    }
+}
+
 // occ != nullptr: report resident CTAs per SM instead of launching.
 template <int R, int BY, int NY, int S, bool GRAD>
 cudaError_t launch3d_t(const FieldGeom& g, const SweepConfig& cfg, const SweepMaps& m,
@@ -387,16 +628,61 @@ cudaError_t launch3d_t(const FieldGeom& g, const SweepConfig& cfg, const SweepMa
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     if (occ) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, kern, 32 * (BY + 1), smem);
-    dim3 grid(cfg.tiles_x, cfg.tiles_y, cfg.zchunks);
-    dim3 block(32, BY + 1);  // BY consumer warps + the TMA producer warp
-    kern<<<grid, block, smem, s>>>(m.uh, m.uc, m.c1, m.c2, m.ut, m.gr, a, g.Px, g.Py, g.py, g.pz);
-    return cudaGetLastError();
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(cfg.tiles_x, cfg.tiles_y, cfg.zchunks);
+    lc.blockDim = dim3(32, BY + 1);  // BY consumer warps + the TMA producer warp
+    lc.dynamicSmemBytes = smem;
+    lc.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = cfg.pdl ? 1 : 0;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    return cudaLaunchKernelEx(&lc, kern, m.uh, m.uc, m.c1, m.c2, m.ut, m.gr, a, g.Px, g.Py,
+                              g.py, g.pz);
+}
+
+template <int R, int BY, int NY, int S, bool GRAD, int MINB, bool ROT>
+cudaError_t launch3d_pair_t(const FieldGeom& g, const SweepConfig& cfg, const SweepMaps& m,
+                            const SweepArgs& a, cudaStream_t s, int* occ) {
+    auto kern = sweep3d_pair_kernel<R, BY, NY, S, GRAD, MINB, ROT>;
+    const size_t smem = sweep3d_smem_bytes(R, cfg, GRAD);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    if (occ) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, kern, 32 * (BY + 1), smem);
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(cfg.tiles_x, cfg.tiles_y, cfg.zchunks);
+    lc.blockDim = dim3(32, BY + 1);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = cfg.pdl ? 1 : 0;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    return cudaLaunchKernelEx(&lc, kern, m.uh, m.uc, m.c1, m.c2, m.ut, m.gr, a, g.Px, g.Py,
+                              g.py, g.pz);
 }
 
 template <int R, bool GRAD>
 cudaError_t launch3d_r(const FieldGeom& g, const SweepConfig& cfg, const SweepMaps& m,
                        const SweepArgs& a, cudaStream_t s, int* occ) {
     // (by, ny, stages) variants compiled for every radius (see kSweepVariants).
+    // Pair-mapping variants (by, ny, stages); the register budget (resident
+    // CTAs the kernel is compiled for) follows from the z queue, ny (2R+1)
+    // float2 per thread.
+    constexpr int MB2 = R <= 4 ? 4 : (R <= 6 ? 3 : 2);  // ny = 2, 4 warps
+#define SFDB_P(BY, NY, S, MINB, ROT)                                                      \
+    if (cfg.pair && cfg.by == BY && cfg.ny == NY && cfg.stages == S && cfg.rot == ROT)    \
+        return launch3d_pair_t<R, BY, NY, S, GRAD, MINB, ROT>(g, cfg, m, a, s, occ);
+    SFDB_P(4, 2, 4, MB2, 0)
+    SFDB_P(4, 2, 3, (R <= 4 ? 4 : 3), 0)
+    SFDB_P(4, 1, 4, 4, 0)
+    SFDB_P(4, 2, 4, MB2, 1)
+    SFDB_P(8, 2, 3, (R <= 4 ? 2 : 1), 1)
+#undef SFDB_P
+    if (cfg.pair) return cudaErrorInvalidConfiguration;
 #define SFDB_V(BY, NY, S)                                              \
     if (cfg.by == BY && cfg.ny == NY && cfg.stages == S)               \
         return launch3d_t<R, BY, NY, S, GRAD>(g, cfg, m, a, s, occ);

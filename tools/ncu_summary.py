@@ -33,7 +33,17 @@ WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "smsp__warp_issue_stalled_branch_resolving_per_warp_active.pct",
         "smsp__warp_issue_stalled_drain_per_warp_active.pct",
         "smsp__warp_issue_stalled_imc_miss_per_warp_active.pct",
-        "smsp__warp_issue_stalled_tex_throttle_per_warp_active.pct"]
+        "smsp__warp_issue_stalled_tex_throttle_per_warp_active.pct",
+        "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
+        "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum",
+        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum",
+        "l1tex__data_pipe_lsu_wavefronts_mem_shared.avg.pct_of_peak_sustained_elapsed",
+        "smsp__inst_executed_op_shared_ld.sum",
+        "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+        "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+        "sm__cycles_active.avg"]
 
 
 def main(path):
