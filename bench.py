@@ -223,6 +223,15 @@ def run_reference(args):
     print(json.dumps(line))
 
 
+def bytes_per_point(plan, kind):
+    """Algorithmic bytes per updated point of the kernel the plan runs: the
+    SURVEY §8(d) figure (20 B forward/adjoint, 32 B fused gradient), minus the
+    c1 coefficient stream (4 B) when the damping field is max-separable and the
+    sweep forms c1 from its per-axis profiles."""
+    info = plan.info()
+    return int(info.get("bytes_per_point", BYTES_PER_POINT[kind]))
+
+
 def kernel_name(plan):
     info = plan.info()
     return "sweep3d_pair_kernel" if info.get("mapping", "").startswith("column") else "sweep3d_kernel"
@@ -343,12 +352,13 @@ def run_ours(args):
         interior = plan.points_per_step // (ze - zb) * ((ze - zb) - R * ((rank > 0) + (rank < world - 1)))
     # 2-D runs the whole time loop in one cooperative launch
     sweeps_per_launch = plan.steps if nd == 2 else 1
-    alg = BYTES_PER_POINT["forward"] * interior * sweeps_per_launch
+    bpp = bytes_per_point(plan, "forward")
+    alg = bpp * interior * sweeps_per_launch
     achieved = alg / (per_launch_ms / 1e3) / 1e9
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": ncu_traffic(w.name),
             "kernel": kernel_name(plan) if nd == 3 else "loop2d_kernel (all steps, cooperative)",
-            "alg_bytes_per_launch": alg, "mean_launch_ms": per_launch_ms,
+            "alg_bytes_per_launch": alg, "bytes_per_point": bpp, "mean_launch_ms": per_launch_ms,
             "kernel_timing": "CUDA events around each launch of one execute() after the timed region",
             "kernel_share_of_step": sweep_ms / (ms / args.steps), "peak_source": peak_src}
 
@@ -444,11 +454,12 @@ def run_fwi(args):
            "path": "sfdb200_run(gradient plan bound to the saved forward's device history)"}
     peak, peak_src = measured_peak()
     per_launch_ms = sweep_ms / max(1, sweep_n)
-    alg = BYTES_PER_POINT["gradient"] * w.points_per_step
+    bpp = bytes_per_point(g, "gradient")
+    alg = bpp * w.points_per_step
     achieved = alg / (per_launch_ms / 1e3) / 1e9
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": ncu_traffic(w.name),
-            "kernel": kernel_name(g) + "<GRAD>", "alg_bytes_per_launch": alg,
+            "kernel": kernel_name(g) + "<GRAD>", "alg_bytes_per_launch": alg, "bytes_per_point": bpp,
             "mean_launch_ms": per_launch_ms, "kernel_share_of_step": sweep_ms / (ms / args.steps),
             "peak_source": peak_src}
     cb = None

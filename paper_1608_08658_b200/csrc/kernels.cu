@@ -179,16 +179,88 @@ __global__ void sample_kernel(const float* __restrict__ field, const long long* 
 
 // ---------------------------------------------------------------- conversions
 
+// 3-D (R > 0): the coefficients of the x/y halo cells (never updated) are
+// zero, so the sweep may store its result there unconditionally: with
+// u1 = u2 = 0 on the halo the update yields exactly 0 (sweep3d.cuh).
 __global__ void coeffs_kernel(const double* __restrict__ m, const double* __restrict__ damp,
                               double dt, float* __restrict__ c1, float* __restrict__ c2,
-                              long long cells, int Px, int XP) {
+                              long long cells, int Px, int XP, int Py, int R) {
     const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
     if (i >= cells) return;
     const long long r = i / Px, x = i - r * Px;
+    const long long y = r % Py;
+    if (R > 0 && (x < R || x >= Px - R || y < R || y >= Py - R)) {
+        c1[r * XP + x] = 0.0f;
+        c2[r * XP + x] = 0.0f;
+        return;
+    }
     const double a = m[i] / (dt * dt);
     const double b = damp[i] / (2.0 * dt);
     c1[r * XP + x] = static_cast<float>((a - b) / (a + b));
     c2[r * XP + x] = static_cast<float>(1.0 / (a + b));
+}
+
+// ---- separable damping profiles (see SweepArgs::ez) ----------------------
+// Non-negative doubles order like their bit patterns, so the per-axis minima
+// are 64-bit atomicMin on the bits; any other input fails the exact check.
+__global__ void prof_fill_kernel(unsigned long long* a, int n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) a[i] = 0x7FF0000000000000ull;  // +inf
+}
+
+constexpr int kProfRows = 16;
+
+__global__ void prof_min_kernel(const double* __restrict__ damp, int Pz, int Py, int Px,
+                                unsigned long long* pz, unsigned long long* py,
+                                unsigned long long* px) {
+    const int z = blockIdx.y, y0 = blockIdx.x * kProfRows;
+    const int ny = min(kProfRows, Py - y0);
+    unsigned long long rmin[kProfRows];
+#pragma unroll
+    for (int r = 0; r < kProfRows; ++r) rmin[r] = ~0ull;
+    for (int x = threadIdx.x; x < Px; x += blockDim.x) {
+        unsigned long long cmin = ~0ull;
+#pragma unroll
+        for (int r = 0; r < kProfRows; ++r) {
+            if (r < ny) {
+                const unsigned long long v = __double_as_longlong(
+                    damp[(static_cast<long long>(z) * Py + y0 + r) * Px + x]);
+                cmin = min(cmin, v);
+                rmin[r] = min(rmin[r], v);
+            }
+        }
+        atomicMin(px + x, cmin);
+    }
+    unsigned long long plane = ~0ull;
+#pragma unroll
+    for (int r = 0; r < kProfRows; ++r) {
+        unsigned long long v = rmin[r];
+        for (int o = 16; o; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+        if ((threadIdx.x & 31) == 0 && r < ny) atomicMin(py + y0 + r, v);
+        plane = min(plane, v);
+    }
+    if ((threadIdx.x & 31) == 0) atomicMin(pz + z, plane);
+}
+
+__global__ void prof_check_kernel(const double* __restrict__ damp, int Pz, int Py, int Px,
+                                  const unsigned long long* pz, const unsigned long long* py,
+                                  const unsigned long long* px, unsigned int* mismatch) {
+    const long long n = static_cast<long long>(Pz) * Py * Px;
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long zy = i / Px;
+        const int x = static_cast<int>(i - zy * Px);
+        const int z = static_cast<int>(zy / Py), y = static_cast<int>(zy - static_cast<long long>(z) * Py);
+        const double r = fmax(fmax(__longlong_as_double(pz[z]), __longlong_as_double(py[y])),
+                              __longlong_as_double(px[x]));
+        const double v = damp[i];
+        if (!(v == r) || !(v >= 0.0)) *mismatch = 1u;
+    }
+}
+
+__global__ void prof_out_kernel(const unsigned long long* a, int n, double dt, float* out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = static_cast<float>(__longlong_as_double(a[i]) / dt);
 }
 
 __global__ void to_f32_kernel(const double* __restrict__ src, float* __restrict__ dst,
@@ -369,7 +441,27 @@ cudaError_t launch_sample(const float* field, const long long* off, const float*
 cudaError_t launch_coeffs(const FieldGeom& g, const double* m, const double* damp, double dt,
                           float* c1, float* c2, cudaStream_t s) {
     const long long cells = static_cast<long long>(g.Pz) * g.Py * g.Px;
-    coeffs_kernel<<<grid_for(cells, 256), 256, 0, s>>>(m, damp, dt, c1, c2, cells, g.Px, g.XP);
+    coeffs_kernel<<<grid_for(cells, 256), 256, 0, s>>>(m, damp, dt, c1, c2, cells, g.Px, g.XP,
+                                                        g.Py, g.ndim == 3 ? g.R : 0);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_damp_profiles(const double* damp, int Pz, int Py, int Px, double dt,
+                                 unsigned long long* scratch, float* ez, float* ey, float* ex,
+                                 unsigned int* mismatch, cudaStream_t s) {
+    unsigned long long* pz = scratch;
+    unsigned long long* py = pz + Pz;
+    unsigned long long* px = py + Py;
+    const int n = Pz + Py + Px;
+    cudaError_t e = cudaMemsetAsync(mismatch, 0, sizeof(unsigned int), s);
+    if (e != cudaSuccess) return e;
+    prof_fill_kernel<<<grid_for(n, 256), 256, 0, s>>>(scratch, n);
+    prof_min_kernel<<<dim3((Py + kProfRows - 1) / kProfRows, Pz), 256, 0, s>>>(damp, Pz, Py, Px,
+                                                                                 pz, py, px);
+    prof_check_kernel<<<4 * 148, 256, 0, s>>>(damp, Pz, Py, Px, pz, py, px, mismatch);
+    prof_out_kernel<<<grid_for(Pz, 256), 256, 0, s>>>(pz, Pz, dt, ez);
+    prof_out_kernel<<<grid_for(Py, 256), 256, 0, s>>>(py, Py, dt, ey);
+    prof_out_kernel<<<grid_for(Px, 256), 256, 0, s>>>(px, Px, dt, ex);
     return cudaGetLastError();
 }
 

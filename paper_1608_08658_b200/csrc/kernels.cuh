@@ -35,6 +35,14 @@ struct SweepArgs {
     const float* u2;        // row read at the centre
     const float* c1;
     const float* c2;
+    // Separable damping: when damp(z,y,x) == max(dz[z], dy[y],
+    // dx[x]) exactly, as the reference's build_damping makes it, the 3-D sweep
+    // forms c1 = 1 - e c2 with e = damp/dt = max(ez[z], ey[y], ex[x]) instead
+    // of streaming the c1 field (16 instead of 20 B per updated point).
+    // nullptr: stream c1.
+    const float* ez;
+    const float* ey;
+    const float* ex;
     const float* ut;        // GRAD: u history row t
     float* grad;            // GRAD
     int row_out, row_u1, row_u2, row_ut;  // row coordinates for the tensor maps
@@ -168,6 +176,13 @@ cudaError_t launch_sample(const float* field, const long long* off, const float*
 // fp32 pitched layout.
 cudaError_t launch_coeffs(const FieldGeom& g, const double* m, const double* damp, double dt,
                           float* c1, float* c2, cudaStream_t s);
+// Splits a dense fp64 damp field [Pz][Py][Px] into per-axis profiles
+// e*[i] = fp32(min-profile / dt) and sets *mismatch != 0 unless
+// damp == max(dz[z], dy[y], dx[x]) holds bit-exactly for every cell.
+// scratch: Pz + Py + Px 64-bit words.
+cudaError_t launch_damp_profiles(const double* damp, int Pz, int Py, int Px, double dt,
+                                 unsigned long long* scratch, float* ez, float* ey, float* ex,
+                                 unsigned int* mismatch, cudaStream_t s);
 cudaError_t launch_to_f32(const FieldGeom& g, const double* src, float* dst, long long rows,
                           cudaStream_t s);
 cudaError_t launch_to_f64(const FieldGeom& g, const float* src, double* dst, long long rows,

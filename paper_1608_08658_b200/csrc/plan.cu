@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <functional>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -43,6 +44,9 @@ sfdb200_plan::~sfdb200_plan() {
     cudaFree(field);
     cudaFree(c1);
     cudaFree(c2);
+    cudaFree(eprof);
+    cudaFree(eprof_scratch);
+    cudaFree(flag);
     if (own_hist) cudaFree(hist);
     cudaFree(grad);
     for (SparseDev* s : {&src, &rec}) {
@@ -129,12 +133,15 @@ void validate(const sfdb200_desc& d) {
 }
 
 // Compiled sweep variants worth timing for radius R, best-first (B200
-// measurements, profiles/r01): the half-tile mapping up to R = 4, the
-// column-pair mapping with a shifted (not renamed) z queue above, where the
-// fully unrolled queue rotation overflows the instruction cache.
+// measurements, profiles/r01): the column-pair mapping throughout (8-byte
+// shared-memory reads, 8-byte stores); above R = 4 with a shifted (not
+// renamed) z queue, since the fully unrolled queue rotation overflows the
+// instruction cache.  The half-tile mapping stays as a candidate.
 struct V { int by, ny, stages, pair = 0, rot = 1; };
 std::vector<V> sweep_variants(int R) {
-    if (R <= 4) return {{4, 2, 3}, {4, 2, 4}, {4, 2, 6}, {4, 1, 4}, {4, 1, 6}, {4, 2, 3, 1, 0}};
+    if (R <= 4)
+        return {{4, 2, 3, 1, 0}, {4, 2, 4, 1, 1}, {4, 2, 3, 1, 1}, {4, 2, 4, 1, 0}, {4, 2, 3},
+                {4, 1, 4}};
     return {{4, 2, 4, 1, 0}, {4, 2, 3, 1, 0}, {8, 2, 3, 1, 1}, {4, 1, 4, 1, 0}, {4, 1, 4}, {4, 1, 3}};
 }
 
@@ -284,6 +291,12 @@ void create(const sfdb200_desc& gd, Comm* comm, sfdb200_plan& p) {
     p.c2 = dalloc<float>(static_cast<size_t>(g.slot));
     if (p.grad_kind()) p.grad = dalloc<float>(static_cast<size_t>(g.slot));
     p.counter = dalloc<unsigned long long>(1);
+    p.flag = dalloc<unsigned int>(1);
+    if (g.ndim == 3) {
+        const size_t n = static_cast<size_t>(g.Pz + g.Py + g.Px);
+        p.eprof = dalloc<float>(n);
+        p.eprof_scratch = dalloc<unsigned long long>(n);
+    }
     // Pitch padding columns and halo cells must read as zero for the TMA boxes.
     ck(cudaMemsetAsync(p.c1, 0, g.slot * 4, p.stream), "memset");
     ck(cudaMemsetAsync(p.c2, 0, g.slot * 4, p.stream), "memset");
@@ -362,6 +375,7 @@ void autotune(sfdb200_plan& p) {
         std::getenv("SFDB200_TILE") || std::getenv("SFDB200_ZCHUNKS"))
         return;
     p.tuned = true;
+    p.cands.clear();
     const int R = p.g.R;
     const int zupd = std::max(1, p.zint_hi - p.zint_lo);
     const std::vector<V> variants = sweep_variants(R);
@@ -419,13 +433,18 @@ void autotune(sfdb200_plan& p) {
                 best = t;
                 pick = c;
             }
+            p.cands.emplace_back(t, c);
         }
     }
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
+    std::stable_sort(p.cands.begin(), p.cands.end(),
+                     [](const auto& x, const auto& y) { return x.first < y.first; });
     p.cfg = pick;
     build_maps(p);
 }
+
+void refine_with_sparse(sfdb200_plan& p, const std::function<void()>& tables);
 
 void do_upload(sfdb200_plan& p, void** argv) {
     const sfdb200_desc& d = p.d;
@@ -442,6 +461,22 @@ void do_upload(sfdb200_plan& p, void** argv) {
     ck(cudaMemcpyAsync(p.staging + cells, damp + off, cells * 8, cudaMemcpyHostToDevice,
                        p.stream), "H2D damp");
     ck(launch_coeffs(p.g, p.staging, p.staging + cells, d.dt, p.c1, p.c2, p.stream), "coeffs");
+    p.sep_damp = false;
+    if (p.g.ndim == 3 && env_int("SFDB200_SEPDAMP", 1)) {
+        float* ez = p.eprof;
+        float* ey = ez + p.g.Pz;
+        float* ex = ey + p.g.Py;
+        ck(launch_damp_profiles(p.staging + cells, p.g.Pz, p.g.Py, p.g.Px, d.dt, p.eprof_scratch,
+                                ez, ey, ex, p.flag, p.stream),
+           "damp profiles");
+        unsigned int bad = 1;
+        ck(cudaMemcpyAsync(&bad, p.flag, sizeof bad, cudaMemcpyDeviceToHost, p.stream), "D2H");
+        ck(cudaStreamSynchronize(p.stream), "damp profiles");
+        p.sep_damp = bad == 0;
+    }
+    p.base.ez = p.sep_damp ? p.eprof : nullptr;
+    p.base.ey = p.sep_damp ? p.eprof + p.g.Pz : nullptr;
+    p.base.ex = p.sep_damp ? p.eprof + p.g.Pz + p.g.Py : nullptr;
     ck(cudaStreamSynchronize(p.stream), "coeffs");
     p.h2d += 2 * cells * 8;
 
@@ -457,17 +492,25 @@ void do_upload(sfdb200_plan& p, void** argv) {
         }
         build_maps(p);
         autotune(p);  // before the fused sparse tables, which depend on the tiling
-        upload_sparse(p, p.rec, static_cast<const long*>(argv[5]),
-                      static_cast<const double*>(argv[6]), m);
         upload_trace(p, p.rec, static_cast<const double*>(argv[7]));
+        const auto tables = [&] {
+            upload_sparse(p, p.rec, static_cast<const long*>(argv[5]),
+                          static_cast<const double*>(argv[6]), m);
+        };
+        tables();
+        refine_with_sparse(p, tables);
     } else {
         autotune(p);
-        upload_sparse(p, p.src, static_cast<const long*>(argv[3]),
-                      static_cast<const double*>(argv[4]), m);
-        upload_sparse(p, p.rec, static_cast<const long*>(argv[6]),
-                      static_cast<const double*>(argv[7]), m);
         if (d.kind == SFDB200_FORWARD) upload_trace(p, p.src, static_cast<const double*>(argv[5]));
         else upload_trace(p, p.rec, static_cast<const double*>(argv[8]));
+        const auto tables = [&] {
+            upload_sparse(p, p.src, static_cast<const long*>(argv[3]),
+                          static_cast<const double*>(argv[4]), m);
+            upload_sparse(p, p.rec, static_cast<const long*>(argv[6]),
+                          static_cast<const double*>(argv[7]), m);
+        };
+        tables();
+        refine_with_sparse(p, tables);
     }
     ck(cudaStreamSynchronize(p.stream), "upload");
 }
@@ -629,6 +672,65 @@ void phase_samples(sfdb200_plan& p, StepState& st) {
     }
     st.prev_srow = st.srow;
     st.prev_out = st.a.out;
+}
+
+// Second autotune stage, after the sparse tables exist: the isolated-launch
+// timings of autotune() leave out the fused injection / sampling work and the
+// overlap of consecutive launches, which can reorder the candidates (many
+// receivers, single partial waves).  The best few are re-timed over a short
+// run of real steps, tables rebuilt for each tiling.
+void refine_with_sparse(sfdb200_plan& p, const std::function<void()>& tables) {
+    const long n = std::min<long>(6, p.steps());
+    const bool sparse = p.src.n + p.rec.n > 0;
+    if (p.cands.size() < 2 || p.dist() || n < 2 || !sparse) {
+        p.cands.clear();
+        return;
+    }
+    const size_t K = std::min<size_t>(6, p.cands.size());
+    cudaEvent_t e0, e1;
+    ck(cudaEventCreate(&e0), "cudaEventCreate");
+    ck(cudaEventCreate(&e1), "cudaEventCreate");
+    const bool timing = p.timing;
+    p.timing = false;
+    float best = 1e30f;
+    size_t pick = 0, built = 0;
+    for (size_t k = 0; k < K; ++k) {
+        if (k != built) {
+            p.cfg = p.cands[k].second;
+            build_maps(p);
+            tables();
+            built = k;
+        }
+        float t = 1e30f;
+        for (int rep = 0; rep < 2; ++rep) {
+            exec_begin(p);
+            StepState st;
+            ck(cudaEventRecord(e0, p.stream), "event");
+            for (long i = 0; i < n; ++i) {
+                step_setup(p, i, st);
+                phase_interior(p, i, st);
+                phase_samples(p, st);
+            }
+            ck(cudaEventRecord(e1, p.stream), "event");
+            ck(cudaEventSynchronize(e1), "refine");
+            float ms = 0;
+            ck(cudaEventElapsedTime(&ms, e0, e1), "elapsed");
+            t = std::min(t, ms);
+        }
+        if (t < best) {
+            best = t;
+            pick = k;
+        }
+    }
+    p.timing = timing;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (pick != built) {
+        p.cfg = p.cands[pick].second;
+        build_maps(p);
+        tables();
+    }
+    p.cands.clear();
 }
 
 void exec_end(sfdb200_plan& p, StepState& st) {
@@ -1093,12 +1195,16 @@ int sfdb200_plan_info(const sfdb200_plan* p, char* buf, long len) {
                       "{\"tile\": [32, %d], \"warps\": %d, \"rows_per_thread\": %d, "
                       "\"stages\": %d, \"tiles\": [%d, %d], \"zchunks\": %d, \"zlen\": %d, "
                       "\"smem_bytes\": %zu, \"fused_sparse\": %s, \"slab\": [%ld, %ld], "
-                      "\"x_pitch\": %d, \"mapping\": \"%s\", \"pdl\": %s}",
+                      "\"x_pitch\": %d, \"mapping\": \"%s\", \"pdl\": %s, "
+                      "\"separable_damping\": %s, \"bytes_per_point\": %d}",
                       c.ty(), c.by + 1, 2 * c.ny, c.stages, c.tiles_x, c.tiles_y, c.zchunks,
                       c.zlen, c.smem_bytes, p->fused ? "true" : "false", p->zoff + p->g.R,
                       p->zoff + p->g.Pz - p->g.R, p->g.XP,
-                      c.pair ? "column pairs x ny rows" : "2 half-tiles x ny rows",
-                      c.pdl ? "true" : "false");
+                      c.pair ? (c.rot ? "column pairs x ny rows, renamed z queue"
+                                      : "column pairs x ny rows, shifted z queue")
+                             : "2 half-tiles x ny rows",
+                      c.pdl ? "true" : "false", p->sep_damp ? "true" : "false",
+                      (p->grad_kind() ? 32 : 20) - (p->sep_damp ? 4 : 0));
     });
 }
 

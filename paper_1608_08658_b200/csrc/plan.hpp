@@ -141,6 +141,9 @@ struct sfdb200_plan {
     float* field = nullptr;  // u (forward) / v (adjoint, gradient), `rows` rows
     float* c1 = nullptr;
     float* c2 = nullptr;
+    float* eprof = nullptr;  // 3-D: damp/dt profiles ez[Pz], ey[Py], ex[Px] (SweepArgs::ez)
+    unsigned long long* eprof_scratch = nullptr;
+    bool sep_damp = false;   // the uploaded damp field is max-separable
     float* hist = nullptr;   // gradient: u history
     bool own_hist = false;
     float* grad = nullptr;
@@ -148,6 +151,7 @@ struct sfdb200_plan {
     double* staging = nullptr;
     size_t staging_elems = 0;
     unsigned long long* counter = nullptr;
+    unsigned int* flag = nullptr;
 
     cudaStream_t own_stream = nullptr;
     cudaStream_t stream = nullptr;
@@ -155,6 +159,7 @@ struct sfdb200_plan {
     sfdb200::SweepMaps maps{};
     sfdb200::SweepArgs base{};
     bool maps_ready = false;
+    std::vector<std::pair<float, sfdb200::SweepConfig>> cands;  // autotune timings, fastest first
     bool fused = true;
     bool tuned = false;
 

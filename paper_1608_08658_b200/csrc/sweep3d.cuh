@@ -43,26 +43,36 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                  : "memory");
 }
 
+// try_wait with a suspend-time hint: a thread whose phase is not complete
+// sleeps until it completes (or the hint, in ns, elapses) instead of spinning
+// through the issue slots the other warps of its SM sub-partition need.
 __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
     uint32_t ok;
     asm volatile(
         "{\n"
         ".reg .pred p;\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
         "selp.u32 %0, 1, 0, p;\n"
         "}\n"
         : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(parity)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(0x989680u)
         : "memory");
     return ok != 0;
 }
 
-// Spins on the stage barrier; a transaction count that can never complete
-// (a bug) traps instead of hanging the GPU.
+__device__ __forceinline__ uint64_t global_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Waits for the stage barrier's phase; a transaction count that can never
+// complete (a bug) traps after 20 s instead of hanging the GPU.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    uint32_t spins = 0;
+    if (mbar_try_wait(bar, parity)) return;
+    const uint64_t t0 = global_ns();
     while (!mbar_try_wait(bar, parity))
-        if (++spins == (1u << 26)) __trap();
+        if (global_ns() - t0 > 20000000000ull) __trap();
 }
 
 // Programmatic dependent launch: the next sweep may be scheduled once every
@@ -200,11 +210,12 @@ __global__ void __launch_bounds__(32 * (BY + 1), 4)
     auto issue = [&](int stage, int z) {
         float* sb = smem + stage * T::SF;
         uint64_t* bar = &full[stage];
-        mbar_arrive_expect_tx(bar, T::BYTES);
+        const bool sep = a.ez != nullptr;  // c1 formed from the damping profiles
+        mbar_arrive_expect_tx(bar, sep ? T::BYTES - 4u * T::CF : T::BYTES);
         tma_load_4d(sb, &tm_uh, x0 - T::RA, y0 - R, z, a.row_u1, bar);
         tma_load_4d(sb + T::HF, &tm_uc, x0, y0, z + R, a.row_u1, bar);
         tma_load_4d(sb + T::HF + T::CF, &tm_uc, x0, y0, z, a.row_u2, bar);
-        tma_load_4d(sb + T::HF + 2 * T::CF, &tm_c1, x0, y0, z, 0, bar);
+        if (!sep) tma_load_4d(sb + T::HF + 2 * T::CF, &tm_c1, x0, y0, z, 0, bar);
         tma_load_4d(sb + T::HF + 3 * T::CF, &tm_c2, x0, y0, z, 0, bar);
         if constexpr (GRAD) {
             tma_load_4d(sb + T::HF + 4 * T::CF, &tm_ut, x0, y0, z, a.row_ut, bar);
@@ -264,14 +275,16 @@ __global__ void __launch_bounds__(32 * (BY + 1), 4)
     pdl_wait();
 
     // Queue slot of plane zb - R + t is t mod Q.
+    // Rows inside the allocation.  Halo and pad cells of a row are stored too:
+    // their coefficients are zero and their u1, u2 are zero, so the update
+    // writes back exactly 0 (kernels.cu coeffs_kernel).
     float2 q[NY][Q];
     bool va[NY], vb[NY];
-    const bool xin = x >= R && x < Px - R;
 #pragma unroll
     for (int j = 0; j < NY; ++j) {
         const int ya_ = y0 + ly0 + j, yb_ = ya_ + T::HALF;
-        va[j] = xin && ya_ < Py - R;
-        vb[j] = xin && yb_ < Py - R;
+        va[j] = ya_ < Py;
+        vb[j] = yb_ < Py;
         const float* ca = a.u1 + static_cast<long long>(ya_) * py + x;
         const float* cb = a.u1 + static_cast<long long>(yb_) * py + x;
 #pragma unroll
@@ -287,19 +300,35 @@ __global__ void __launch_bounds__(32 * (BY + 1), 4)
 #pragma unroll
     for (int k = 0; k <= R; ++k) wk[k] = f2(a.w[k], a.w[k]);
     const float2 nidt2 = f2(a.nidt2, a.nidt2);
+    // Separable damping: -max(ey[y], ex[x]) of this thread's points (fixed along z).
+    const bool sep = a.ez != nullptr;
+    float2 nexy[NY];
+#pragma unroll
+    for (int j = 0; j < NY; ++j) {
+        const int ya_ = y0 + ly0 + j, yb_ = ya_ + T::HALF;
+        const float exv = sep && x < Px ? __ldg(a.ex + x) : 0.0f;
+        nexy[j] = f2(-fmaxf(sep && ya_ < Py ? __ldg(a.ey + ya_) : 0.0f, exv),
+                     -fmaxf(sep && yb_ < Py ? __ldg(a.ey + yb_) : 0.0f, exv));
+    }
 
-    float* outa = a.out + static_cast<long long>(y0 + ly0) * py + x;
-    float* outb = outa + T::HALF * py;
-    float* ga = GRAD ? a.grad + static_cast<long long>(y0 + ly0) * py + x : nullptr;
-    float* gb = GRAD ? ga + T::HALF * py : nullptr;
+    // Store cursor: byte address of (plane zb + i, row y0 + ly0, column x) in
+    // the output row, advanced one plane per iteration; the other rows and
+    // the gradient field are fixed byte offsets from it.
+    char* cur = reinterpret_cast<char*>(a.out + static_cast<long long>(zb) * pz +
+                                        static_cast<long long>(y0 + ly0) * py + x);
+    const long long rowb = py * 4, halfb = T::HALF * py * 4, planeb = pz * 4;
+    const long long gdiff = GRAD ? reinterpret_cast<char*>(a.grad) - reinterpret_cast<char*>(a.out) : 0;
+
+    int stage = 0;        // pipeline stage of the current plane
+    uint32_t phase = 0;   // its full-barrier parity
 
     // One z plane.  PH is the compile-time phase of plane i within the queue
     // rotation (always 0 without ROT, where the queue is shifted instead).
     auto plane = [&](auto ph_c, const int i) {
         constexpr int PH = decltype(ph_c)::value;
         auto slot = [](int off) { return ((PH + off + R) % Q + Q) % Q; };
-        const int st = i % S;
-        mbar_wait(&full[st], static_cast<uint32_t>((i / S) & 1));
+        const int st = stage;
+        mbar_wait(&full[st], phase);
         const float* H = smem + st * T::SF;
         const float* Cq = H + T::HF;
         const float* U2 = Cq + T::CF;
@@ -322,7 +351,7 @@ __global__ void __launch_bounds__(32 * (BY + 1), 4)
             ya[k] = f2(hA[k * T::BW], hB[k * T::BW]);
             yb[k] = f2(hA[(NY + R + k) * T::BW], hB[(NY + R + k) * T::BW]);
         }
-        const long long zoff = static_cast<long long>(zb + i) * pz;
+        const float nez = sep ? -__ldg(a.ez + zb + i) : 0.0f;
 
 #pragma unroll
         for (int j = 0; j < NY; ++j) {
@@ -343,20 +372,27 @@ __global__ void __launch_bounds__(32 * (BY + 1), 4)
             }
             const int ia = ca + j * T::TX, ib = cb + j * T::TX;
             const float2 d = fma2(f2(U2[ia], U2[ib]), mone, c0);           // c0 - u2, exact form
-            const float2 inc = fma2(f2(C1[ia], C1[ib]), d, mul2(f2(C2[ia], C2[ib]), lap));
+            const float2 c2v = f2(C2[ia], C2[ib]);
+            // c1 = 1 - e c2, e = damp/dt (separable) or the streamed c1 field
+            const float2 c1v = sep ? fma2(f2(fminf(nez, nexy[j].x), fminf(nez, nexy[j].y)), c2v,
+                                          f2(1.0f, 1.0f))
+                                   : f2(C1[ia], C1[ib]);
+            const float2 inc = fma2(c1v, d, mul2(c2v, lap));
             const float2 o = add2(c0, inc);
-            const long long off = zoff + j * py;
-            if (va[j]) outa[off] = o.x;
-            if (vb[j]) outb[off] = o.y;
+            char* pa = cur + j * rowb;
+            char* pb = pa + halfb;
+            if (va[j]) *reinterpret_cast<float*>(pa) = o.x;
+            if (vb[j]) *reinterpret_cast<float*>(pb) = o.y;
             if constexpr (GRAD) {
                 // grad += -(1/dt^2) u_t (v_t - 2 v_{t+1} + v_{t+2}) = nidt2 * u_t * (inc - d)
                 const float2 vtt = fma2(d, mone, inc);
                 const float2 coef = mul2(nidt2, f2(UT[ia], UT[ib]));
-                if (va[j]) ga[off] = fmaf(coef.x, vtt.x, GR[ia]);
-                if (vb[j]) gb[off] = fmaf(coef.y, vtt.y, GR[ib]);
+                if (va[j]) *reinterpret_cast<float*>(pa + gdiff) = fmaf(coef.x, vtt.x, GR[ia]);
+                if (vb[j]) *reinterpret_cast<float*>(pb + gdiff) = fmaf(coef.y, vtt.y, GR[ib]);
             }
         }
 
+        cur += planeb;
         if constexpr (!ROT) {
 #pragma unroll
             for (int j = 0; j < NY; ++j)
@@ -376,6 +412,10 @@ __global__ void __launch_bounds__(32 * (BY + 1), 4)
         if (i >= irng.x && i < irng.y) {
             named_barrier_sync(1, NT);
             inject_plane<GRAD, NT>(a, itab, i, tid);
+        }
+        if (++stage == S) {
+            stage = 0;
+            phase ^= 1u;
         }
     };
 
@@ -436,11 +476,12 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
     auto issue = [&](int stage, int z) {
         float* sb = smem + stage * T::SF;
         uint64_t* bar = &full[stage];
-        mbar_arrive_expect_tx(bar, T::BYTES);
+        const bool sep = a.ez != nullptr;  // c1 formed from the damping profiles
+        mbar_arrive_expect_tx(bar, sep ? T::BYTES - 4u * T::CF : T::BYTES);
         tma_load_4d(sb, &tm_uh, x0 - T::RA, y0 - R, z, a.row_u1, bar);
         tma_load_4d(sb + T::HF, &tm_uc, x0, y0, z + R, a.row_u1, bar);
         tma_load_4d(sb + T::HF + T::CF, &tm_uc, x0, y0, z, a.row_u2, bar);
-        tma_load_4d(sb + T::HF + 2 * T::CF, &tm_c1, x0, y0, z, 0, bar);
+        if (!sep) tma_load_4d(sb + T::HF + 2 * T::CF, &tm_c1, x0, y0, z, 0, bar);
         tma_load_4d(sb + T::HF + 3 * T::CF, &tm_c2, x0, y0, z, 0, bar);
         if constexpr (GRAD) {
             tma_load_4d(sb + T::HF + 4 * T::CF, &tm_ut, x0, y0, z, a.row_ut, bar);
@@ -496,13 +537,12 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
     const int px = lx & 15, gy = lx >> 4;
     const int r0 = (threadIdx.y * 2 + gy) * NY;  // first tile row of this thread
     const int x = x0 + 2 * px;
-    const bool vx0 = x >= R && x < Px - R, vx1 = x + 1 >= R && x + 1 < Px - R;
     float2 q[NY][Q];
-    bool vy[NY];
+    bool vy[NY];  // rows inside the allocation (halo cells store 0, see sweep3d_kernel)
 #pragma unroll
     for (int j = 0; j < NY; ++j) {
         const int y = y0 + r0 + j;
-        vy[j] = y < Py - R;
+        vy[j] = y < Py;
         const float* c = a.u1 + static_cast<long long>(y) * py + x;
 #pragma unroll
         for (int t = 0; t < 2 * R; ++t) {
@@ -517,22 +557,27 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
 #pragma unroll
     for (int k = 0; k <= R; ++k) wk[k] = f2(a.w[k], a.w[k]);
     const float2 nidt2 = f2(a.nidt2, a.nidt2);
-    float* outp = a.out + static_cast<long long>(y0 + r0) * py + x;
-    float* gp = GRAD ? a.grad + static_cast<long long>(y0 + r0) * py + x : nullptr;
-    auto put = [&](float* p, float2 v) {
-        if (vx0 && vx1) {
-            st2(p, v);
-        } else {
-            if (vx0) p[0] = v.x;
-            if (vx1) p[1] = v.y;
-        }
-    };
+    const bool sep = a.ez != nullptr;
+    float2 nexy[NY];
+#pragma unroll
+    for (int j = 0; j < NY; ++j) {
+        const int y = y0 + r0 + j;
+        const float eyv = sep && y < Py ? __ldg(a.ey + y) : 0.0f;
+        nexy[j] = f2(-fmaxf(eyv, sep && x < Px ? __ldg(a.ex + x) : 0.0f),
+                     -fmaxf(eyv, sep && x + 1 < Px ? __ldg(a.ex + x + 1) : 0.0f));
+    }
+    char* cur = reinterpret_cast<char*>(a.out + static_cast<long long>(zb) * pz +
+                                        static_cast<long long>(y0 + r0) * py + x);
+    const long long rowb = py * 4, planeb = pz * 4;
+    const long long gdiff = GRAD ? reinterpret_cast<char*>(a.grad) - reinterpret_cast<char*>(a.out) : 0;
 
+    int stage = 0;
+    uint32_t phase = 0;
     auto plane = [&](auto ph_c, const int i) {
         constexpr int PH = decltype(ph_c)::value;
         auto slot = [](int off) { return ((PH + off + R) % Q + Q) % Q; };
-        const int st = i % S;
-        mbar_wait(&full[st], static_cast<uint32_t>((i / S) & 1));
+        const int st = stage;
+        mbar_wait(&full[st], phase);
         const float* H = smem + st * T::SF;
         const float* Cq = H + T::HF;
         const float* U2 = Cq + T::CF;
@@ -551,7 +596,7 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
             yu[k - 1] = ld2(hp - k * T::BW);
             yd[k - 1] = ld2(hp + (NY - 1 + k) * T::BW);
         }
-        const long long zoff = static_cast<long long>(zb + i) * pz;
+        const float nez = sep ? -__ldg(a.ez + zb + i) : 0.0f;
 
 #pragma unroll
         for (int j = 0; j < NY; ++j) {
@@ -581,16 +626,21 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
             if constexpr (R >= 5) lap = add2(lap, lap2);
             const int ci = cidx + j * T::TX;
             const float2 d = fma2(ld2(U2 + ci), mone, c0);
-            const float2 inc = fma2(ld2(C1 + ci), d, mul2(ld2(C2 + ci), lap));
+            const float2 c2v = ld2(C2 + ci);
+            const float2 c1v = sep ? fma2(f2(fminf(nez, nexy[j].x), fminf(nez, nexy[j].y)), c2v,
+                                          f2(1.0f, 1.0f))
+                                   : ld2(C1 + ci);
+            const float2 inc = fma2(c1v, d, mul2(c2v, lap));
             const float2 o = add2(c0, inc);
-            const long long off = zoff + j * py;
-            if (vy[j]) put(outp + off, o);
+            char* pj = cur + j * rowb;
+            if (vy[j]) st2(reinterpret_cast<float*>(pj), o);
             if constexpr (GRAD) {
                 const float2 vtt = fma2(d, mone, inc);
                 const float2 coef = mul2(nidt2, ld2(UT + ci));
-                if (vy[j]) put(gp + off, fma2(coef, vtt, ld2(GR + ci)));
+                if (vy[j]) st2(reinterpret_cast<float*>(pj + gdiff), fma2(coef, vtt, ld2(GR + ci)));
             }
         }
+        cur += planeb;
 
         if constexpr (!ROT) {
 #pragma unroll
@@ -604,6 +654,10 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
         if (i >= irng.x && i < irng.y) {
             named_barrier_sync(1, NT);
             inject_plane<GRAD, NT>(a, itab, i, tid);
+        }
+        if (++stage == S) {
+            stage = 0;
+            phase ^= 1u;
         }
     };
 
@@ -680,15 +734,18 @@ cudaError_t launch3d_r(const FieldGeom& g, const SweepConfig& cfg, const SweepMa
     SFDB_P(4, 2, 3, (R <= 4 ? 4 : 3), 0)
     SFDB_P(4, 1, 4, 4, 0)
     SFDB_P(4, 2, 4, MB2, 1)
+    SFDB_P(4, 2, 3, (R <= 4 ? 4 : 3), 1)
     SFDB_P(8, 2, 3, (R <= 4 ? 2 : 1), 1)
 #undef SFDB_P
     if (cfg.pair) return cudaErrorInvalidConfiguration;
 #define SFDB_V(BY, NY, S)                                              \
     if (cfg.by == BY && cfg.ny == NY && cfg.stages == S)               \
         return launch3d_t<R, BY, NY, S, GRAD>(g, cfg, m, a, s, occ);
-    SFDB_V(4, 2, 4)
-    SFDB_V(4, 2, 3)
-    SFDB_V(4, 2, 6)
+    if constexpr (R <= 4) {  // two rows per half: the queue fits the registers
+        SFDB_V(4, 2, 4)
+        SFDB_V(4, 2, 3)
+        SFDB_V(4, 2, 6)
+    }
     SFDB_V(4, 1, 4)
     SFDB_V(4, 1, 3)
     SFDB_V(4, 1, 6)

@@ -208,3 +208,30 @@ def test_cli_run_and_bench(tmp_path):
                      "--set", "time=0.1", "bench"]) == 0
     rows = [_json.loads(x) for x in open(out2 / "bench.jsonl")]
     assert rows[0]["gpts"] > 0 and rows[1]["plan"] == "b200-e2e"
+
+
+@pytest.mark.parametrize("kind", ["separable", "perturbed", "negative"])
+def test_damping_profiles_or_streamed_c1(kind):
+    """The sweep forms c1 from per-axis damping profiles only when the damp
+    field is max-separable bit for bit (the reference's build_damping); any
+    other damp field streams c1 and still matches the oracle."""
+    from paper_1608_08658_b200 import _lib as L
+    w = configs.cfg2(n=28, nt=122, nbpml=8, nrec_side=6)
+    model, src, rec = _setup(w)
+    damp = model.damp.copy()
+    if kind == "perturbed":  # one interior cell breaks separability
+        damp[damp.size // 2 + 5] = 1e-3
+    elif kind == "negative":  # non-negative bit order no longer holds
+        damp[damp.size // 2 + 5] = -1e-9
+    argv = [np.zeros((3, *model.padded)), model.m, damp, src.idx, src.w, O._f64(w.wavelet),
+            rec.idx, rec.w, np.zeros((w.nt, rec.npoints))]
+    p = L.Plan(L.FORWARD, 3, model.padded, w.space_order, w.nt, w.dt, w.h, src.npoints,
+               rec.npoints, False, 0)
+    p.run(argv)
+    info = p.info()
+    p.close()
+    assert info["separable_damping"] == (kind == "separable")
+    assert info["bytes_per_point"] == (16 if kind == "separable" else 20)
+    uo, ro = O.forward(model.padded, w.space_order, w.h, w.dt, w.nt, model.m, damp,
+                       src.idx, src.w, w.wavelet, rec.idx, rec.w)
+    assert O.rel_l2(argv[0], uo) <= TOL and O.rel_l2(argv[8], ro) <= TOL
