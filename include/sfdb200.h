@@ -89,6 +89,20 @@ SFDB200_API int sfdb200_download(sfdb200_plan* plan, void** argv);
 /* Gradient plans: take the u history from a saved Forward plan's device
  * buffer (same problem) instead of uploading a host copy. */
 SFDB200_API int sfdb200_bind_history(sfdb200_plan* gradient_plan, const sfdb200_plan* forward_plan);
+
+/* ---- history storage by uniform checkpointing -------
+ * The reference keeps the whole saved history (spilling it to an mmap'd file,
+ * proj/src/runtime.cpp:122-169).  A 3-D single-GPU Forward plan (save = 0)
+ * with an interval k > 0 instead keeps rows u[jk], u[jk+1] (j >= 1) during
+ * execute(); a Gradient plan bound to it recomputes each k-step segment of the
+ * history from those rows (one extra forward sweep per step) into a k+2-row
+ * buffer while it runs backwards.  Device memory: 2 (ceil((nt-2)/k) - 1) + k + 2
+ * rows instead of nt + 1.  The gradient plan's argv[1] (u history) is ignored.
+ * interval 0 turns checkpointing off. */
+SFDB200_API int sfdb200_set_checkpointing(sfdb200_plan* forward_plan, long interval);
+SFDB200_API int sfdb200_bind_checkpoints(sfdb200_plan* gradient_plan, sfdb200_plan* forward_plan);
+/* Device bytes the checkpoint store and one segment buffer take (0 if off). */
+SFDB200_API long sfdb200_checkpoint_bytes(const sfdb200_plan* forward_plan);
 /* Launch on a caller stream (a cudaStream_t passed as void*); 0 = plan's own. */
 SFDB200_API int sfdb200_set_stream(sfdb200_plan* plan, void* cuda_stream);
 /* When on, execute() brackets every stencil launch with CUDA events. */

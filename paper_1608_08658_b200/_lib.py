@@ -46,6 +46,9 @@ _SIGS = {
     "sfdb200_execute": (_i, [_P]),
     "sfdb200_download": (_i, [_P, _P]),
     "sfdb200_bind_history": (_i, [_P, _P]),
+    "sfdb200_set_checkpointing": (_i, [_P, _L]),
+    "sfdb200_bind_checkpoints": (_i, [_P, _P]),
+    "sfdb200_checkpoint_bytes": (_L, [_P]),
     "sfdb200_set_stream": (_i, [_P, _P]),
     "sfdb200_set_timing": (_i, [_P, _i]),
     "sfdb200_stencil_time": (_i, [_P, _dp, _lp]),
@@ -165,6 +168,19 @@ class Plan:
 
     def bind_history(self, forward_plan):
         check(lib().sfdb200_bind_history(self.handle, forward_plan.handle))
+
+    def set_checkpointing(self, interval):
+        """Forward plans: keep restart rows every `interval` steps (0: off)."""
+        check(lib().sfdb200_set_checkpointing(self.handle, int(interval)))
+
+    def bind_checkpoints(self, forward_plan):
+        """Gradient plans: recompute the u history from a checkpointing forward plan."""
+        check(lib().sfdb200_bind_checkpoints(self.handle, forward_plan.handle))
+        self._ck_fwd = forward_plan  # keep it alive while bound
+
+    @property
+    def checkpoint_bytes(self):
+        return int(lib().sfdb200_checkpoint_bytes(self.handle))
 
     def set_stream(self, stream_handle):
         check(lib().sfdb200_set_stream(self.handle, C.c_void_p(stream_handle or None)))

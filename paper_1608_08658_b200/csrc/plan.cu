@@ -46,6 +46,7 @@ sfdb200_plan::~sfdb200_plan() {
     cudaFree(c2);
     cudaFree(eprof);
     cudaFree(eprof_scratch);
+    cudaFree(ck_store);
     cudaFree(flag);
     if (own_hist) cudaFree(hist);
     cudaFree(grad);
@@ -480,8 +481,18 @@ void do_upload(sfdb200_plan& p, void** argv) {
     ck(cudaStreamSynchronize(p.stream), "coeffs");
     p.h2d += 2 * cells * 8;
 
+    if (grad && p.ck_fwd) {  // history recomputed per segment from checkpoints
+        const long rows = p.ck_fwd->ck_interval + 2;
+        if (!p.hist || p.hist_rows != rows) {
+            if (p.own_hist) cudaFree(p.hist);
+            p.hist = nullptr;
+            p.hist_rows = rows;
+            p.hist = dalloc<float>(static_cast<size_t>(rows * p.g.slot));
+            p.own_hist = true;
+        }
+    }
     if (grad) {
-        if (!p.hist || p.own_hist) {
+        if (!p.ck_fwd && (!p.hist || p.own_hist)) {
             if (!p.hist) {
                 p.hist_rows = d.nt + 1;
                 p.hist = dalloc<float>(static_cast<size_t>(p.hist_rows * p.g.slot));
@@ -708,6 +719,10 @@ void refine_with_sparse(sfdb200_plan& p, const std::function<void()>& tables) {
             ck(cudaEventRecord(e0, p.stream), "event");
             for (long i = 0; i < n; ++i) {
                 step_setup(p, i, st);
+                if (p.grad_kind() && p.ck_fwd) {  // segment buffer: any row is a valid stand-in
+                    st.a.ut = p.hist;
+                    st.a.row_ut = 0;
+                }
                 phase_interior(p, i, st);
                 phase_samples(p, st);
             }
@@ -818,9 +833,130 @@ void flush_rows(sfdb200_plan& p, long upto) {
     p.flushed = upto;
 }
 
+// ---- uniform checkpointing --------------------------------------------------
+//
+// Segment j of a run covers steps t in [2 + j k, min(2 + (j+1) k, nt)).  The
+// forward run keeps, for j >= 1, the rows u[j k] and u[j k + 1] (pair j - 1)
+// once step t = j k + 1 is done.  A gradient plan bound to it walks the
+// segments last to first: restore the pair into rows 0, 1 of its segment
+// buffer, recompute u[ts .. te-1] into rows 2.. with the forward plan's own
+// tiling, tables and source injection (no sampling), then run its backward
+// steps te-1 .. ts reading u[t] from that buffer.  Memory: 2 (J-1) + k + 2
+// rows instead of nt + 1 (J = ceil(steps / k)); cost: one more forward sweep
+// per step.
+
+long ck_segments(long steps, long k) { return (steps + k - 1) / k; }
+
+void take_checkpoint(sfdb200_plan& p, long t) {
+    const long k = p.ck_interval;
+    if (!k || t < 1 + k || (t - 1) % k != 0) return;
+    const long j = (t - 1) / k;  // segment restarted from this pair
+    if (j - 1 >= p.ck_pairs) return;
+    const long long slot = p.g.slot;
+    float* dst = p.ck_store + 2 * (j - 1) * slot;
+    ck(cudaMemcpyAsync(dst, p.field + ((t - 1) % 3) * slot, slot * 4, cudaMemcpyDeviceToDevice,
+                       p.stream), "checkpoint");
+    ck(cudaMemcpyAsync(dst + slot, p.field + (t % 3) * slot, slot * 4, cudaMemcpyDeviceToDevice,
+                       p.stream), "checkpoint");
+}
+
+void prepare_checkpoints(sfdb200_plan& p) {
+    p.ck_valid = false;
+    if (!p.ck_interval) return;
+    const long pairs = std::max(0L, ck_segments(p.steps(), p.ck_interval) - 1);
+    if (pairs != p.ck_pairs || (pairs && !p.ck_store)) {
+        cudaFree(p.ck_store);
+        p.ck_store = nullptr;
+        p.ck_pairs = pairs;
+        if (pairs) p.ck_store = dalloc<float>(static_cast<size_t>(2 * pairs * p.g.slot));
+    }
+}
+
+// One forward sweep of the checkpointed forward plan fp, recomputing u[t] into
+// row t - ts + 2 of the gradient plan's segment buffer.
+void recompute_step(sfdb200_plan& fp, const SweepMaps& maps, float* seg, long ts, long t,
+                    cudaStream_t s) {
+    const FieldGeom& g = fp.g;
+    SweepArgs a = fp.base;
+    const long r0 = t - ts + 2;
+    a.out = seg + r0 * g.slot;
+    a.u1 = seg + (r0 - 1) * g.slot;
+    a.u2 = seg + (r0 - 2) * g.slot;
+    a.c1 = fp.c1;
+    a.c2 = fp.c2;
+    a.row_out = static_cast<int>(r0);
+    a.row_u1 = static_cast<int>(r0 - 1);
+    a.row_u2 = static_cast<int>(r0 - 2);
+    a.zlo = fp.zint_lo;
+    a.zhi = fp.zint_hi;
+    a.zchunk = fp.cfg.zlen;
+    SparseDev& src = fp.src;
+    const float* row = src.n ? src.trace + (t - 1) * src.n : nullptr;  // forward: trace row t-1
+    if (fp.fused && src.f_tab) {
+        a.inj_tab = src.f_tab;
+        a.inj_rng = src.f_rng;
+        a.inj_off = src.f_off;
+        a.inj_coef = src.f_coef;
+        a.inj_pt = src.f_pt;
+        a.inj_gm = src.f_gm;
+        a.inj_row = row;
+    }
+    ck(launch_sweep3d(g, fp.cfg, maps, a, false, s), "sweep3d (recompute)");
+    if (src.inj_rest.n)
+        ck(launch_inject(a.out, src.inj_rest.off, src.inj_rest.coef, src.inj_rest.pt, row,
+                         src.inj_rest.n, nullptr, nullptr, nullptr, 0.0f, s),
+           "inject (recompute)");
+}
+
+void do_execute_checkpointed(sfdb200_plan& p) {
+    sfdb200_plan& fp = *p.ck_fwd;
+    if (!fp.ck_valid || fp.d.nt != p.d.nt)
+        fail(SFDB200_EINVAL, "the bound forward plan holds no checkpoints of this run "
+                             "(execute it with checkpointing first)");
+    if (!fp.maps_ready) fail(SFDB200_EINVAL, "the bound forward plan is not uploaded");
+    const long k = fp.ck_interval, steps = p.steps(), nt = p.d.nt;
+    const long long slot = p.g.slot;
+    if (p.hist_rows != k + 2) fail(SFDB200_EINVAL, "segment buffer does not match the interval");
+    // The forward plan's tiling over the segment buffer.
+    SweepMaps seg = fp.maps;
+    const unsigned TY = static_cast<unsigned>(fp.cfg.ty());
+    seg.uh = make_map(p.hist, p.g, p.hist_rows, static_cast<unsigned>(fp.cfg.bw(p.g.R)),
+                      TY + 2 * p.g.R);
+    seg.uc = make_map(p.hist, p.g, p.hist_rows, 32, TY);
+    seg.ut = seg.uc;
+    seg.gr = seg.uc;
+    exec_begin(p);
+    StepState st;
+    for (long j = ck_segments(steps, k) - 1; j >= 0; --j) {
+        const long ts = 2 + j * k, te = std::min(ts + k, nt);
+        if (j == 0) {
+            ck(cudaMemsetAsync(p.hist, 0, 2 * slot * 4, p.stream), "memset");
+        } else {
+            ck(cudaMemcpyAsync(p.hist, fp.ck_store + 2 * (j - 1) * slot, 2 * slot * 4,
+                               cudaMemcpyDeviceToDevice, p.stream), "restore");
+        }
+        for (long t = ts; t < te; ++t) recompute_step(fp, seg, p.hist, ts, t, p.stream);
+        p.launches += te - ts;
+        for (long t = te - 1; t >= ts; --t) {
+            const long i = nt - 1 - t;
+            step_setup(p, i, st);
+            st.a.ut = p.hist + (t - ts + 2) * slot;
+            st.a.row_ut = static_cast<int>(t - ts + 2);
+            phase_interior(p, i, st);
+            phase_samples(p, st);
+        }
+    }
+    exec_end(p, st);
+}
+
 void do_execute(sfdb200_plan& p) {
     if (p.dist() && comm_loopback(p.comm))
         fail(SFDB200_EINVAL, "loopback ranks run through sfdb200_execute_group");
+    if (p.ck_fwd) {
+        do_execute_checkpointed(p);
+        return;
+    }
+    if (p.ck_interval) prepare_checkpoints(p);
     exec_begin(p);
     p.flushed = 0;
     const bool stream_out = p.host_rec && p.g.ndim == 3 && p.d.kind == SFDB200_FORWARD &&
@@ -848,8 +984,10 @@ void do_execute(sfdb200_plan& p) {
         phase_samples(p, st);
         // forward: rows < t are final once step t's sweep sampled row t-1
         if (stream_out && i % 64 == 63) flush_rows(p, 2 + i);
+        take_checkpoint(p, 2 + i);
     }
     exec_end(p, st);
+    p.ck_valid = p.ck_interval > 0;
 }
 
 // Emulated ranks on ONE GPU (test harness for the decomposition): the plans
@@ -1062,11 +1200,55 @@ int sfdb200_bind_history(sfdb200_plan* gp, const sfdb200_plan* fp) {
             std::memcmp(gp->d.padded, fp->d.padded, sizeof gp->d.padded) != 0)
             fail(SFDB200_EINVAL, "history comes from a different problem");
         if (gp->own_hist) cudaFree(gp->hist);
+        gp->ck_fwd = nullptr;
         gp->hist = fp->field;
         gp->hist_rows = fp->rows;
         gp->own_hist = false;
         gp->maps_ready = false;
     });
+}
+
+int sfdb200_set_checkpointing(sfdb200_plan* p, long interval) {
+    return guarded([&] {
+        if (!p) fail(SFDB200_EINVAL, "null plan");
+        if (interval < 0) fail(SFDB200_EINVAL, "negative checkpoint interval");
+        if (interval && (p->d.kind != SFDB200_FORWARD || p->d.save || p->g.ndim != 3 || p->dist()))
+            fail(SFDB200_EINVAL,
+                 "checkpointing needs a single-GPU 3-D Forward plan without a saved history");
+        p->ck_interval = interval;
+        p->ck_valid = false;
+        if (!interval) {
+            cudaFree(p->ck_store);
+            p->ck_store = nullptr;
+            p->ck_pairs = 0;
+        }
+    });
+}
+
+int sfdb200_bind_checkpoints(sfdb200_plan* gp, sfdb200_plan* fp) {
+    return guarded([&] {
+        if (!gp || !fp) fail(SFDB200_EINVAL, "null plan");
+        if (gp->d.kind != SFDB200_GRADIENT || fp->d.kind != SFDB200_FORWARD || !fp->ck_interval)
+            fail(SFDB200_EINVAL,
+                 "bind_checkpoints needs a Gradient plan and a checkpointing Forward plan");
+        if (gp->d.nt != fp->d.nt || gp->d.ndim != fp->d.ndim || gp->d.device != fp->d.device ||
+            gp->d.space_order != fp->d.space_order || gp->dist() || fp->dist() ||
+            std::memcmp(gp->d.padded, fp->d.padded, sizeof gp->d.padded) != 0 ||
+            gp->d.dt != fp->d.dt || gp->d.h != fp->d.h)
+            fail(SFDB200_EINVAL, "checkpoints come from a different problem");
+        if (gp->own_hist) cudaFree(gp->hist);
+        gp->hist = nullptr;
+        gp->hist_rows = 0;
+        gp->own_hist = false;
+        gp->ck_fwd = fp;
+        gp->maps_ready = false;
+    });
+}
+
+long sfdb200_checkpoint_bytes(const sfdb200_plan* p) {
+    if (!p || !p->ck_interval) return 0;
+    const long pairs = std::max(0L, ck_segments(p->steps(), p->ck_interval) - 1);
+    return static_cast<long>((2 * pairs + p->ck_interval + 2) * p->g.slot * 4);
 }
 
 int sfdb200_set_stream(sfdb200_plan* p, void* stream) {

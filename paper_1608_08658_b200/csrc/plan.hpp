@@ -144,6 +144,16 @@ struct sfdb200_plan {
     float* eprof = nullptr;  // 3-D: damp/dt profiles ez[Pz], ey[Py], ex[Px] (SweepArgs::ez)
     unsigned long long* eprof_scratch = nullptr;
     bool sep_damp = false;   // the uploaded damp field is max-separable
+    // Uniform checkpointing (forward plans, 3-D): every ck_interval steps the
+    // two latest rows are copied to ck_store (pairs 0..ck_pairs-1; pair j-1
+    // restarts segment j, see do_execute_checkpointed).
+    long ck_interval = 0;
+    float* ck_store = nullptr;
+    long ck_pairs = 0;
+    bool ck_valid = false;   // the last execute() filled the store
+    // Gradient plans bound to a checkpointed forward plan: hist holds one
+    // recomputed segment (ck_interval + 2 rows).
+    sfdb200_plan* ck_fwd = nullptr;
     float* hist = nullptr;   // gradient: u history
     bool own_hist = false;
     float* grad = nullptr;

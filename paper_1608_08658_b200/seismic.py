@@ -301,6 +301,74 @@ def gradient(model: VelocityModel, rec: SparsePoints, residual: ShotRecord, u_hi
     return out
 
 
+@dataclass
+class FwiResult:
+    phi: float               # 1/2 sum (syn - obs)^2
+    grad: np.ndarray         # padded cells
+    record: ShotRecord       # synthetic traces
+    history_bytes: int       # device bytes holding the forward wavefield for the gradient
+    stats: RunStats          # forward + gradient wall time, gradient steps counted
+
+
+def fwi_gradient(model: VelocityModel, src: SparsePoints, src_trace, rec: SparsePoints,
+                 observed: ShotRecord, nt, dt, checkpoint_interval: Optional[int] = None,
+                 cfg: Optional[RunConfig] = None) -> FwiResult:
+    """One FWI gradient (the forward(save) -> objective -> gradient chain of
+    verify.cpp:179-297 / the cfg3 workload) kept on the device.
+
+    checkpoint_interval: 0 keeps the whole u history in HBM (nt + 1 rows, the
+    reference's saved-history semantics); k > 0 keeps restart rows every k steps
+    and recomputes each segment during the backward pass (3-D only; SURVEY
+    §8(f) row 2, sfdb200_set_checkpointing); None picks ~sqrt(steps) in 3-D."""
+    cfg = cfg or RunConfig()
+    check_dt(model, dt)
+    nd = model.ndim()
+    steps = max(0, int(nt) - 2)
+    if checkpoint_interval is None:
+        checkpoint_interval = max(1, int(round(steps ** 0.5))) if nd == 3 else 0
+    k = int(checkpoint_interval)
+    if k and nd != 3:
+        raise L.InvalidArgument(L.EINVAL, "checkpointing is implemented for 3-D problems")
+    trace = L.f64(src_trace).ravel()
+    if trace.size != nt * src.npoints:
+        raise L.InvalidArgument(L.EINVAL, "source trace must hold nt samples per source point")
+    obs = L.f64(observed.data)
+    if observed.nt != nt or observed.npoints != rec.npoints:
+        raise L.InvalidArgument(L.EINVAL, "observed record does not match nt and the receivers")
+    si, sw = _sparse_args(src, nd)
+    ri, rw = _sparse_args(rec, nd)
+    m, damp = L.f64(model.m), L.f64(model.damp)
+    fwd = L.Plan(L.FORWARD, nd, model.padded, model.space_order, nt, dt, model.h, src.npoints,
+                 rec.npoints, k == 0, cfg.device)
+    g = L.Plan(L.GRADIENT, nd, model.padded, model.space_order, nt, dt, model.h, 0,
+               rec.npoints, False, cfg.device)
+    try:
+        t0 = time.perf_counter()
+        syn = np.empty((int(nt), rec.npoints))
+        fargv = [None, m, damp, si, sw, trace, ri, rw, syn]
+        if k:
+            fwd.set_checkpointing(k)
+        fwd.upload(fargv)
+        fwd.execute()
+        fwd.download(fargv)
+        resid = syn - obs.reshape(syn.shape)
+        phi = 0.5 * float(np.dot(resid.ravel(), resid.ravel()))
+        if k:
+            g.bind_checkpoints(fwd)
+            hist_bytes = fwd.checkpoint_bytes
+        else:
+            g.bind_history(fwd)
+            hist_bytes = history_rows(nt) * int(np.prod(model.padded)) * 4
+        grad = np.empty(model.padded)
+        g.run([None, None, m, damp, grad, ri, rw, resid])
+        secs = time.perf_counter() - t0
+        return FwiResult(phi, grad, ShotRecord(int(nt), float(dt), rec.npoints, syn),
+                         int(hist_bytes), _stats(g, secs))
+    finally:
+        g.close()
+        fwd.close()
+
+
 def objective(synthetic: ShotRecord, observed: ShotRecord, want_residual=False):
     """seismic.cpp:498-510: Phi = 1/2 sum (syn - obs)^2 (and the residual record)."""
     a = np.asarray(synthetic.data, np.float64)
