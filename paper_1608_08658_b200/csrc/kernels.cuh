@@ -157,6 +157,56 @@ struct Loop2dArgs {
     long smp_n;
 };
 cudaError_t launch_loop2d(const Loop2dArgs& a, int R, bool grad, int ctas, cudaStream_t s);
+
+// 2-D: the whole time loop in ONE thread-block cluster (cluster2d.cu).  The
+// wavefield lives in the cluster's shared memory: CTA c owns a band of
+// updated rows (cluster2d_band) plus R halo rows a side in three time slots;
+// halo rows move between CTAs through distributed shared memory and the
+// steps are separated by cluster barriers instead of grid-wide ones.
+struct Cluster2dArgs {
+    float* field;              // global rows (non-save: the 3 slots at the end)
+    float* hist;               // forward save: history rows written every step
+    const float* ut;           // GRAD: u history rows (read)
+    float* grad;               // GRAD
+    const float* c1;
+    const float* c2;
+    long long slot;            // elements per row
+    int kind, save;
+    long nt;
+    float w[kMaxRadius + 1];
+    float neg2nd, nidt2;
+    int Pz, Px, XP, nc, nbmax;
+    // injection / sampling tables (SparseDev::k_*), traces [nt][n]
+    const int* inj_begin;
+    const int* inj_soff;
+    const long long* inj_goff;
+    const float* inj_coef;
+    const int* inj_pt;
+    const unsigned char* inj_gm;
+    const float* inj_trace;
+    long inj_n;
+    const int* smp_begin;
+    const int* smp_soff;
+    const float* smp_w;
+    const int* smp_pt;
+    float* smp_trace;
+    long smp_n;
+    // Entries per CTA staged in shared memory (an L1 line does not survive the
+    // acquire of a cluster barrier); the rest are read from global memory.
+    int inj_cap, smp_cap;
+};
+// Rows [zb, ze) of CTA c (updated rows R .. Pz-R split evenly).
+__host__ __device__ inline void cluster2d_band(int Pz, int R, int nc, int c, int* zb, int* ze) {
+    const int nz = Pz - 2 * R, base = nz / nc, rem = nz % nc;
+    *zb = R + c * base + (c < rem ? c : rem);
+    *ze = *zb + base + (c < rem ? 1 : 0);
+}
+// 0 when the problem does not fit one cluster (caller keeps loop2d).
+int cluster2d_ctas(int Pz, int Px, int XP, int R, bool grad);
+size_t cluster2d_smem_bytes(int Pz, int XP, int R, int nc, bool grad);
+constexpr size_t kCluster2dSmemMax = 227 * 1024;
+constexpr int kCluster2dInjBytes = 16, kCluster2dSmpBytes = 36;  // staged bytes per entry
+cudaError_t launch_cluster2d(const Cluster2dArgs& a, int R, bool grad, cudaStream_t s);
 int loop2d_blocks_per_sm(int R, bool grad);
 
 // Sparse operators over flat entry lists: off = element offset of a corner

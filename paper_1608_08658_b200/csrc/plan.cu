@@ -312,6 +312,11 @@ void create(const sfdb200_desc& gd, Comm* comm, sfdb200_plan& p) {
         if (occ < 1) fail(SFDB200_ECUDA, "2-D time loop kernel cannot be resident");
         p.ctas2d = static_cast<int>(std::max<long long>(
             1, std::min<long long>(static_cast<long long>(occ) * p.sms, (npts + 255) / 256)));
+        if (const int c = env_int("SFDB200_CTAS2D", 0))
+            p.ctas2d = std::min(c, occ * p.sms);
+        // One thread-block cluster holding the field in shared memory when it fits.
+        if (env_int("SFDB200_CLUSTER2D", 1))
+            p.nc2d = cluster2d_ctas(g.Pz, g.Px, g.XP, R, p.grad_kind());
         p.per_cta2d = (npts + p.ctas2d - 1) / p.ctas2d;
     }
     if (!p.grad_kind()) build_maps(p);
@@ -761,6 +766,65 @@ void exec_end(sfdb200_plan& p, StepState& st) {
     ck(cudaGetLastError(), "execute");
 }
 
+// 2-D, field in one cluster's shared memory (cluster2d.cu).
+void execute_cluster2d(sfdb200_plan& p) {
+    const sfdb200_desc& d = p.d;
+    const FieldGeom& g = p.g;
+    SparseDev& inj = p.injected();
+    SparseDev* smp = sampled_nonempty(p);
+    Cluster2dArgs a{};
+    a.field = p.field;
+    a.hist = d.save && d.kind == SFDB200_FORWARD ? p.field : nullptr;
+    a.ut = p.hist;
+    a.grad = p.grad;
+    a.c1 = p.c1;
+    a.c2 = p.c2;
+    a.slot = g.slot;
+    a.kind = d.kind;
+    a.save = d.save && d.kind == SFDB200_FORWARD;
+    a.nt = d.nt;
+    for (int k = 0; k <= g.R; ++k) a.w[k] = p.base.w[k];
+    a.neg2nd = p.base.neg2nd;
+    a.nidt2 = p.base.nidt2;
+    a.Pz = g.Pz;
+    a.Px = g.Px;
+    a.XP = g.XP;
+    a.nc = p.nc2d;
+    a.nbmax = (g.Pz - 2 * g.R + p.nc2d - 1) / p.nc2d;
+    if (inj.n && inj.k_begin) {
+        a.inj_begin = inj.k_begin;
+        a.inj_soff = inj.k_soff;
+        a.inj_goff = inj.k_goff;
+        a.inj_coef = inj.k_coef;
+        a.inj_pt = inj.k_pt;
+        a.inj_gm = inj.k_gm;
+        a.inj_trace = inj.trace;
+        a.inj_n = inj.n;
+    }
+    {  // stage as many sparse entries per CTA as the shared memory left allows
+        const size_t base = cluster2d_smem_bytes(g.Pz, g.XP, g.R, p.nc2d, p.grad_kind());
+        size_t left = kCluster2dSmemMax > base ? kCluster2dSmemMax - base : 0;
+        a.inj_cap = static_cast<int>(std::min<size_t>(inj.k_begin ? inj.k_max : 0,
+                                                      left / kCluster2dInjBytes));
+        left -= static_cast<size_t>(a.inj_cap) * kCluster2dInjBytes;
+        a.smp_cap = static_cast<int>(std::min<size_t>(smp && smp->k_begin ? smp->k_max : 0,
+                                                      left / kCluster2dSmpBytes));
+    }
+    if (smp && smp->k_begin) {
+        a.smp_begin = smp->k_begin;
+        a.smp_soff = smp->k_soff;
+        a.smp_w = smp->k_coef;
+        a.smp_pt = smp->k_pt;
+        a.smp_trace = smp->trace;
+        a.smp_n = smp->n;
+    }
+    if (p.timing) ck(cudaEventRecord(p.events[0], p.stream), "event");
+    ck(launch_cluster2d(a, g.R, p.grad_kind(), p.stream), "cluster2d");
+    if (p.timing) ck(cudaEventRecord(p.events[1], p.stream), "event");
+    p.timed_launches = 1;
+    p.launches = 1;
+}
+
 // 2-D: the whole time loop is one cooperative launch (kernels.cu loop2d_kernel).
 void execute_2d(sfdb200_plan& p) {
     const sfdb200_desc& d = p.d;
@@ -803,6 +867,10 @@ void execute_2d(sfdb200_plan& p) {
         a.smp_n = smp->n;
     }
     if (p.steps() == 0) return;
+    if (p.nc2d) {
+        execute_cluster2d(p);
+        return;
+    }
     if (p.timing) ck(cudaEventRecord(p.events[0], p.stream), "event");
     ck(launch_loop2d(a, g.R, p.grad_kind(), p.ctas2d, p.stream), "loop2d");
     if (p.timing) ck(cudaEventRecord(p.events[1], p.stream), "event");
@@ -1378,7 +1446,7 @@ int sfdb200_plan_info(const sfdb200_plan* p, char* buf, long len) {
                       "\"stages\": %d, \"tiles\": [%d, %d], \"zchunks\": %d, \"zlen\": %d, "
                       "\"smem_bytes\": %zu, \"fused_sparse\": %s, \"slab\": [%ld, %ld], "
                       "\"x_pitch\": %d, \"mapping\": \"%s\", \"pdl\": %s, "
-                      "\"separable_damping\": %s, \"bytes_per_point\": %d}",
+                      "\"separable_damping\": %s, \"bytes_per_point\": %d, \"cluster2d_ctas\": %d}",
                       c.ty(), c.by + 1, 2 * c.ny, c.stages, c.tiles_x, c.tiles_y, c.zchunks,
                       c.zlen, c.smem_bytes, p->fused ? "true" : "false", p->zoff + p->g.R,
                       p->zoff + p->g.Pz - p->g.R, p->g.XP,
@@ -1386,7 +1454,7 @@ int sfdb200_plan_info(const sfdb200_plan* p, char* buf, long len) {
                                       : "column pairs x ny rows, shifted z queue")
                              : "2 half-tiles x ny rows",
                       c.pdl ? "true" : "false", p->sep_damp ? "true" : "false",
-                      (p->grad_kind() ? 32 : 20) - (p->sep_damp ? 4 : 0));
+                      (p->grad_kind() ? 32 : 20) - (p->sep_damp ? 4 : 0), p->nc2d);
     });
 }
 

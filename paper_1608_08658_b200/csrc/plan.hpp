@@ -79,6 +79,17 @@ struct SparseDev {
     int* s_pt = nullptr;
     float* s_acc = nullptr;
     SampleList smp_rest, smp_all;
+    // 2-D cluster time loop (cluster2d.cu): entries grouped by the CTA whose
+    // row band holds the corner (inject) or the receiver's base row (sample),
+    // with offsets into that CTA's shared-memory slot.
+    long k_n = 0;
+    int k_max = 0;                 // most entries of one CTA
+    int* k_begin = nullptr;        // [nc + 1]
+    int* k_soff = nullptr;         // inject: [n]; sample: [n][4]
+    long long* k_goff = nullptr;   // inject: element offset in a global row (u_t)
+    float* k_coef = nullptr;       // inject: coefficient; sample: [n][4] weights
+    int* k_pt = nullptr;
+    unsigned char* k_gm = nullptr;
 
     template <class T>
     T* upload(const std::vector<T>& v, cudaStream_t st) {
@@ -100,6 +111,10 @@ struct SparseDev {
         inj_rest = InjectList{};
         smp_rest = SampleList{};
         smp_all = SampleList{};
+        k_n = 0;
+        k_max = 0;
+        k_begin = nullptr; k_soff = nullptr; k_goff = nullptr; k_coef = nullptr; k_pt = nullptr;
+        k_gm = nullptr;
     }
 };
 
@@ -133,6 +148,7 @@ struct sfdb200_plan {
     long zoff = 0;
     int zint_lo = 0, zint_hi = 0;  // interior sweep launch (local planes)
     int ctas2d = 0;                // 2-D: cooperative time-loop grid
+    int nc2d = 0;                  // 2-D: CTAs of the single-cluster time loop (0: cooperative)
     long long per_cta2d = 0;       // 2-D: updated points per CTA
     sfdb200::Comm* comm = nullptr;
     cudaStream_t cstream = nullptr;

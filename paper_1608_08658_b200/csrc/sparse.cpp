@@ -38,6 +38,33 @@ bool in_interior(const sfdb200_plan& p, long zl, long y, long x) {
 
 int ctas_of(const sfdb200_plan& p) { return p.cfg.tiles_x * p.cfg.tiles_y * p.cfg.zchunks; }
 
+// 2-D cluster time loop: the CTA whose shared-memory rows hold row z (its
+// band; the global halo rows belong to the first / last CTA) and the first
+// global row of its shared-memory slot.
+int band_owner(const sfdb200_plan& p, long z, int* row0) {
+    const int R = p.g.R, nc = p.nc2d;
+    int c = 0;
+    for (int k = 0; k < nc; ++k) {
+        int zb, ze;
+        cluster2d_band(p.g.Pz, R, nc, k, &zb, &ze);
+        if (z >= zb) c = k;
+    }
+    int zb, ze;
+    cluster2d_band(p.g.Pz, R, nc, c, &zb, &ze);
+    *row0 = zb - R;
+    return c;
+}
+
+// CSR begin offsets [nc + 1] from per-entry owners (entries sorted by owner).
+std::vector<int> csr_begin(const std::vector<int>& owner, int n, int* most) {
+    std::vector<int> b(static_cast<size_t>(n) + 1, 0);
+    for (int o : owner) ++b[static_cast<size_t>(o) + 1];
+    *most = 0;
+    for (int c = 0; c < n; ++c) *most = std::max(*most, b[static_cast<size_t>(c) + 1]);
+    for (int c = 0; c < n; ++c) b[static_cast<size_t>(c) + 1] += b[static_cast<size_t>(c)];
+    return b;
+}
+
 // Per-CTA plane table over keys sorted by (cta, plane): entries of CTA c at
 // plane i are [tab[c*L + i], tab[c*L + i + 1]), L = zlen + 1.
 std::vector<int> plane_table(const sfdb200_plan& p, const std::vector<Owner>& keys) {
@@ -194,6 +221,37 @@ void upload_sparse(sfdb200_plan& p, SparseDev& s, const long* idx, const double*
         s.f_coef = s.upload(ecoef, st);
         s.f_pt = s.upload(ept, st);
         s.f_gm = s.upload(egm, st);
+        if (p.nc2d) {  // cluster loop: by row band, shared-memory offsets, (p, c) order
+            struct K { int cta; int soff; size_t i; };
+            std::vector<K> ks;
+            for (size_t i = 0; i < cs.size(); ++i) {
+                const Corner& k = cs[i];
+                int row0 = 0;
+                const int cta = band_owner(p, k.zl, &row0);
+                ks.push_back({cta, static_cast<int>((k.zl - row0) * g.XP + k.x), i});
+            }
+            std::stable_sort(ks.begin(), ks.end(), [](const K& a, const K& b) { return a.cta < b.cta; });
+            std::vector<int> owner, soff, kpt;
+            std::vector<long long> goff;
+            std::vector<float> coef;
+            std::vector<unsigned char> gm;
+            for (const K& k : ks) {
+                const Corner& c = cs[k.i];
+                owner.push_back(k.cta);
+                soff.push_back(k.soff);
+                goff.push_back(c.off);
+                coef.push_back(static_cast<float>(w[k.i] * (gd.dt * gd.dt) / m[c.dense]));
+                kpt.push_back(static_cast<int>(k.i / C));
+                gm.push_back(c.updated ? 1 : 0);
+            }
+            s.k_n = static_cast<long>(ks.size());
+            s.k_begin = s.upload(csr_begin(owner, p.nc2d, &s.k_max), st);
+            s.k_soff = s.upload(soff, st);
+            s.k_goff = s.upload(goff, st);
+            s.k_coef = s.upload(coef, st);
+            s.k_pt = s.upload(kpt, st);
+            s.k_gm = s.upload(gm, st);
+        }
     } else if (is_inj) {
         // coef = w * dt^2 / m[corner]: the reference's v = w; v *= scale;
         // v /= m with the data factor applied on the device (interpreter.cpp:144-147).
@@ -287,6 +345,33 @@ void upload_sparse(sfdb200_plan& p, SparseDev& s, const long* idx, const double*
                 }
                 r_pt.push_back(static_cast<int>(q));
             }
+        }
+        if (nd == 2 && p.nc2d) {  // cluster loop: by the band of the base row
+            struct K { int cta; long q; };
+            std::vector<K> ks;
+            for (long q = 0; q < s.n; ++q) {
+                int row0 = 0;
+                ks.push_back({band_owner(p, cs[static_cast<size_t>(q) * C].zl, &row0), q});
+            }
+            std::stable_sort(ks.begin(), ks.end(), [](const K& a, const K& b) { return a.cta < b.cta; });
+            std::vector<int> owner, soff, kpt;
+            std::vector<float> kw;
+            for (const K& k : ks) {
+                int row0 = 0;
+                band_owner(p, cs[static_cast<size_t>(k.q) * C].zl, &row0);
+                owner.push_back(k.cta);
+                kpt.push_back(static_cast<int>(k.q));
+                for (int c = 0; c < C; ++c) {
+                    const Corner& cc = cs[static_cast<size_t>(k.q) * C + c];
+                    soff.push_back(static_cast<int>((cc.zl - row0) * g.XP + cc.x));
+                    kw.push_back(static_cast<float>(w[static_cast<size_t>(k.q) * C + c]));
+                }
+            }
+            s.k_n = s.n;
+            s.k_begin = s.upload(csr_begin(owner, p.nc2d, &s.k_max), st);
+            s.k_soff = s.upload(soff, st);
+            s.k_coef = s.upload(kw, st);
+            s.k_pt = s.upload(kpt, st);
         }
         s.smp_all.n = static_cast<long>(a_pt.size());
         s.smp_all.off = s.upload(a_off, st);
