@@ -90,7 +90,8 @@ struct SweepConfig {        // 3-D tiling, chosen by choose_config()
     int ny = 2;             // y rows per thread in each tile half (tile is 2*by*ny rows);
                             // pair mapping: rows per thread (two row groups per warp)
     int stages = 4;         // TMA pipeline depth
-    int rot = 1;            // z loop unrolled by 2R+1 (register queue rotates by renaming)
+    int rot = 1;            // z unroll: 1 = by 2R+1 (queue rotates by renaming), 0 = none,
+                            // k >= 2 = by k (pair mapping; sweep3d.cuh z_unroll)
     int zchunks = 1;        // CTAs along z per (x, y) tile
     int zlen = 1;           // planes per z chunk
     int pdl = 1;            // programmatic dependent launch (overlap launch + CTA setup)

@@ -135,15 +135,17 @@ void validate(const sfdb200_desc& d) {
 
 // Compiled sweep variants worth timing for radius R, best-first (B200
 // measurements, profiles/r01): the column-pair mapping throughout (8-byte
-// shared-memory reads, 8-byte stores); above R = 4 with a shifted (not
-// renamed) z queue, since the fully unrolled queue rotation overflows the
-// instruction cache.  The half-tile mapping stays as a candidate.
+// shared-memory reads, 8-byte stores); above R = 4 the z loop is unrolled by
+// 4 or 2 only (queue shifted every 4 / 2 planes), since the fully unrolled
+// rotation overflows the instruction cache.  The half-tile mapping stays as a
+// candidate.
 struct V { int by, ny, stages, pair = 0, rot = 1; };
 std::vector<V> sweep_variants(int R) {
     if (R <= 4)
         return {{4, 2, 3, 1, 0}, {4, 2, 4, 1, 1}, {4, 2, 3, 1, 1}, {4, 2, 4, 1, 0}, {4, 2, 3},
                 {4, 1, 4}};
-    return {{4, 2, 4, 1, 0}, {4, 2, 3, 1, 0}, {8, 2, 3, 1, 1}, {4, 1, 4, 1, 0}, {4, 1, 4}, {4, 1, 3}};
+    return {{4, 2, 4, 1, 4}, {4, 2, 4, 1, 2}, {4, 2, 4, 1, 0}, {4, 2, 3, 1, 0}, {8, 2, 3, 1, 1},
+            {4, 1, 4, 1, 0}, {4, 1, 4}, {4, 1, 3}};
 }
 
 // 3-D tiling of the interior launch [zint_lo, zint_hi): 32-column x tiles,
@@ -1446,15 +1448,17 @@ int sfdb200_plan_info(const sfdb200_plan* p, char* buf, long len) {
                       "\"stages\": %d, \"tiles\": [%d, %d], \"zchunks\": %d, \"zlen\": %d, "
                       "\"smem_bytes\": %zu, \"fused_sparse\": %s, \"slab\": [%ld, %ld], "
                       "\"x_pitch\": %d, \"mapping\": \"%s\", \"pdl\": %s, "
-                      "\"separable_damping\": %s, \"bytes_per_point\": %d, \"cluster2d_ctas\": %d}",
+                      "\"separable_damping\": %s, \"bytes_per_point\": %d, \"cluster2d_ctas\": %d, \"z_unroll\": %d}",
                       c.ty(), c.by + 1, 2 * c.ny, c.stages, c.tiles_x, c.tiles_y, c.zchunks,
                       c.zlen, c.smem_bytes, p->fused ? "true" : "false", p->zoff + p->g.R,
                       p->zoff + p->g.Pz - p->g.R, p->g.XP,
-                      c.pair ? (c.rot ? "column pairs x ny rows, renamed z queue"
-                                      : "column pairs x ny rows, shifted z queue")
+                      c.pair ? (c.rot == 1 ? "column pairs x ny rows, renamed z queue"
+                                : c.rot == 0 ? "column pairs x ny rows, shifted z queue"
+                                             : "column pairs x ny rows, partly unrolled z loop")
                              : "2 half-tiles x ny rows",
                       c.pdl ? "true" : "false", p->sep_damp ? "true" : "false",
-                      (p->grad_kind() ? 32 : 20) - (p->sep_damp ? 4 : 0), p->nc2d);
+                      (p->grad_kind() ? 32 : 20) - (p->sep_damp ? 4 : 0), p->nc2d,
+                      c.rot == 1 ? 2 * p->g.R + 1 : (c.rot == 0 ? 1 : c.rot));
     });
 }
 

@@ -446,7 +446,13 @@ __device__ __forceinline__ float2 ld2(const float* p) {
 }
 __device__ __forceinline__ void st2(float* p, float2 v) { *reinterpret_cast<float2*>(p) = v; }
 
-template <int R, int BY, int NY, int S, bool GRAD, int MINB, bool ROT>
+// Unrolling of the z loop, z_unroll(R, ROTV): cfg.rot 1 = by Q (the queue
+// rotates by renaming), 0 = none (the queue shifts by one plane per plane),
+// k >= 2 = by k (the queue shifts by k planes every k planes).
+template <int R, int ROTV>
+constexpr int z_unroll() { return ROTV == 1 ? 2 * R + 1 : (ROTV == 0 ? 1 : ROTV); }
+
+template <int R, int BY, int NY, int S, bool GRAD, int MINB, int UN>
 __global__ void __launch_bounds__(32 * (BY + 1), MINB)
     sweep3d_pair_kernel(const __grid_constant__ CUtensorMap tm_uh,
                         const __grid_constant__ CUtensorMap tm_uc,
@@ -537,7 +543,9 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
     const int px = lx & 15, gy = lx >> 4;
     const int r0 = (threadIdx.y * 2 + gy) * NY;  // first tile row of this thread
     const int x = x0 + 2 * px;
-    float2 q[NY][Q];
+    constexpr bool ROT = UN == Q;
+    constexpr int QS = ROT ? Q : Q + UN - 1;  // queue slots
+    float2 q[NY][QS];
     bool vy[NY];  // rows inside the allocation (halo cells store 0, see sweep3d_kernel)
 #pragma unroll
     for (int j = 0; j < NY; ++j) {
@@ -575,7 +583,7 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
     uint32_t phase = 0;
     auto plane = [&](auto ph_c, const int i) {
         constexpr int PH = decltype(ph_c)::value;
-        auto slot = [](int off) { return ((PH + off + R) % Q + Q) % Q; };
+        auto slot = [](int off) { return ROT ? ((PH + off + R) % Q + Q) % Q : PH + R + off; };
         const int st = stage;
         mbar_wait(&full[st], phase);
         const float* H = smem + st * T::SF;
@@ -642,12 +650,6 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
         }
         cur += planeb;
 
-        if constexpr (!ROT) {
-#pragma unroll
-            for (int j = 0; j < NY; ++j)
-#pragma unroll
-                for (int t = 0; t < 2 * R; ++t) q[j][t] = q[j][t + 1];
-        }
         if (i >= srng.x && i < srng.y) sample_plane<T::BW, NT>(a, H, stab, i, tid);
         __syncwarp();
         if (lx == 0) mbar_arrive(&empty[st]);
@@ -661,14 +663,16 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
         }
     };
 
-    if constexpr (ROT) {
-        for (int base = 0; base < n; base += Q) {
-            [&]<int... P>(std::integer_sequence<int, P...>) {
-                ((base + P < n ? (plane(IC<P>{}, base + P), true) : false) && ...);
-            }(std::make_integer_sequence<int, Q>{});
+    for (int base = 0; base < n; base += UN) {
+        [&]<int... P>(std::integer_sequence<int, P...>) {
+            ((base + P < n ? (plane(IC<P>{}, base + P), true) : false) && ...);
+        }(std::make_integer_sequence<int, UN>{});
+        if constexpr (!ROT) {  // drop the UN oldest planes
+#pragma unroll
+            for (int j = 0; j < NY; ++j)
+#pragma unroll
+                for (int t = 0; t < 2 * R; ++t) q[j][t] = q[j][t + UN];
         }
-    } else {
-        for (int i = 0; i < n; ++i) plane(IC<0>{}, i);
     }
 }
 
@@ -696,10 +700,10 @@ cudaError_t launch3d_t(const FieldGeom& g, const SweepConfig& cfg, const SweepMa
                               g.py, g.pz);
 }
 
-template <int R, int BY, int NY, int S, bool GRAD, int MINB, bool ROT>
+template <int R, int BY, int NY, int S, bool GRAD, int MINB, int UN>
 cudaError_t launch3d_pair_t(const FieldGeom& g, const SweepConfig& cfg, const SweepMaps& m,
                             const SweepArgs& a, cudaStream_t s, int* occ) {
-    auto kern = sweep3d_pair_kernel<R, BY, NY, S, GRAD, MINB, ROT>;
+    auto kern = sweep3d_pair_kernel<R, BY, NY, S, GRAD, MINB, UN>;
     const size_t smem = sweep3d_smem_bytes(R, cfg, GRAD);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
@@ -727,15 +731,20 @@ cudaError_t launch3d_r(const FieldGeom& g, const SweepConfig& cfg, const SweepMa
     // CTAs the kernel is compiled for) follows from the z queue, ny (2R+1)
     // float2 per thread.
     constexpr int MB2 = R <= 4 ? 4 : (R <= 6 ? 3 : 2);  // ny = 2, 4 warps
-#define SFDB_P(BY, NY, S, MINB, ROT)                                                      \
-    if (cfg.pair && cfg.by == BY && cfg.ny == NY && cfg.stages == S && cfg.rot == ROT)    \
-        return launch3d_pair_t<R, BY, NY, S, GRAD, MINB, ROT>(g, cfg, m, a, s, occ);
+#define SFDB_P(BY, NY, S, MINB, ROTV)                                                       \
+    if (cfg.pair && cfg.by == BY && cfg.ny == NY && cfg.stages == S && cfg.rot == ROTV)     \
+        return launch3d_pair_t<R, BY, NY, S, GRAD, MINB, z_unroll<R, ROTV>()>(g, cfg, m, a, s, occ);
     SFDB_P(4, 2, 4, MB2, 0)
     SFDB_P(4, 2, 3, (R <= 4 ? 4 : 3), 0)
     SFDB_P(4, 1, 4, 4, 0)
     SFDB_P(4, 2, 4, MB2, 1)
     SFDB_P(4, 2, 3, (R <= 4 ? 4 : 3), 1)
     SFDB_P(8, 2, 3, (R <= 4 ? 2 : 1), 1)
+    if constexpr (R >= 5) {  // partial unrolls for the long queues
+        SFDB_P(4, 2, 4, MB2, 2)
+        SFDB_P(4, 2, 4, MB2, 4)
+        SFDB_P(4, 2, 4, MB2, 8)
+    }
 #undef SFDB_P
     if (cfg.pair) return cudaErrorInvalidConfiguration;
 #define SFDB_V(BY, NY, S)                                              \

@@ -1,0 +1,61 @@
+"""Every tiling variant the autotuner may pick (plan.cu sweep_variants), forced
+through SFDB200_TILE, against the oracle: forward at so 8 / 12 / 16 and the
+gradient kernel at so 8 (GRAD instantiations)."""
+import os
+
+import numpy as np
+import pytest
+
+import oracle_lib as O
+from paper_1608_08658_b200 import configs, seismic as S
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-5
+
+# "by,ny,stages,rot,pair" (sweep3d.cuh launch3d_r)
+LOW = ["4,2,3,0,1", "4,2,4,1,1", "4,2,3,1,1", "4,2,4,0,1", "4,2,3,1,0", "4,1,4,1,0", "8,2,3,1,1"]
+HIGH = ["4,2,4,4,1", "4,2,4,2,1", "4,2,4,8,1", "4,2,4,0,1", "4,2,3,0,1", "8,2,3,1,1",
+        "4,1,4,0,1", "4,1,4,1,0", "4,1,3,1,0"]
+
+
+def _forced(tile):
+    os.environ["SFDB200_TILE"] = tile
+
+
+@pytest.fixture(autouse=True)
+def _clean_env():
+    yield
+    os.environ.pop("SFDB200_TILE", None)
+
+
+@pytest.mark.parametrize("so,tile", [(8, t) for t in LOW] + [(12, t) for t in HIGH] +
+                         [(16, t) for t in HIGH])
+def test_forward_variant(so, tile):
+    w = configs.cfg4(so, n=36, nt=82, nbpml=8) if so != 8 else \
+        configs.cfg2(n=36, nt=82, nbpml=8, nrec_side=8)
+    model = S.make_model(w.interior, w.h, w.nbpml, w.space_order, w.m_interior)
+    src = S.locate_points(model, w.src_coords)
+    rec = S.locate_points(model, w.rec_coords)
+    _forced(tile)
+    f = S.forward(model, src, w.wavelet, rec, w.nt, w.dt, False)
+    u, r = O.forward(model.padded, w.space_order, w.h, w.dt, w.nt, model.m, model.damp,
+                     src.idx, src.w, w.wavelet, rec.idx, rec.w)
+    assert O.rel_l2(f.u, u) <= TOL, tile
+    if rec.npoints:
+        assert O.rel_l2(f.record.data, r) <= TOL, tile
+
+
+@pytest.mark.parametrize("tile", LOW)
+def test_gradient_variant(tile):
+    w = configs.cfg2(n=30, nt=102, nbpml=8, nrec_side=8)
+    model = S.make_model(w.interior, w.h, w.nbpml, w.space_order, w.m_interior)
+    src = S.locate_points(model, w.src_coords)
+    rec = S.locate_points(model, w.rec_coords)
+    u, r = O.forward(model.padded, w.space_order, w.h, w.dt, w.nt, model.m, model.damp,
+                     src.idx, src.w, w.wavelet, rec.idx, rec.w, save=True)
+    resid = O._f64(np.random.default_rng(2).standard_normal(r.shape).astype(np.float32))
+    _forced(tile)
+    g = S.gradient(model, rec, S.ShotRecord(w.nt, w.dt, rec.npoints, resid), u, w.nt, w.dt)
+    go, _ = O.gradient(model.padded, w.space_order, w.h, w.dt, w.nt, model.m, model.damp, u,
+                       rec.idx, rec.w, resid)
+    assert O.rel_l2(g.grad, go) <= TOL, tile
