@@ -142,8 +142,8 @@ void validate(const sfdb200_desc& d) {
 struct V { int by, ny, stages, pair = 0, rot = 1; };
 std::vector<V> sweep_variants(int R) {
     if (R <= 4)
-        return {{4, 2, 3, 1, 0}, {4, 2, 4, 1, 1}, {4, 2, 3, 1, 1}, {4, 2, 4, 1, 0}, {4, 2, 3},
-                {4, 1, 4}};
+        return {{4, 2, 3, 1, 0}, {4, 2, 4, 1, 1}, {4, 2, 4, 1, 3}, {4, 2, 4, 1, 2}, {4, 2, 3, 1, 1},
+                {4, 2, 4, 1, 0}, {4, 1, 4, 1, 0}, {4, 2, 3}, {4, 1, 4}};
     return {{4, 2, 4, 1, 4}, {4, 2, 4, 1, 2}, {4, 2, 4, 1, 0}, {4, 2, 3, 1, 0}, {8, 2, 3, 1, 1},
             {4, 1, 4, 1, 0}, {4, 1, 4}, {4, 1, 3}};
 }

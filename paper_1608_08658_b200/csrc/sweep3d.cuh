@@ -740,10 +740,14 @@ cudaError_t launch3d_r(const FieldGeom& g, const SweepConfig& cfg, const SweepMa
     SFDB_P(4, 2, 4, MB2, 1)
     SFDB_P(4, 2, 3, (R <= 4 ? 4 : 3), 1)
     SFDB_P(8, 2, 3, (R <= 4 ? 2 : 1), 1)
-    if constexpr (R >= 5) {  // partial unrolls for the long queues
-        SFDB_P(4, 2, 4, MB2, 2)
-        SFDB_P(4, 2, 4, MB2, 4)
-        SFDB_P(4, 2, 4, MB2, 8)
+    // partial unrolls (queue shifted every 2 / 3 / 4 / 8 planes)
+    SFDB_P(4, 2, 4, MB2, 2)
+    SFDB_P(4, 2, 4, MB2, 4)
+    if constexpr (R >= 5) SFDB_P(4, 2, 4, MB2, 8)
+    if constexpr (R <= 4) {
+        SFDB_P(4, 2, 3, 4, 3)
+        SFDB_P(4, 2, 4, 4, 3)
+        SFDB_P(4, 2, 3, 4, 4)
     }
 #undef SFDB_P
     if (cfg.pair) return cudaErrorInvalidConfiguration;

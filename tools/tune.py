@@ -21,6 +21,8 @@ def main():
     ap.add_argument("--zchunks", default="0")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--no-rec", action="store_true")
+    ap.add_argument("--gradient", action="store_true",
+                    help="time the fused gradient (GRAD) kernel with a zero history")
     args = ap.parse_args()
 
     import torch
@@ -34,6 +36,13 @@ def main():
     argv = [np.empty((3, *model.padded)), L.f64(model.m), L.f64(model.damp), L.i64(src.idx),
             L.f64(src.w), L.f64(w.wavelet), L.i64(rec.idx), L.f64(rec.w),
             np.empty((w.nt, rec.npoints))]
+    kind, nsrc = L.FORWARD, src.npoints
+    if args.gradient:  # residual injected at the receivers, u history all zero
+        kind, nsrc = L.GRADIENT, 0
+        hist = np.zeros((w.nt + 1, *model.padded))
+        resid = np.random.default_rng(0).standard_normal((w.nt, rec.npoints))
+        argv = [None, hist, L.f64(model.m), L.f64(model.damp), np.empty(model.padded),
+                L.i64(rec.idx), L.f64(rec.w), resid]
     for tile in args.tiles.split(";"):
         for zc in args.zchunks.split(","):
             os.environ["SFDB200_TILE"] = tile
@@ -41,8 +50,8 @@ def main():
                 os.environ["SFDB200_ZCHUNKS"] = zc
             else:
                 os.environ.pop("SFDB200_ZCHUNKS", None)
-            plan = L.Plan(L.FORWARD, 3, model.padded, w.space_order, w.nt, w.dt, w.h,
-                          src.npoints, rec.npoints, False, 0)
+            plan = L.Plan(kind, 3, model.padded, w.space_order, w.nt, w.dt, w.h,
+                          nsrc, rec.npoints, False, 0)
             plan.upload(argv)
             plan.execute()
             torch.cuda.synchronize()
@@ -59,7 +68,7 @@ def main():
             e1.record()
             torch.cuda.synchronize()
             step_ms = e0.elapsed_time(e1) / plan.steps
-            gbs = 20 * plan.points_per_step / (best / 1e3) / 1e9
+            gbs = plan.info()["bytes_per_point"] * plan.points_per_step / (best / 1e3) / 1e9
             print(json.dumps({"workload": w.name, "tile": tile, "zchunks": zc,
                               "sweep_ms": best, "cfg": plan.info(), "gpts": plan.points_per_step / best / 1e6,
                               "alg_GBps": gbs}), flush=True)
