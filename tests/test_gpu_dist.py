@@ -87,3 +87,38 @@ def test_emulated_ranks_adjoint_so16():
     v, tr = _run_group(L.ADJOINT, w, model, src, rec, wav, 3, resid)
     assert O.rel_l2(v, ref.v) <= 1e-6
     assert O.rel_l2(tr, ref.src_samples.data) <= 1e-6
+
+
+def test_nccl_communicator_single_rank():
+    """The real NCCL path as far as one GPU allows: torch.distributed (nccl)
+    loads libnccl, libsfdb200 resolves it at run time, builds a 1-rank
+    communicator from a unique id and runs a plan over it (no neighbour, so no
+    exchange); the result equals the plan without a communicator."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0,
+                            world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        uid = L.Comm.unique_id()
+        assert len(uid) == 128 and any(uid)
+        comm = L.Comm(uid, 1, 0, 0)
+        w, model, src, rec, wav = _problem()
+        outs = []
+        for c in (comm, None):
+            p = L.Plan(L.FORWARD, 3, model.padded, w.space_order, w.nt, w.dt, w.h, src.npoints,
+                       rec.npoints, False, 0, comm=c)
+            u = np.zeros((3, *model.padded))
+            tr = np.zeros((w.nt, rec.npoints))
+            p.run([u, model.m, model.damp, src.idx, src.w, wav, rec.idx, rec.w, tr])
+            p.close()
+            outs.append((u, tr))
+        comm.close()
+        assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+    finally:
+        dist.destroy_process_group()
