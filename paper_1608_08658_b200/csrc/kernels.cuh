@@ -51,25 +51,23 @@ struct SweepArgs {
     float neg2nd;           // -2 * ndim
     float nidt2;            // -1 / dt^2
 
-    // Fused sparse operators (3-D sweep only; nullptr disables them).  Both
-    // use per-CTA plane tables: entries of CTA c at its local plane i are
-    // [tab[c*(zchunk+1) + i], tab[c*(zchunk+1) + i + 1]).
+    // Fused sparse operators (3-D sweep only; nullptr disables them), kept
+    // out of the plane loop: they run once per CTA, before and after it.
     //
-    // Sample the PREVIOUS step's row (= this launch's u1) straight from the
-    // staged halo plane in shared memory: corners c = 0..3 (plane z0) when z0
-    // is staged, c = 4..7 (plane z0 + 1) on the next plane, summed in the
-    // reference's order (codegen.cpp:450-458) through a per-entry scratch.
-    const int* smp_tab;
-    const int2* smp_rng;    // [cta] planes [x, y) that have sample work (one load per CTA)
-    const int* smp_hidx;    // halo-plane smem index of corner 0
+    // Sample the PREVIOUS step's row (= this launch's u1, complete once the
+    // launch has passed griddepcontrol.wait) at the start of every CTA: the
+    // receivers are split evenly over the CTAs of the launch, corner c of
+    // receiver e at smp_base[e] + (c>>2) pz + ((c>>1)&1) py + (c&1), summed
+    // c = 0..7 in the reference's order (codegen.cpp:450-458).
+    const long long* smp_base;  // element offset of corner 0 in a row
     const float* smp_w;     // [entry][8]
-    const int* smp_pt;      // receiver index
-    float* smp_acc;         // [entry] half sums
+    const int* smp_pt;      // receiver index (trace column)
+    int smp_n;              // entries
     float* smp_row;         // trace row being sampled
-    // Inject into this step's output right after the owning plane is stored
-    // (codegen.cpp:436-449); colliding corners are summed with atomics.
+    // Inject into this step's output once the CTA has stored all its planes
+    // (codegen.cpp:436-449): entries of CTA c are [inj_tab[c], inj_tab[c+1]),
+    // the corners it stores; colliding corners are summed with atomics.
     const int* inj_tab;
-    const int2* inj_rng;    // [cta] planes [x, y) that have injections
     const long long* inj_off;
     const float* inj_coef;
     const int* inj_pt;
@@ -96,6 +94,8 @@ struct SweepConfig {        // 3-D tiling, chosen by choose_config()
     int zlen = 1;           // planes per z chunk
     int pdl = 1;            // programmatic dependent launch (overlap launch + CTA setup)
     int pair = 0;           // thread owns column pairs x, x+1 (sweep3d_pair_kernel)
+    int minb = 0;           // pair mapping: resident CTAs the registers are budgeted for
+                            // (0 = the variant's default, sweep3d.cuh launch3d_r)
     int tiles_x = 0, tiles_y = 0;
     size_t smem_bytes = 0;
     int ty() const { return 2 * by * ny; }

@@ -139,11 +139,12 @@ void validate(const sfdb200_desc& d) {
 // 4 or 2 only (queue shifted every 4 / 2 planes), since the fully unrolled
 // rotation overflows the instruction cache.  The half-tile mapping stays as a
 // candidate.
-struct V { int by, ny, stages, pair = 0, rot = 1; };
+struct V { int by, ny, stages, pair = 0, rot = 1, minb = 0; };
 std::vector<V> sweep_variants(int R) {
     if (R <= 4)
         return {{4, 2, 3, 1, 0}, {4, 2, 4, 1, 1}, {4, 2, 4, 1, 3}, {4, 2, 4, 1, 2}, {4, 2, 3, 1, 1},
-                {4, 2, 4, 1, 0}, {4, 1, 4, 1, 0}, {4, 2, 3}, {4, 1, 4}};
+                {4, 2, 4, 1, 0}, {4, 1, 4, 1, 0}, {4, 2, 3}, {4, 1, 4}, {4, 2, 4, 1, 4},
+                {4, 2, 4, 1, 4, 3}, {4, 2, 3, 1, 3, 3}, {4, 2, 4, 1, 1, 3}};
     return {{4, 2, 4, 1, 4}, {4, 2, 4, 1, 2}, {4, 2, 4, 1, 0}, {4, 2, 3, 1, 0}, {8, 2, 3, 1, 1},
             {4, 1, 4, 1, 0}, {4, 1, 4}, {4, 1, 3}};
 }
@@ -159,7 +160,7 @@ void choose_config(sfdb200_plan& p) {
     variants.resize(1);  // the measured best on B200 (autotune() times the rest)
     if (const char* t = std::getenv("SFDB200_TILE")) {
         V v{4, 2, 4};
-        std::sscanf(t, "%d,%d,%d,%d,%d", &v.by, &v.ny, &v.stages, &v.rot, &v.pair);
+        std::sscanf(t, "%d,%d,%d,%d,%d,%d", &v.by, &v.ny, &v.stages, &v.rot, &v.pair, &v.minb);
         variants = {v};
     }
     const int zc_env = env_int("SFDB200_ZCHUNKS", 0);
@@ -172,6 +173,7 @@ void choose_config(sfdb200_plan& p) {
         c.stages = v.stages;
         c.pair = v.pair;
         c.rot = v.pair ? v.rot : 1;
+        c.minb = v.pair ? v.minb : 0;
         c.tiles_x = static_cast<int>((p.g.Px - R + 31) / 32);  // tiles start at x = 0 (TMA alignment)
         c.tiles_y = static_cast<int>((p.g.Py - 2 * R + c.ty() - 1) / c.ty());
         c.smem_bytes = sweep3d_smem_bytes(R, c, p.grad_kind());
@@ -417,6 +419,7 @@ void autotune(sfdb200_plan& p) {
             c.stages = v.stages;
             c.pair = v.pair;
             c.rot = v.rot;
+            c.minb = v.minb;
             c.tiles_y = static_cast<int>((p.g.Py - 2 * R + c.ty() - 1) / c.ty());
             c.smem_bytes = sweep3d_smem_bytes(R, c, p.grad_kind());
             c.zlen = (zupd + zc - 1) / zc;
@@ -654,20 +657,17 @@ void phase_interior(sfdb200_plan& p, long i, StepState& st) {
     c.zchunk = p.cfg.zlen;
     if (p.fused && inj.f_tab) {
         c.inj_tab = inj.f_tab;
-        c.inj_rng = inj.f_rng;
         c.inj_off = inj.f_off;
         c.inj_coef = inj.f_coef;
         c.inj_pt = inj.f_pt;
         c.inj_gm = inj.f_gm;
         c.inj_row = st.inj_row;
     }
-    if (p.fused && smp && st.prev_srow >= 0 && smp->s_tab) {  // previous row == this u1
-        c.smp_tab = smp->s_tab;
-        c.smp_rng = smp->s_rng;
-        c.smp_hidx = smp->s_hidx;
-        c.smp_w = smp->s_w;
-        c.smp_pt = smp->s_pt;
-        c.smp_acc = smp->s_acc;
+    if (p.fused && smp && st.prev_srow >= 0 && smp->s_base) {  // previous row == this u1
+        c.smp_base = smp->s_base;
+        c.smp_w = smp->smp_all.w;
+        c.smp_pt = smp->smp_all.pt;
+        c.smp_n = static_cast<int>(smp->smp_all.n);
         c.smp_row = smp->trace + st.prev_srow * smp->n;
     }
     if (p.timing) ck(cudaEventRecord(p.events[2 * i], p.stream), "event");
@@ -681,7 +681,8 @@ void phase_interior(sfdb200_plan& p, long i, StepState& st) {
 
 void phase_samples(sfdb200_plan& p, StepState& st) {
     SparseDev* smp = sampled_nonempty(p);
-    const SampleList* rest = smp ? (p.fused ? &smp->smp_rest : &smp->smp_all) : nullptr;
+    // Fused: this row is sampled by the next interior launch (or exec_end).
+    const SampleList* rest = smp && !(p.fused && smp->s_base) ? &smp->smp_all : nullptr;
     if (rest && rest->n) {
         ck(launch_sample(st.a.out, rest->off, rest->w, rest->pt, smp->trace + st.srow * smp->n,
                          rest->n, p.corners, p.stream),
@@ -758,7 +759,7 @@ void refine_with_sparse(sfdb200_plan& p, const std::function<void()>& tables) {
 void exec_end(sfdb200_plan& p, StepState& st) {
     SparseDev* smp = sampled_nonempty(p);
     // The last row has no following sweep to be sampled in.
-    if (p.fused && smp && st.prev_out && smp->s_tab) {
+    if (p.fused && smp && st.prev_out && smp->s_base) {
         ck(launch_sample(st.prev_out, smp->smp_all.off, smp->smp_all.w, smp->smp_all.pt,
                          smp->trace + st.prev_srow * smp->n, smp->smp_all.n, p.corners,
                          p.stream),
@@ -964,7 +965,6 @@ void recompute_step(sfdb200_plan& fp, const SweepMaps& maps, float* seg, long ts
     const float* row = src.n ? src.trace + (t - 1) * src.n : nullptr;  // forward: trace row t-1
     if (fp.fused && src.f_tab) {
         a.inj_tab = src.f_tab;
-        a.inj_rng = src.f_rng;
         a.inj_off = src.f_off;
         a.inj_coef = src.f_coef;
         a.inj_pt = src.f_pt;
@@ -1448,7 +1448,7 @@ int sfdb200_plan_info(const sfdb200_plan* p, char* buf, long len) {
                       "\"stages\": %d, \"tiles\": [%d, %d], \"zchunks\": %d, \"zlen\": %d, "
                       "\"smem_bytes\": %zu, \"fused_sparse\": %s, \"slab\": [%ld, %ld], "
                       "\"x_pitch\": %d, \"mapping\": \"%s\", \"pdl\": %s, "
-                      "\"separable_damping\": %s, \"bytes_per_point\": %d, \"cluster2d_ctas\": %d, \"z_unroll\": %d}",
+                      "\"separable_damping\": %s, \"bytes_per_point\": %d, \"cluster2d_ctas\": %d, \"z_unroll\": %d, \"variant\": \"%d,%d,%d,%d,%d,%d\"}",
                       c.ty(), c.by + 1, 2 * c.ny, c.stages, c.tiles_x, c.tiles_y, c.zchunks,
                       c.zlen, c.smem_bytes, p->fused ? "true" : "false", p->zoff + p->g.R,
                       p->zoff + p->g.Pz - p->g.R, p->g.XP,
@@ -1458,7 +1458,8 @@ int sfdb200_plan_info(const sfdb200_plan* p, char* buf, long len) {
                              : "2 half-tiles x ny rows",
                       c.pdl ? "true" : "false", p->sep_damp ? "true" : "false",
                       (p->grad_kind() ? 32 : 20) - (p->sep_damp ? 4 : 0), p->nc2d,
-                      c.rot == 1 ? 2 * p->g.R + 1 : (c.rot == 0 ? 1 : c.rot));
+                      c.rot == 1 ? 2 * p->g.R + 1 : (c.rot == 0 ? 1 : c.rot), c.by, c.ny,
+                      c.stages, c.rot, c.pair, c.minb);
     });
 }
 

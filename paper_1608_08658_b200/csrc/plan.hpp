@@ -59,26 +59,22 @@ struct SparseDev {
     std::vector<void*> bufs;   // device buffers owned by the tables below
     unsigned long long key = 0;  // fingerprint of the inputs the tables were built from
 
-    // Injection: entries of the interior sweep launch, per (CTA, plane)
-    // (fused into the sweep), and the rest (boundary / halo planes, or every
-    // entry when the sweep is not fused) as a flat list.
+    // Injection: entries of the interior sweep launch, CSR over its CTAs
+    // (applied by the CTA that stores the corner, after its planes), and the
+    // rest (boundary / halo planes, or every entry when the sweep is not
+    // fused) as a flat list.
     int* f_tab = nullptr;
-    int2* f_rng = nullptr;
     long long* f_off = nullptr;
     float* f_coef = nullptr;
     int* f_pt = nullptr;
     unsigned char* f_gm = nullptr;
     InjectList inj_rest;
-    // Sampling: receivers read from the staged plane by the interior sweep
-    // (previous row), the rest (fallback) sampled after the step, and every
-    // owned receiver (last row).
-    int* s_tab = nullptr;
-    int2* s_rng = nullptr;
-    int* s_hidx = nullptr;
-    float* s_w = nullptr;
-    int* s_pt = nullptr;
-    float* s_acc = nullptr;
-    SampleList smp_rest, smp_all;
+    // Sampling: every owned receiver (smp_all).  In the fused 3-D sweep the
+    // previous row is sampled at the start of the next interior launch
+    // (s_base = corner-0 offsets, weights and columns shared with smp_all);
+    // otherwise after each step.  The last row always after the last step.
+    long long* s_base = nullptr;
+    SampleList smp_all;
     // 2-D cluster time loop (cluster2d.cu): entries grouped by the CTA whose
     // row band holds the corner (inject) or the receiver's base row (sample),
     // with offsets into that CTA's shared-memory slot.
@@ -104,12 +100,9 @@ struct SparseDev {
         for (void* q : bufs) cudaFree(q);
         bufs.clear();
         key = 0;
-        f_tab = nullptr; f_rng = nullptr; f_off = nullptr; f_coef = nullptr; f_pt = nullptr;
-        f_gm = nullptr;
-        s_tab = nullptr; s_rng = nullptr; s_hidx = nullptr; s_w = nullptr; s_pt = nullptr;
-        s_acc = nullptr;
+        f_tab = nullptr; f_off = nullptr; f_coef = nullptr; f_pt = nullptr; f_gm = nullptr;
+        s_base = nullptr;
         inj_rest = InjectList{};
-        smp_rest = SampleList{};
         smp_all = SampleList{};
         k_n = 0;
         k_max = 0;

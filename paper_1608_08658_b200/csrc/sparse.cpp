@@ -65,40 +65,6 @@ std::vector<int> csr_begin(const std::vector<int>& owner, int n, int* most) {
     return b;
 }
 
-// Per-CTA plane table over keys sorted by (cta, plane): entries of CTA c at
-// plane i are [tab[c*L + i], tab[c*L + i + 1]), L = zlen + 1.
-std::vector<int> plane_table(const sfdb200_plan& p, const std::vector<Owner>& keys) {
-    const int ctas = ctas_of(p), L = p.cfg.zlen + 1;
-    std::vector<int> tab(static_cast<size_t>(ctas) * L, 0);
-    size_t e = 0;
-    for (int c = 0; c < ctas; ++c)
-        for (int i = 0; i < L; ++i) {
-            while (e < keys.size() &&
-                   (keys[e].cta < c || (keys[e].cta == c && keys[e].plane < i)))
-                ++e;
-            tab[static_cast<size_t>(c) * L + i] = static_cast<int>(e);
-        }
-    return tab;
-}
-
-// Per CTA, the plane range [lo, hi + extra) holding entries (extra = 1 for
-// samples, whose second half is read one plane later); empty: (0, 0).
-std::vector<int2> plane_ranges(const sfdb200_plan& p, const std::vector<int>& tab, int extra) {
-    const int ctas = ctas_of(p), L = p.cfg.zlen + 1;
-    std::vector<int2> r(static_cast<size_t>(ctas), make_int2(0, 0));
-    for (int c = 0; c < ctas; ++c) {
-        const int* t = tab.data() + static_cast<size_t>(c) * L;
-        int lo = -1, hi = -1;
-        for (int i = 0; i + 1 < L; ++i)
-            if (t[i + 1] > t[i]) {
-                if (lo < 0) lo = i;
-                hi = i;
-            }
-        if (lo >= 0) r[static_cast<size_t>(c)] = make_int2(lo, std::min(hi + 1 + extra, L - 1));
-    }
-    return r;
-}
-
 struct Corner {
     long long off;     // element offset in one local row
     long zl, y, x;     // local position
@@ -279,27 +245,23 @@ void upload_sparse(sfdb200_plan& p, SparseDev& s, const long* idx, const double*
         s.inj_rest.pt = s.upload(r_pt, st);
         s.inj_rest.gm = s.upload(r_gm, st);
         if (!fused.empty()) {
-            // (plane, point, corner) order: each plane's injections follow the
-            // reference's (p, c) order.
-            std::stable_sort(fused.begin(), fused.end(), [](const E& a, const E& b) {
-                return a.o.cta != b.o.cta ? a.o.cta < b.o.cta : a.o.plane < b.o.plane;
-            });
-            std::vector<Owner> keys;
+            // CSR over the CTAs, the reference's (p, c) order within a CTA.
+            std::stable_sort(fused.begin(), fused.end(),
+                             [](const E& a, const E& b) { return a.o.cta < b.o.cta; });
+            std::vector<int> owner, ept;
             std::vector<long long> eoff;
             std::vector<float> ecoef;
-            std::vector<int> ept;
             std::vector<unsigned char> egm;
             for (const E& e : fused) {
                 const Corner& k = cs[e.i];
-                keys.push_back(e.o);
+                owner.push_back(e.o.cta);
                 eoff.push_back(k.off);
                 ecoef.push_back(static_cast<float>(w[e.i] * (gd.dt * gd.dt) / m[k.dense]));
                 ept.push_back(static_cast<int>(e.i / C));
                 egm.push_back(1);
             }
-            const std::vector<int> tab = plane_table(p, keys);
-            s.f_tab = s.upload(tab, st);
-            s.f_rng = s.upload(plane_ranges(p, tab, 0), st);
+            int most = 0;
+            s.f_tab = s.upload(csr_begin(owner, ctas_of(p), &most), st);
             s.f_off = s.upload(eoff, st);
             s.f_coef = s.upload(ecoef, st);
             s.f_pt = s.upload(ept, st);
@@ -308,17 +270,11 @@ void upload_sparse(sfdb200_plan& p, SparseDev& s, const long* idx, const double*
     }
 
     if (is_smp) {
-        // A receiver belongs to the rank owning its base plane z0.  The sweep
-        // reads it from the staged halo plane when the base (y, x) lies in a
-        // tile and z0, z0 + 1 lie in one z chunk of the interior launch (all
-        // x/y corners are then inside tile + halo); the rest is sampled by
-        // sample_kernel after the step (after the ghost exchange).
-        const int RA = (R + 3) & ~3, BW = p.cfg.bw(R);
-        struct E { Owner o; int hidx; long q; };
-        std::vector<E> fused;
-        std::vector<long long> a_off, r_off;
-        std::vector<float> a_w, r_w;
-        std::vector<int> a_pt, r_pt;
+        // A receiver belongs to the rank owning its base plane z0 (z0 + 1 may
+        // be a ghost plane, exchanged before the next step).
+        std::vector<long long> a_off, a_base;
+        std::vector<float> a_w;
+        std::vector<int> a_pt;
         for (long q = 0; q < s.n; ++q) {
             const Corner& b = cs[static_cast<size_t>(q) * C];  // corner 0: the base
             if (!b.owned) continue;
@@ -326,25 +282,8 @@ void upload_sparse(sfdb200_plan& p, SparseDev& s, const long* idx, const double*
                 a_off.push_back(cs[static_cast<size_t>(q) * C + c].off);
                 a_w.push_back(static_cast<float>(w[static_cast<size_t>(q) * C + c]));
             }
+            a_base.push_back(b.off);
             a_pt.push_back(static_cast<int>(q));
-            bool ok = fused3d && b.zl >= p.zint_lo && b.zl + 1 < p.zint_hi && b.y >= R &&
-                      b.y < g.Py - R && b.x >= 0 && b.x < 32L * p.cfg.tiles_x;
-            Owner o{0, 0};
-            if (ok) {
-                o = owner_of(p, b.zl, b.y, b.x);
-                ok = o.plane + 1 < p.cfg.zlen;  // z0 + 1 in the same chunk
-            }
-            if (ok) {
-                const long y0 = R + ((b.y - R) / p.cfg.ty()) * p.cfg.ty();
-                const long x0 = (b.x / 32) * 32;
-                fused.push_back({o, static_cast<int>((b.y - y0 + R) * BW + (b.x - x0 + RA)), q});
-            } else {
-                for (int c = 0; c < C; ++c) {
-                    r_off.push_back(cs[static_cast<size_t>(q) * C + c].off);
-                    r_w.push_back(static_cast<float>(w[static_cast<size_t>(q) * C + c]));
-                }
-                r_pt.push_back(static_cast<int>(q));
-            }
         }
         if (nd == 2 && p.nc2d) {  // cluster loop: by the band of the base row
             struct K { int cta; long q; };
@@ -377,32 +316,7 @@ void upload_sparse(sfdb200_plan& p, SparseDev& s, const long* idx, const double*
         s.smp_all.off = s.upload(a_off, st);
         s.smp_all.w = s.upload(a_w, st);
         s.smp_all.pt = s.upload(a_pt, st);
-        s.smp_rest.n = static_cast<long>(r_pt.size());
-        s.smp_rest.off = s.upload(r_off, st);
-        s.smp_rest.w = s.upload(r_w, st);
-        s.smp_rest.pt = s.upload(r_pt, st);
-        if (!fused.empty()) {
-            std::stable_sort(fused.begin(), fused.end(), [](const E& a, const E& b) {
-                return a.o.cta != b.o.cta ? a.o.cta < b.o.cta : a.o.plane < b.o.plane;
-            });
-            std::vector<Owner> keys;
-            std::vector<int> hidx, pt;
-            std::vector<float> w8;
-            for (const E& e : fused) {
-                keys.push_back(e.o);
-                hidx.push_back(e.hidx);
-                pt.push_back(static_cast<int>(e.q));
-                for (int c = 0; c < C; ++c)
-                    w8.push_back(static_cast<float>(w[static_cast<size_t>(e.q) * C + c]));
-            }
-            const std::vector<int> tab = plane_table(p, keys);
-            s.s_tab = s.upload(tab, st);
-            s.s_rng = s.upload(plane_ranges(p, tab, 1), st);
-            s.s_hidx = s.upload(hidx, st);
-            s.s_w = s.upload(w8, st);
-            s.s_pt = s.upload(pt, st);
-            s.s_acc = s.upload(std::vector<float>(fused.size(), 0.0f), st);
-        }
+        if (fused3d) s.s_base = s.upload(a_base, st);
     }
     ck(cudaStreamSynchronize(st), "sparse upload");
     s.key = key;

@@ -138,41 +138,42 @@ struct IC {
 // transaction bytes) and an "empty" one (one arrival per consumer warp once
 // it is done reading the stage), so no CTA-wide barrier runs per plane.
 
-// The fused sparse work of one plane, kept out of line: it runs on a handful
-// of planes, and inlined into every phase of the unrolled plane loop it would
-// only crowd the instruction cache.
-template <int BW, int NT>
-__device__ __noinline__ void sample_plane(const SweepArgs& a, const float* H, const int* stab,
-                                          int i, int tid) {
-    const int e1 = stab[i], e2 = stab[i + 1];
-    if (i > 0)
-        for (int e = stab[i - 1] + tid; e < e1; e += NT) {
-            const float* hp = H + a.smp_hidx[e];
-            const float* w = a.smp_w + 8LL * e + 4;
-            float acc = a.smp_acc[e];
-            acc = fmaf(__ldg(w + 0), hp[0], acc);
-            acc = fmaf(__ldg(w + 1), hp[1], acc);
-            acc = fmaf(__ldg(w + 2), hp[BW], acc);
-            acc = fmaf(__ldg(w + 3), hp[BW + 1], acc);
-            a.smp_row[a.smp_pt[e]] = acc;
-        }
-    for (int e = e1 + tid; e < e2; e += NT) {
-        const float* hp = H + a.smp_hidx[e];
-        const float* w = a.smp_w + 8LL * e;
-        float acc = __ldg(w + 0) * hp[0];
-        acc = fmaf(__ldg(w + 1), hp[1], acc);
-        acc = fmaf(__ldg(w + 2), hp[BW], acc);
-        acc = fmaf(__ldg(w + 3), hp[BW + 1], acc);
-        a.smp_acc[e] = acc;
+// The fused sparse work, once per CTA and out of the plane loop (so the loop
+// carries no calls and no sparse state).  `a` lives in the kernel's parameter
+// space (__grid_constant__), so passing it by reference copies nothing.
+//
+// Samples of the previous step's row (this launch's u1): this CTA's even share
+// of the receivers, read from global memory (the row is complete once the
+// launch has passed griddepcontrol.wait), summed c = 0..7 left to right.
+template <int NT>
+__device__ __noinline__ void sample_cta(const SweepArgs& a, long long py, long long pz, int cta,
+                                        int nctas, int tid) {
+    const int per = (a.smp_n + nctas - 1) / nctas;
+    const int e0 = cta * per, e1 = min(e0 + per, a.smp_n);
+    for (int e = e0 + tid; e < e1; e += NT) {
+        const float* u = a.u1 + __ldg(a.smp_base + e);
+        const float4 wl = __ldg(reinterpret_cast<const float4*>(a.smp_w) + 2 * e);
+        const float4 wh = __ldg(reinterpret_cast<const float4*>(a.smp_w) + 2 * e + 1);
+        const float* v = u + pz;
+        float acc = wl.x * u[0];
+        acc = fmaf(wl.y, u[1], acc);
+        acc = fmaf(wl.z, u[py], acc);
+        acc = fmaf(wl.w, u[py + 1], acc);
+        acc = fmaf(wh.x, v[0], acc);
+        acc = fmaf(wh.y, v[1], acc);
+        acc = fmaf(wh.z, v[py], acc);
+        acc = fmaf(wh.w, v[py + 1], acc);
+        a.smp_row[__ldg(a.smp_pt + e)] = acc;
     }
 }
 
+// Injections into the corners this CTA stored, after all its planes.
 template <bool GRAD, int NT>
-__device__ __noinline__ void inject_plane(const SweepArgs& a, const int* itab, int i, int tid) {
-    const int e0 = itab[i], e1 = itab[i + 1];
+__device__ __noinline__ void inject_cta(const SweepArgs& a, int cta, int tid) {
+    const int e0 = __ldg(a.inj_tab + cta), e1 = __ldg(a.inj_tab + cta + 1);
     for (int e = e0 + tid; e < e1; e += NT) {
-        const long long o = a.inj_off[e];
-        const float delta = a.inj_coef[e] * __ldg(a.inj_row + a.inj_pt[e]);
+        const long long o = __ldg(a.inj_off + e);
+        const float delta = __ldg(a.inj_coef + e) * __ldg(a.inj_row + __ldg(a.inj_pt + e));
         atomicAdd(a.out + o, delta);
         if constexpr (GRAD)
             if (a.inj_gm[e]) atomicAdd(a.grad + o, a.nidt2 * __ldg(a.ut + o) * delta);
@@ -186,7 +187,8 @@ __global__ void __launch_bounds__(32 * (BY + 1), 4)
                    const __grid_constant__ CUtensorMap tm_c1,
                    const __grid_constant__ CUtensorMap tm_c2,
                    const __grid_constant__ CUtensorMap tm_ut,
-                   const __grid_constant__ CUtensorMap tm_gr, const SweepArgs a, const int Px,
+                   const __grid_constant__ CUtensorMap tm_gr,
+                   const __grid_constant__ SweepArgs a, const int Px,
                    const int Py, const long long py, const long long pz) {
     using T = Tile<R, BY, NY, GRAD>;
     constexpr int Q = T::Q;
@@ -207,10 +209,14 @@ __global__ void __launch_bounds__(32 * (BY + 1), 4)
     const int n = ze - zb;
     const int x = x0 + lx;
 
-    auto issue = [&](int stage, int z) {
+    // Separable damping: the producer also stages -ez[z] in the (then unused)
+    // c1 slot of the stage, ordered before the consumers' acquire by the
+    // release of its arrive.
+    auto issue = [&](int stage, int z, float nez) {
         float* sb = smem + stage * T::SF;
         uint64_t* bar = &full[stage];
         const bool sep = a.ez != nullptr;  // c1 formed from the damping profiles
+        if (sep) sb[T::HF + 2 * T::CF] = nez;
         mbar_arrive_expect_tx(bar, sep ? T::BYTES - 4u * T::CF : T::BYTES);
         tma_load_4d(sb, &tm_uh, x0 - T::RA, y0 - R, z, a.row_u1, bar);
         tma_load_4d(sb + T::HF, &tm_uc, x0, y0, z + R, a.row_u1, bar);
@@ -235,44 +241,24 @@ __global__ void __launch_bounds__(32 * (BY + 1), 4)
     __syncthreads();
     if (threadIdx.y == BY) {  // producer warp: one lane streams the planes
         pdl_wait();
-        if (lx == 0)
+        if (lx == 0) {
+            const float* ez = a.ez ? a.ez + zb : nullptr;
+            float nxt = ez ? -__ldg(ez) : 0.0f;
             for (int j = 0; j < n; ++j) {
                 const int st = j % S;
+                const float cur = nxt;
+                if (ez && j + 1 < n) nxt = -__ldg(ez + j + 1);
                 if (j >= S) mbar_wait(&empty[st], static_cast<uint32_t>((j / S - 1) & 1));
-                issue(st, zb + j);
+                issue(st, zb + j, cur);
             }
+        }
         return;
     }
 
     const int cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
-    // Plane ranges with fused sparse work: loaded once, so planes without
-    // sparse work (nearly all) never touch the tables.
-    const int* stab = a.smp_tab ? a.smp_tab + static_cast<long long>(cta) * (a.zchunk + 1) : nullptr;
-    const int* itab = a.inj_tab ? a.inj_tab + static_cast<long long>(cta) * (a.zchunk + 1) : nullptr;
-    const int2 srng = stab ? a.smp_rng[cta] : make_int2(0, 0);
-    const int2 irng = itab ? a.inj_rng[cta] : make_int2(0, 0);
-    // Warm L2 with this CTA's entry records so the planes that use them do
-    // not stall on DRAM latency.
-    auto prefetch = [&](const void* base, long long bytes) {
-        const char* b = static_cast<const char*>(base);
-        for (long long o = tid * 128LL; o < bytes; o += NT * 128LL)
-            asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(b + o));
-    };
-    if (srng.y > srng.x) {
-        const int e0 = stab[srng.x], e1 = stab[srng.y];
-        prefetch(a.smp_hidx + e0, 4LL * (e1 - e0));
-        prefetch(a.smp_pt + e0, 4LL * (e1 - e0));
-        prefetch(a.smp_w + 8LL * e0, 32LL * (e1 - e0));
-    }
-    if (irng.y > irng.x) {
-        const int e0 = itab[irng.x], e1 = itab[irng.y];
-        prefetch(a.inj_off + e0, 8LL * (e1 - e0));
-        prefetch(a.inj_coef + e0, 4LL * (e1 - e0));
-        prefetch(a.inj_pt + e0, 4LL * (e1 - e0));
-    }
-
     // Everything below reads or writes rows the previous sweep touches.
     pdl_wait();
+    if (a.smp_base) sample_cta<NT>(a, py, pz, cta, gridDim.x * gridDim.y * gridDim.z, tid);
 
     // Queue slot of plane zb - R + t is t mod Q.
     // Rows inside the allocation.  Halo and pad cells of a row are stored too:
@@ -351,7 +337,7 @@ __global__ void __launch_bounds__(32 * (BY + 1), 4)
             ya[k] = f2(hA[k * T::BW], hB[k * T::BW]);
             yb[k] = f2(hA[(NY + R + k) * T::BW], hB[(NY + R + k) * T::BW]);
         }
-        const float nez = sep ? -__ldg(a.ez + zb + i) : 0.0f;
+        const float nez = sep ? C1[0] : 0.0f;  // -ez[z], staged by the producer
 
 #pragma unroll
         for (int j = 0; j < NY; ++j) {
@@ -399,20 +385,9 @@ __global__ void __launch_bounds__(32 * (BY + 1), 4)
 #pragma unroll
                 for (int t = 0; t < 2 * R; ++t) q[j][t] = q[j][t + 1];
         }
-        // Fused Sample from the staged u1 plane (see SweepArgs): first halves
-        // (corners 0..3) of receivers based on this plane, second halves
-        // (4..7) of those based on the previous one.  Entry e is handled by
-        // the same thread in both passes, so its half sum needs no barrier.
-        if (i >= srng.x && i < srng.y) sample_plane<T::BW, NT>(a, H, stab, i, tid);
         // Release the stage to the producer (one arrival per consumer warp).
         __syncwarp();
         if (lx == 0) mbar_arrive(&empty[st]);
-        // Fused Inject (see SweepArgs) after all consumer warps stored this
-        // plane (named barrier over the consumer warps only).
-        if (i >= irng.x && i < irng.y) {
-            named_barrier_sync(1, NT);
-            inject_plane<GRAD, NT>(a, itab, i, tid);
-        }
         if (++stage == S) {
             stage = 0;
             phase ^= 1u;
@@ -427,6 +402,12 @@ __global__ void __launch_bounds__(32 * (BY + 1), 4)
         }
     } else {
         for (int i = 0; i < n; ++i) plane(IC<0>{}, i);
+    }
+    // Fused Inject once every consumer warp has stored its planes (named
+    // barrier over the consumer warps only).
+    if (a.inj_tab) {
+        named_barrier_sync(1, NT);
+        inject_cta<GRAD, NT>(a, cta, tid);
     }
 }
 
@@ -459,7 +440,8 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
                         const __grid_constant__ CUtensorMap tm_c1,
                         const __grid_constant__ CUtensorMap tm_c2,
                         const __grid_constant__ CUtensorMap tm_ut,
-                        const __grid_constant__ CUtensorMap tm_gr, const SweepArgs a,
+                        const __grid_constant__ CUtensorMap tm_gr,
+                   const __grid_constant__ SweepArgs a,
                         const int Px, const int Py, const long long py, const long long pz) {
     using T = Tile<R, BY, NY, GRAD>;
     constexpr int Q = T::Q;
@@ -479,10 +461,14 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
     if (zb >= ze) return;
     const int n = ze - zb;
 
-    auto issue = [&](int stage, int z) {
+    // Separable damping: the producer also stages -ez[z] in the (then unused)
+    // c1 slot of the stage, ordered before the consumers' acquire by the
+    // release of its arrive.
+    auto issue = [&](int stage, int z, float nez) {
         float* sb = smem + stage * T::SF;
         uint64_t* bar = &full[stage];
         const bool sep = a.ez != nullptr;  // c1 formed from the damping profiles
+        if (sep) sb[T::HF + 2 * T::CF] = nez;
         mbar_arrive_expect_tx(bar, sep ? T::BYTES - 4u * T::CF : T::BYTES);
         tma_load_4d(sb, &tm_uh, x0 - T::RA, y0 - R, z, a.row_u1, bar);
         tma_load_4d(sb + T::HF, &tm_uc, x0, y0, z + R, a.row_u1, bar);
@@ -507,38 +493,23 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
     __syncthreads();
     if (threadIdx.y == BY) {
         pdl_wait();
-        if (lx == 0)
+        if (lx == 0) {
+            const float* ez = a.ez ? a.ez + zb : nullptr;
+            float nxt = ez ? -__ldg(ez) : 0.0f;
             for (int j = 0; j < n; ++j) {
                 const int st = j % S;
+                const float cur = nxt;
+                if (ez && j + 1 < n) nxt = -__ldg(ez + j + 1);
                 if (j >= S) mbar_wait(&empty[st], static_cast<uint32_t>((j / S - 1) & 1));
-                issue(st, zb + j);
+                issue(st, zb + j, cur);
             }
+        }
         return;
     }
 
     const int cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
-    const int* stab = a.smp_tab ? a.smp_tab + static_cast<long long>(cta) * (a.zchunk + 1) : nullptr;
-    const int* itab = a.inj_tab ? a.inj_tab + static_cast<long long>(cta) * (a.zchunk + 1) : nullptr;
-    const int2 srng = stab ? a.smp_rng[cta] : make_int2(0, 0);
-    const int2 irng = itab ? a.inj_rng[cta] : make_int2(0, 0);
-    auto prefetch = [&](const void* base, long long bytes) {
-        const char* b = static_cast<const char*>(base);
-        for (long long o = tid * 128LL; o < bytes; o += NT * 128LL)
-            asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(b + o));
-    };
-    if (srng.y > srng.x) {
-        const int e0 = stab[srng.x], e1 = stab[srng.y];
-        prefetch(a.smp_hidx + e0, 4LL * (e1 - e0));
-        prefetch(a.smp_pt + e0, 4LL * (e1 - e0));
-        prefetch(a.smp_w + 8LL * e0, 32LL * (e1 - e0));
-    }
-    if (irng.y > irng.x) {
-        const int e0 = itab[irng.x], e1 = itab[irng.y];
-        prefetch(a.inj_off + e0, 8LL * (e1 - e0));
-        prefetch(a.inj_coef + e0, 4LL * (e1 - e0));
-        prefetch(a.inj_pt + e0, 4LL * (e1 - e0));
-    }
     pdl_wait();
+    if (a.smp_base) sample_cta<NT>(a, py, pz, cta, gridDim.x * gridDim.y * gridDim.z, tid);
 
     const int px = lx & 15, gy = lx >> 4;
     const int r0 = (threadIdx.y * 2 + gy) * NY;  // first tile row of this thread
@@ -579,12 +550,15 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
     const long long rowb = py * 4, planeb = pz * 4;
     const long long gdiff = GRAD ? reinterpret_cast<char*>(a.grad) - reinterpret_cast<char*>(a.out) : 0;
 
+    // With UN a multiple of S every unrolled phase uses a fixed stage, so the
+    // stage addresses are compile-time offsets.
+    constexpr bool SST = UN % S == 0;
     int stage = 0;
     uint32_t phase = 0;
     auto plane = [&](auto ph_c, const int i) {
         constexpr int PH = decltype(ph_c)::value;
         auto slot = [](int off) { return ROT ? ((PH + off + R) % Q + Q) % Q : PH + R + off; };
-        const int st = stage;
+        const int st = SST ? PH % S : stage;
         mbar_wait(&full[st], phase);
         const float* H = smem + st * T::SF;
         const float* Cq = H + T::HF;
@@ -604,7 +578,7 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
             yu[k - 1] = ld2(hp - k * T::BW);
             yd[k - 1] = ld2(hp + (NY - 1 + k) * T::BW);
         }
-        const float nez = sep ? -__ldg(a.ez + zb + i) : 0.0f;
+        const float nez = sep ? C1[0] : 0.0f;  // -ez[z], staged by the producer
 
 #pragma unroll
         for (int j = 0; j < NY; ++j) {
@@ -650,14 +624,11 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
         }
         cur += planeb;
 
-        if (i >= srng.x && i < srng.y) sample_plane<T::BW, NT>(a, H, stab, i, tid);
         __syncwarp();
         if (lx == 0) mbar_arrive(&empty[st]);
-        if (i >= irng.x && i < irng.y) {
-            named_barrier_sync(1, NT);
-            inject_plane<GRAD, NT>(a, itab, i, tid);
-        }
-        if (++stage == S) {
+        if constexpr (SST) {
+            if constexpr (PH % S == S - 1) phase ^= 1u;
+        } else if (++stage == S) {
             stage = 0;
             phase ^= 1u;
         }
@@ -673,6 +644,10 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
 #pragma unroll
                 for (int t = 0; t < 2 * R; ++t) q[j][t] = q[j][t + UN];
         }
+    }
+    if (a.inj_tab) {
+        named_barrier_sync(1, NT);
+        inject_cta<GRAD, NT>(a, cta, tid);
     }
 }
 
@@ -731,9 +706,11 @@ cudaError_t launch3d_r(const FieldGeom& g, const SweepConfig& cfg, const SweepMa
     // CTAs the kernel is compiled for) follows from the z queue, ny (2R+1)
     // float2 per thread.
     constexpr int MB2 = R <= 4 ? 4 : (R <= 6 ? 3 : 2);  // ny = 2, 4 warps
-#define SFDB_P(BY, NY, S, MINB, ROTV)                                                       \
-    if (cfg.pair && cfg.by == BY && cfg.ny == NY && cfg.stages == S && cfg.rot == ROTV)     \
+#define SFDB_PM(BY, NY, S, MINB, ROTV, M)                                                   \
+    if (cfg.pair && cfg.by == BY && cfg.ny == NY && cfg.stages == S && cfg.rot == ROTV &&   \
+        cfg.minb == M)                                                                      \
         return launch3d_pair_t<R, BY, NY, S, GRAD, MINB, z_unroll<R, ROTV>()>(g, cfg, m, a, s, occ);
+#define SFDB_P(BY, NY, S, MINB, ROTV) SFDB_PM(BY, NY, S, MINB, ROTV, 0)
     SFDB_P(4, 2, 4, MB2, 0)
     SFDB_P(4, 2, 3, (R <= 4 ? 4 : 3), 0)
     SFDB_P(4, 1, 4, 4, 0)
@@ -748,8 +725,14 @@ cudaError_t launch3d_r(const FieldGeom& g, const SweepConfig& cfg, const SweepMa
         SFDB_P(4, 2, 3, 4, 3)
         SFDB_P(4, 2, 4, 4, 3)
         SFDB_P(4, 2, 3, 4, 4)
+        // three resident CTAs: ~20 % more registers, fewer rematerialised
+        // addresses per plane
+        SFDB_PM(4, 2, 4, 3, 4, 3)
+        SFDB_PM(4, 2, 3, 3, 3, 3)
+        SFDB_PM(4, 2, 4, 3, 1, 3)
     }
 #undef SFDB_P
+#undef SFDB_PM
     if (cfg.pair) return cudaErrorInvalidConfiguration;
 #define SFDB_V(BY, NY, S)                                              \
     if (cfg.by == BY && cfg.ny == NY && cfg.stages == S)               \
