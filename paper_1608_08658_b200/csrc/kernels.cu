@@ -300,7 +300,10 @@ size_t sweep3d_smem_bytes(int R, const SweepConfig& cfg, bool grad) {
     const int BW = cfg.bw(R);
     const int HF = ((TY + 2 * R) * BW + 31) & ~31;
     const int CF = TY * 32;
-    const int SF = HF + (grad ? 6 : 4) * CF;
+    // sweep3d.cuh Tile: the separable layout drops the c1 box and keeps 32
+    // floats for -ez[z]
+    const bool sep = cfg.pair && cfg.sep;
+    const int SF = HF + ((grad ? 6 : 4) - (sep ? 1 : 0)) * CF + (sep ? 32 : 0);
     return static_cast<size_t>(cfg.stages) * SF * 4 + cfg.stages * 16 + 128;
 }
 

@@ -94,8 +94,8 @@ struct SweepConfig {        // 3-D tiling, chosen by choose_config()
     int zlen = 1;           // planes per z chunk
     int pdl = 1;            // programmatic dependent launch (overlap launch + CTA setup)
     int pair = 0;           // thread owns column pairs x, x+1 (sweep3d_pair_kernel)
-    int minb = 0;           // pair mapping: resident CTAs the registers are budgeted for
-                            // (0 = the variant's default, sweep3d.cuh launch3d_r)
+    int sep = 1;            // pair mapping: separable-damping stage layout (no c1 box);
+                            // must match SweepArgs::ez != nullptr
     int tiles_x = 0, tiles_y = 0;
     size_t smem_bytes = 0;
     int ty() const { return 2 * by * ny; }

@@ -139,14 +139,14 @@ void validate(const sfdb200_desc& d) {
 // 4 or 2 only (queue shifted every 4 / 2 planes), since the fully unrolled
 // rotation overflows the instruction cache.  The half-tile mapping stays as a
 // candidate.
-struct V { int by, ny, stages, pair = 0, rot = 1, minb = 0; };
+struct V { int by, ny, stages, pair = 0, rot = 1; };
 std::vector<V> sweep_variants(int R) {
     if (R <= 4)
         return {{4, 2, 3, 1, 0}, {4, 2, 4, 1, 1}, {4, 2, 4, 1, 3}, {4, 2, 4, 1, 2}, {4, 2, 3, 1, 1},
                 {4, 2, 4, 1, 0}, {4, 1, 4, 1, 0}, {4, 2, 3}, {4, 1, 4}, {4, 2, 4, 1, 4},
-                {4, 2, 4, 1, 4, 3}, {4, 2, 3, 1, 3, 3}, {4, 2, 4, 1, 1, 3}};
+                {4, 2, 5, 1, 0}, {4, 2, 5, 1, 5}};
     return {{4, 2, 4, 1, 4}, {4, 2, 4, 1, 2}, {4, 2, 4, 1, 0}, {4, 2, 3, 1, 0}, {8, 2, 3, 1, 1},
-            {4, 1, 4, 1, 0}, {4, 1, 4}, {4, 1, 3}};
+            {4, 1, 4, 1, 0}, {4, 1, 4}, {4, 1, 3}, {4, 2, 5, 1, 0}, {4, 2, 5, 1, 5}};
 }
 
 // 3-D tiling of the interior launch [zint_lo, zint_hi): 32-column x tiles,
@@ -156,11 +156,12 @@ std::vector<V> sweep_variants(int R) {
 void choose_config(sfdb200_plan& p) {
     const int R = p.g.R;
     const int zupd = std::max(1, p.zint_hi - p.zint_lo);
+    // The first compiled variant for this layout (the list starts with the
+    // measured best on B200; autotune() times the rest).
     std::vector<V> variants = sweep_variants(R);
-    variants.resize(1);  // the measured best on B200 (autotune() times the rest)
     if (const char* t = std::getenv("SFDB200_TILE")) {
         V v{4, 2, 4};
-        std::sscanf(t, "%d,%d,%d,%d,%d,%d", &v.by, &v.ny, &v.stages, &v.rot, &v.pair, &v.minb);
+        std::sscanf(t, "%d,%d,%d,%d,%d", &v.by, &v.ny, &v.stages, &v.rot, &v.pair);
         variants = {v};
     }
     const int zc_env = env_int("SFDB200_ZCHUNKS", 0);
@@ -173,7 +174,7 @@ void choose_config(sfdb200_plan& p) {
         c.stages = v.stages;
         c.pair = v.pair;
         c.rot = v.pair ? v.rot : 1;
-        c.minb = v.pair ? v.minb : 0;
+        c.sep = p.sep_layout;
         c.tiles_x = static_cast<int>((p.g.Px - R + 31) / 32);  // tiles start at x = 0 (TMA alignment)
         c.tiles_y = static_cast<int>((p.g.Py - 2 * R + c.ty() - 1) / c.ty());
         c.smem_bytes = sweep3d_smem_bytes(R, c, p.grad_kind());
@@ -208,6 +209,7 @@ void choose_config(sfdb200_plan& p) {
                 pick.zlen = zlen;
             }
         }
+        if (best >= 0) break;
     }
     if (best < 0) fail(SFDB200_ECUDA, "no sweep variant fits this device");
     pick.pdl = env_int("SFDB200_PDL", 1);
@@ -419,7 +421,7 @@ void autotune(sfdb200_plan& p) {
             c.stages = v.stages;
             c.pair = v.pair;
             c.rot = v.rot;
-            c.minb = v.minb;
+            c.sep = p.sep_layout;
             c.tiles_y = static_cast<int>((p.g.Py - 2 * R + c.ty() - 1) / c.ty());
             c.smem_bytes = sweep3d_smem_bytes(R, c, p.grad_kind());
             c.zlen = (zupd + zc - 1) / zc;
@@ -484,6 +486,12 @@ void do_upload(sfdb200_plan& p, void** argv) {
         ck(cudaMemcpyAsync(&bad, p.flag, sizeof bad, cudaMemcpyDeviceToHost, p.stream), "D2H");
         ck(cudaStreamSynchronize(p.stream), "damp profiles");
         p.sep_damp = bad == 0;
+    }
+    if (p.g.ndim == 3 && p.sep_layout != p.sep_damp) {  // re-tile for the other stage layout
+        p.sep_layout = p.sep_damp;
+        p.tuned = false;
+        choose_config(p);
+        build_maps(p);
     }
     p.base.ez = p.sep_damp ? p.eprof : nullptr;
     p.base.ey = p.sep_damp ? p.eprof + p.g.Pz : nullptr;
@@ -1448,7 +1456,7 @@ int sfdb200_plan_info(const sfdb200_plan* p, char* buf, long len) {
                       "\"stages\": %d, \"tiles\": [%d, %d], \"zchunks\": %d, \"zlen\": %d, "
                       "\"smem_bytes\": %zu, \"fused_sparse\": %s, \"slab\": [%ld, %ld], "
                       "\"x_pitch\": %d, \"mapping\": \"%s\", \"pdl\": %s, "
-                      "\"separable_damping\": %s, \"bytes_per_point\": %d, \"cluster2d_ctas\": %d, \"z_unroll\": %d, \"variant\": \"%d,%d,%d,%d,%d,%d\"}",
+                      "\"separable_damping\": %s, \"bytes_per_point\": %d, \"cluster2d_ctas\": %d, \"z_unroll\": %d, \"variant\": \"%d,%d,%d,%d,%d\"}",
                       c.ty(), c.by + 1, 2 * c.ny, c.stages, c.tiles_x, c.tiles_y, c.zchunks,
                       c.zlen, c.smem_bytes, p->fused ? "true" : "false", p->zoff + p->g.R,
                       p->zoff + p->g.Pz - p->g.R, p->g.XP,
@@ -1459,7 +1467,7 @@ int sfdb200_plan_info(const sfdb200_plan* p, char* buf, long len) {
                       c.pdl ? "true" : "false", p->sep_damp ? "true" : "false",
                       (p->grad_kind() ? 32 : 20) - (p->sep_damp ? 4 : 0), p->nc2d,
                       c.rot == 1 ? 2 * p->g.R + 1 : (c.rot == 0 ? 1 : c.rot), c.by, c.ny,
-                      c.stages, c.rot, c.pair, c.minb);
+                      c.stages, c.rot, c.pair);
     });
 }
 

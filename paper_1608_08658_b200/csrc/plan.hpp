@@ -153,6 +153,7 @@ struct sfdb200_plan {
     float* eprof = nullptr;  // 3-D: damp/dt profiles ez[Pz], ey[Py], ex[Px] (SweepArgs::ez)
     unsigned long long* eprof_scratch = nullptr;
     bool sep_damp = false;   // the uploaded damp field is max-separable
+    bool sep_layout = true;  // the tiling uses the separable stage layout (cfg.sep)
     // Uniform checkpointing (forward plans, 3-D): every ck_interval steps the
     // two latest rows are copied to ck_store (pairs 0..ck_pairs-1; pair j-1
     // restarts segment j, see do_execute_checkpointed).

@@ -93,7 +93,11 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, i
         : "memory");
 }
 
-template <int R, int BY, int NY, bool GRAD>
+// Stage layout: [u1 halo box][u1 centre R planes ahead][u2][c2][c1][ut][grad]
+// (c1 only without SEP; ut, grad only with GRAD).  SEP (separable damping,
+// c1 formed in registers) drops the c1 box and reserves 32 floats for the
+// producer's -ez[z] instead.
+template <int R, int BY, int NY, bool GRAD, bool SEP = false>
 struct Tile {
     static constexpr int TX = 32;
     static constexpr int HALF = BY * NY;  // rows per tile half
@@ -104,8 +108,11 @@ struct Tile {
     static constexpr int BW = TX + 2 * RA;                     // halo row pitch
     static constexpr int HF = ((TY + 2 * R) * BW + 31) & ~31;  // halo floats, 128 B multiple
     static constexpr int CF = TY * TX;                         // centre box floats
-    static constexpr int NC = GRAD ? 6 : 4;                    // u1c, u2, c1, c2, [ut, grad]
-    static constexpr int SF = HF + NC * CF;                    // floats per stage
+    static constexpr int NC = (GRAD ? 6 : 4) - (SEP ? 1 : 0);  // centre boxes per stage
+    static constexpr int O_U1C = HF, O_U2 = HF + CF, O_C2 = HF + 2 * CF, O_C1 = HF + 3 * CF;
+    static constexpr int O_UT = HF + (SEP ? 3 : 4) * CF, O_GR = O_UT + CF;
+    static constexpr int O_NEZ = HF + NC * CF;                 // SEP: -ez[z]
+    static constexpr int SF = HF + NC * CF + (SEP ? 32 : 0);   // floats per stage
     // Bytes the TMA boxes of one stage deliver (the mbarrier transaction count).
     static constexpr uint32_t BYTES = static_cast<uint32_t>((TY + 2 * R) * BW + NC * CF) * 4u;
     static constexpr int Q = 2 * R + 1;                        // z-queue length
@@ -216,16 +223,16 @@ __global__ void __launch_bounds__(32 * (BY + 1), 4)
         float* sb = smem + stage * T::SF;
         uint64_t* bar = &full[stage];
         const bool sep = a.ez != nullptr;  // c1 formed from the damping profiles
-        if (sep) sb[T::HF + 2 * T::CF] = nez;
+        if (sep) sb[T::O_C1] = nez;
         mbar_arrive_expect_tx(bar, sep ? T::BYTES - 4u * T::CF : T::BYTES);
         tma_load_4d(sb, &tm_uh, x0 - T::RA, y0 - R, z, a.row_u1, bar);
-        tma_load_4d(sb + T::HF, &tm_uc, x0, y0, z + R, a.row_u1, bar);
-        tma_load_4d(sb + T::HF + T::CF, &tm_uc, x0, y0, z, a.row_u2, bar);
-        if (!sep) tma_load_4d(sb + T::HF + 2 * T::CF, &tm_c1, x0, y0, z, 0, bar);
-        tma_load_4d(sb + T::HF + 3 * T::CF, &tm_c2, x0, y0, z, 0, bar);
+        tma_load_4d(sb + T::O_U1C, &tm_uc, x0, y0, z + R, a.row_u1, bar);
+        tma_load_4d(sb + T::O_U2, &tm_uc, x0, y0, z, a.row_u2, bar);
+        if (!sep) tma_load_4d(sb + T::O_C1, &tm_c1, x0, y0, z, 0, bar);
+        tma_load_4d(sb + T::O_C2, &tm_c2, x0, y0, z, 0, bar);
         if constexpr (GRAD) {
-            tma_load_4d(sb + T::HF + 4 * T::CF, &tm_ut, x0, y0, z, a.row_ut, bar);
-            tma_load_4d(sb + T::HF + 5 * T::CF, &tm_gr, x0, y0, z, 0, bar);
+            tma_load_4d(sb + T::O_UT, &tm_ut, x0, y0, z, a.row_ut, bar);
+            tma_load_4d(sb + T::O_GR, &tm_gr, x0, y0, z, 0, bar);
         }
     };
 
@@ -316,12 +323,12 @@ __global__ void __launch_bounds__(32 * (BY + 1), 4)
         const int st = stage;
         mbar_wait(&full[st], phase);
         const float* H = smem + st * T::SF;
-        const float* Cq = H + T::HF;
-        const float* U2 = Cq + T::CF;
-        const float* C1 = U2 + T::CF;
-        const float* C2 = C1 + T::CF;
-        const float* UT = C2 + T::CF;
-        const float* GR = UT + T::CF;  // the gradient plane, staged like the rest
+        const float* Cq = H + T::O_U1C;
+        const float* U2 = H + T::O_U2;
+        const float* C1 = H + T::O_C1;
+        const float* C2 = H + T::O_C2;
+        const float* UT = H + T::O_UT;
+        const float* GR = H + T::O_GR;  // the gradient plane, staged like the rest
         const int ca = ly0 * T::TX + lx, cb = ca + T::HALF * T::TX;
 
 #pragma unroll
@@ -433,7 +440,7 @@ __device__ __forceinline__ void st2(float* p, float2 v) { *reinterpret_cast<floa
 template <int R, int ROTV>
 constexpr int z_unroll() { return ROTV == 1 ? 2 * R + 1 : (ROTV == 0 ? 1 : ROTV); }
 
-template <int R, int BY, int NY, int S, bool GRAD, int MINB, int UN>
+template <int R, int BY, int NY, int S, bool GRAD, int MINB, int UN, bool SEP>
 __global__ void __launch_bounds__(32 * (BY + 1), MINB)
     sweep3d_pair_kernel(const __grid_constant__ CUtensorMap tm_uh,
                         const __grid_constant__ CUtensorMap tm_uc,
@@ -443,7 +450,7 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
                         const __grid_constant__ CUtensorMap tm_gr,
                    const __grid_constant__ SweepArgs a,
                         const int Px, const int Py, const long long py, const long long pz) {
-    using T = Tile<R, BY, NY, GRAD>;
+    using T = Tile<R, BY, NY, GRAD, SEP>;
     constexpr int Q = T::Q;
     constexpr int WL = (R + 1) & ~1;  // x window [x - WL, x + 1 + WL], 8-byte aligned
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -461,23 +468,21 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
     if (zb >= ze) return;
     const int n = ze - zb;
 
-    // Separable damping: the producer also stages -ez[z] in the (then unused)
-    // c1 slot of the stage, ordered before the consumers' acquire by the
-    // release of its arrive.
+    // SEP: the producer also stages -ez[z], ordered before the consumers'
+    // acquire by the release of its arrive.
     auto issue = [&](int stage, int z, float nez) {
         float* sb = smem + stage * T::SF;
         uint64_t* bar = &full[stage];
-        const bool sep = a.ez != nullptr;  // c1 formed from the damping profiles
-        if (sep) sb[T::HF + 2 * T::CF] = nez;
-        mbar_arrive_expect_tx(bar, sep ? T::BYTES - 4u * T::CF : T::BYTES);
+        if constexpr (SEP) sb[T::O_NEZ] = nez;
+        mbar_arrive_expect_tx(bar, T::BYTES);
         tma_load_4d(sb, &tm_uh, x0 - T::RA, y0 - R, z, a.row_u1, bar);
-        tma_load_4d(sb + T::HF, &tm_uc, x0, y0, z + R, a.row_u1, bar);
-        tma_load_4d(sb + T::HF + T::CF, &tm_uc, x0, y0, z, a.row_u2, bar);
-        if (!sep) tma_load_4d(sb + T::HF + 2 * T::CF, &tm_c1, x0, y0, z, 0, bar);
-        tma_load_4d(sb + T::HF + 3 * T::CF, &tm_c2, x0, y0, z, 0, bar);
+        tma_load_4d(sb + T::O_U1C, &tm_uc, x0, y0, z + R, a.row_u1, bar);
+        tma_load_4d(sb + T::O_U2, &tm_uc, x0, y0, z, a.row_u2, bar);
+        if constexpr (!SEP) tma_load_4d(sb + T::O_C1, &tm_c1, x0, y0, z, 0, bar);
+        tma_load_4d(sb + T::O_C2, &tm_c2, x0, y0, z, 0, bar);
         if constexpr (GRAD) {
-            tma_load_4d(sb + T::HF + 4 * T::CF, &tm_ut, x0, y0, z, a.row_ut, bar);
-            tma_load_4d(sb + T::HF + 5 * T::CF, &tm_gr, x0, y0, z, 0, bar);
+            tma_load_4d(sb + T::O_UT, &tm_ut, x0, y0, z, a.row_ut, bar);
+            tma_load_4d(sb + T::O_GR, &tm_gr, x0, y0, z, 0, bar);
         }
     };
 
@@ -494,12 +499,12 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
     if (threadIdx.y == BY) {
         pdl_wait();
         if (lx == 0) {
-            const float* ez = a.ez ? a.ez + zb : nullptr;
-            float nxt = ez ? -__ldg(ez) : 0.0f;
+            const float* ez = SEP ? a.ez + zb : nullptr;
+            float nxt = SEP ? -__ldg(ez) : 0.0f;
             for (int j = 0; j < n; ++j) {
                 const int st = j % S;
                 const float cur = nxt;
-                if (ez && j + 1 < n) nxt = -__ldg(ez + j + 1);
+                if (SEP && j + 1 < n) nxt = -__ldg(ez + j + 1);
                 if (j >= S) mbar_wait(&empty[st], static_cast<uint32_t>((j / S - 1) & 1));
                 issue(st, zb + j, cur);
             }
@@ -536,14 +541,13 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
 #pragma unroll
     for (int k = 0; k <= R; ++k) wk[k] = f2(a.w[k], a.w[k]);
     const float2 nidt2 = f2(a.nidt2, a.nidt2);
-    const bool sep = a.ez != nullptr;
-    float2 nexy[NY];
+    float2 nexy[NY];  // SEP: -max(ey[y], ex[x]) of this thread's points (fixed along z)
 #pragma unroll
     for (int j = 0; j < NY; ++j) {
         const int y = y0 + r0 + j;
-        const float eyv = sep && y < Py ? __ldg(a.ey + y) : 0.0f;
-        nexy[j] = f2(-fmaxf(eyv, sep && x < Px ? __ldg(a.ex + x) : 0.0f),
-                     -fmaxf(eyv, sep && x + 1 < Px ? __ldg(a.ex + x + 1) : 0.0f));
+        const float eyv = SEP && y < Py ? __ldg(a.ey + y) : 0.0f;
+        nexy[j] = f2(-fmaxf(eyv, SEP && x < Px ? __ldg(a.ex + x) : 0.0f),
+                     -fmaxf(eyv, SEP && x + 1 < Px ? __ldg(a.ex + x + 1) : 0.0f));
     }
     char* cur = reinterpret_cast<char*>(a.out + static_cast<long long>(zb) * pz +
                                         static_cast<long long>(y0 + r0) * py + x);
@@ -561,12 +565,12 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
         const int st = SST ? PH % S : stage;
         mbar_wait(&full[st], phase);
         const float* H = smem + st * T::SF;
-        const float* Cq = H + T::HF;
-        const float* U2 = Cq + T::CF;
-        const float* C1 = U2 + T::CF;
-        const float* C2 = C1 + T::CF;
-        const float* UT = C2 + T::CF;
-        const float* GR = UT + T::CF;
+        const float* Cq = H + T::O_U1C;
+        const float* U2 = H + T::O_U2;
+        const float* C1 = H + T::O_C1;
+        const float* C2 = H + T::O_C2;
+        const float* UT = H + T::O_UT;
+        const float* GR = H + T::O_GR;
         const int cidx = r0 * T::TX + 2 * px;
 #pragma unroll
         for (int j = 0; j < NY; ++j) q[j][slot(R)] = ld2(Cq + cidx + j * T::TX);
@@ -578,7 +582,7 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
             yu[k - 1] = ld2(hp - k * T::BW);
             yd[k - 1] = ld2(hp + (NY - 1 + k) * T::BW);
         }
-        const float nez = sep ? C1[0] : 0.0f;  // -ez[z], staged by the producer
+        const float nez = SEP ? H[T::O_NEZ] : 0.0f;  // -ez[z], staged by the producer
 
 #pragma unroll
         for (int j = 0; j < NY; ++j) {
@@ -609,7 +613,7 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
             const int ci = cidx + j * T::TX;
             const float2 d = fma2(ld2(U2 + ci), mone, c0);
             const float2 c2v = ld2(C2 + ci);
-            const float2 c1v = sep ? fma2(f2(fminf(nez, nexy[j].x), fminf(nez, nexy[j].y)), c2v,
+            const float2 c1v = SEP ? fma2(f2(fminf(nez, nexy[j].x), fminf(nez, nexy[j].y)), c2v,
                                           f2(1.0f, 1.0f))
                                    : ld2(C1 + ci);
             const float2 inc = fma2(c1v, d, mul2(c2v, lap));
@@ -675,10 +679,11 @@ cudaError_t launch3d_t(const FieldGeom& g, const SweepConfig& cfg, const SweepMa
                               g.py, g.pz);
 }
 
-template <int R, int BY, int NY, int S, bool GRAD, int MINB, int UN>
+template <int R, int BY, int NY, int S, bool GRAD, int MINB, int UN, bool SEP>
 cudaError_t launch3d_pair_t(const FieldGeom& g, const SweepConfig& cfg, const SweepMaps& m,
                             const SweepArgs& a, cudaStream_t s, int* occ) {
-    auto kern = sweep3d_pair_kernel<R, BY, NY, S, GRAD, MINB, UN>;
+    auto kern = sweep3d_pair_kernel<R, BY, NY, S, GRAD, MINB, UN, SEP>;
+    if (!occ && (a.ez != nullptr) != SEP) return cudaErrorInvalidValue;  // layout mismatch
     const size_t smem = sweep3d_smem_bytes(R, cfg, GRAD);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
@@ -706,33 +711,38 @@ cudaError_t launch3d_r(const FieldGeom& g, const SweepConfig& cfg, const SweepMa
     // CTAs the kernel is compiled for) follows from the z queue, ny (2R+1)
     // float2 per thread.
     constexpr int MB2 = R <= 4 ? 4 : (R <= 6 ? 3 : 2);  // ny = 2, 4 warps
-#define SFDB_PM(BY, NY, S, MINB, ROTV, M)                                                   \
-    if (cfg.pair && cfg.by == BY && cfg.ny == NY && cfg.stages == S && cfg.rot == ROTV &&   \
-        cfg.minb == M)                                                                      \
-        return launch3d_pair_t<R, BY, NY, S, GRAD, MINB, z_unroll<R, ROTV>()>(g, cfg, m, a, s, occ);
-#define SFDB_P(BY, NY, S, MINB, ROTV) SFDB_PM(BY, NY, S, MINB, ROTV, 0)
-    SFDB_P(4, 2, 4, MB2, 0)
-    SFDB_P(4, 2, 3, (R <= 4 ? 4 : 3), 0)
-    SFDB_P(4, 1, 4, 4, 0)
-    SFDB_P(4, 2, 4, MB2, 1)
-    SFDB_P(4, 2, 3, (R <= 4 ? 4 : 3), 1)
-    SFDB_P(8, 2, 3, (R <= 4 ? 2 : 1), 1)
-    // partial unrolls (queue shifted every 2 / 3 / 4 / 8 planes)
-    SFDB_P(4, 2, 4, MB2, 2)
-    SFDB_P(4, 2, 4, MB2, 4)
-    if constexpr (R >= 5) SFDB_P(4, 2, 4, MB2, 8)
+// BOTH: also compiled for streamed c1 (non-separable damping); the other
+// variants exist for the separable layout only.
+#define SFDB_P(BY, NY, S, MINB, ROTV, BOTH)                                                   \
+    if (cfg.pair && cfg.by == BY && cfg.ny == NY && cfg.stages == S && cfg.rot == ROTV) {     \
+        if (cfg.sep)                                                                          \
+            return launch3d_pair_t<R, BY, NY, S, GRAD, MINB, z_unroll<R, ROTV>(), true>(      \
+                g, cfg, m, a, s, occ);                                                        \
+        if constexpr (BOTH)                                                                   \
+            return launch3d_pair_t<R, BY, NY, S, GRAD, MINB, z_unroll<R, ROTV>(), false>(     \
+                g, cfg, m, a, s, occ);                                                        \
+        return cudaErrorInvalidConfiguration;                                                 \
+    }
+    constexpr int MB3 = R <= 4 ? 4 : 3;
+    SFDB_P(4, 2, 4, MB2, 0, 1)
+    SFDB_P(4, 2, 3, MB3, 0, 0)
+    SFDB_P(4, 1, 4, 4, 0, 0)
+    SFDB_P(4, 2, 4, MB2, 1, 0)
+    SFDB_P(4, 2, 3, MB3, 1, 0)
+    SFDB_P(8, 2, 3, (R <= 4 ? 2 : 1), 1, 0)
+    // partial unrolls (queue shifted every 2 / 3 / 4 / 5 / 8 planes); five
+    // stages fit four CTAs per SM only in the separable layout
+    SFDB_P(4, 2, 4, MB2, 2, 0)
+    SFDB_P(4, 2, 4, MB2, 4, 1)
+    SFDB_P(4, 2, 5, MB2, 0, 0)
+    SFDB_P(4, 2, 5, MB2, 5, 0)
+    if constexpr (R >= 5) SFDB_P(4, 2, 4, MB2, 8, 0)
     if constexpr (R <= 4) {
-        SFDB_P(4, 2, 3, 4, 3)
-        SFDB_P(4, 2, 4, 4, 3)
-        SFDB_P(4, 2, 3, 4, 4)
-        // three resident CTAs: ~20 % more registers, fewer rematerialised
-        // addresses per plane
-        SFDB_PM(4, 2, 4, 3, 4, 3)
-        SFDB_PM(4, 2, 3, 3, 3, 3)
-        SFDB_PM(4, 2, 4, 3, 1, 3)
+        SFDB_P(4, 2, 3, 4, 3, 0)
+        SFDB_P(4, 2, 4, 4, 3, 0)
+        SFDB_P(4, 2, 3, 4, 4, 0)
     }
 #undef SFDB_P
-#undef SFDB_PM
     if (cfg.pair) return cudaErrorInvalidConfiguration;
 #define SFDB_V(BY, NY, S)                                              \
     if (cfg.by == BY && cfg.ny == NY && cfg.stages == S)               \

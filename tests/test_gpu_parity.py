@@ -235,3 +235,43 @@ def test_damping_profiles_or_streamed_c1(kind):
     uo, ro = O.forward(model.padded, w.space_order, w.h, w.dt, w.nt, model.m, damp,
                        src.idx, src.w, w.wavelet, rec.idx, rec.w)
     assert O.rel_l2(argv[0], uo) <= TOL and O.rel_l2(argv[8], ro) <= TOL
+
+
+def test_layout_flip_on_reupload():
+    """One plan uploaded with separable, then non-separable, then separable
+    damping re-tiles for the matching stage layout each time (sweep3d.cuh
+    Tile: SEP drops the c1 box) and matches the oracle every run."""
+    from paper_1608_08658_b200 import _lib as L
+    w = configs.cfg2(n=26, nt=90, nbpml=8, nrec_side=5)
+    model, src, rec = _setup(w)
+    p = L.Plan(L.FORWARD, 3, model.padded, w.space_order, w.nt, w.dt, w.h, src.npoints,
+               rec.npoints, False, 0)
+    for k, sep in enumerate([True, False, True]):
+        damp = model.damp.copy()
+        if not sep:
+            damp[damp.size // 2 + 3] = 2e-3
+        argv = [np.zeros((3, *model.padded)), model.m, damp, src.idx, src.w, O._f64(w.wavelet),
+                rec.idx, rec.w, np.zeros((w.nt, rec.npoints))]
+        p.run(argv)
+        assert p.info()["separable_damping"] == sep, k
+        uo, ro = O.forward(model.padded, w.space_order, w.h, w.dt, w.nt, model.m, damp,
+                           src.idx, src.w, w.wavelet, rec.idx, rec.w)
+        assert O.rel_l2(argv[0], uo) <= TOL and O.rel_l2(argv[8], ro) <= TOL, k
+    p.close()
+
+
+def test_gradient_nonseparable_damping():
+    """The fused gradient kernel with a streamed c1 (non-separable damping)."""
+    w = configs.cfg2(n=24, nt=90, nbpml=8, nrec_side=5)
+    model, src, rec = _setup(w)
+    damp = model.damp.copy()
+    damp[damp.size // 2 + 7] = 1e-3
+    import dataclasses
+    model_ns = dataclasses.replace(model, damp=damp)
+    u, r = O.forward(model.padded, w.space_order, w.h, w.dt, w.nt, model.m, damp,
+                     src.idx, src.w, w.wavelet, rec.idx, rec.w, save=True)
+    resid = O._f64(np.random.default_rng(5).standard_normal(r.shape).astype(np.float32))
+    g = S.gradient(model_ns, rec, S.ShotRecord(w.nt, w.dt, rec.npoints, resid), u, w.nt, w.dt)
+    go, _ = O.gradient(model.padded, w.space_order, w.h, w.dt, w.nt, model.m, damp, u,
+                       rec.idx, rec.w, resid)
+    assert O.rel_l2(g.grad, go) <= TOL

@@ -12,11 +12,11 @@ from paper_1608_08658_b200 import configs, seismic as S
 pytestmark = pytest.mark.gpu
 TOL = 1e-5
 
-# "by,ny,stages,rot,pair[,minb]" (sweep3d.cuh launch3d_r)
+# "by,ny,stages,rot,pair" (sweep3d.cuh launch3d_r)
 LOW = ["4,2,3,0,1", "4,2,4,1,1", "4,2,3,1,1", "4,2,4,0,1", "4,2,3,1,0", "4,1,4,1,0", "8,2,3,1,1",
-       "4,2,4,4,1", "4,2,4,3,1", "4,2,4,2,1", "4,2,4,4,1,3", "4,2,3,3,1,3", "4,2,4,1,1,3"]
+       "4,2,4,4,1", "4,2,4,3,1", "4,2,4,2,1", "4,2,5,0,1", "4,2,5,5,1"]
 HIGH = ["4,2,4,4,1", "4,2,4,2,1", "4,2,4,8,1", "4,2,4,0,1", "4,2,3,0,1", "8,2,3,1,1",
-        "4,1,4,0,1", "4,1,4,1,0", "4,1,3,1,0"]
+        "4,1,4,0,1", "4,1,4,1,0", "4,1,3,1,0", "4,2,5,0,1", "4,2,5,5,1"]
 
 
 def _forced(tile):
