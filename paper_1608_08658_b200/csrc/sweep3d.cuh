@@ -3,6 +3,7 @@
 // compile in parallel.
 #pragma once
 
+#include <algorithm>
 #include <cmath>
 #include <utility>
 
@@ -116,6 +117,11 @@ struct Tile {
     // Bytes the TMA boxes of one stage deliver (the mbarrier transaction count).
     static constexpr uint32_t BYTES = static_cast<uint32_t>((TY + 2 * R) * BW + NC * CF) * 4u;
     static constexpr int Q = 2 * R + 1;                        // z-queue length
+    // Pair kernel prologue: the 2R queue planes below a z chunk arrive as
+    // PRO_S boxes of PRO_P centre planes, each within one stage.
+    static constexpr int PRO_P = 2 * R < SF / CF ? 2 * R : SF / CF;
+    static constexpr int PRO_S = (2 * R + PRO_P - 1) / PRO_P;
+    static constexpr uint32_t PRO_BYTES = static_cast<uint32_t>(PRO_P * CF) * 4u;
 };
 
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
@@ -440,6 +446,16 @@ __device__ __forceinline__ void st2(float* p, float2 v) { *reinterpret_cast<floa
 template <int R, int ROTV>
 constexpr int z_unroll() { return ROTV == 1 ? 2 * R + 1 : (ROTV == 0 ? 1 : ROTV); }
 
+// Persistent CTAs: the launch has min(items, resident slots) CTAs and CTA c
+// runs items c, c + gridDim.x, ... (item = x tile fastest, then y tile, then
+// z chunk: the hardware's own CTA order, so tiles still sweep z in step and
+// halos stay in L2).  The producer streams the next item's planes while the
+// consumers finish the current one, so the ring never drains between items,
+// and the 2R queue planes below an item's first plane arrive through the
+// ring too, as PS boxes of P planes (the prologue), instead of synchronous
+// loads.  With UN a multiple of S each item's first plane is aligned to stage
+// 0 by empty "skip" stages, so every unrolled plane phase has a fixed stage
+// and compile-time shared-memory offsets.
 template <int R, int BY, int NY, int S, bool GRAD, int MINB, int UN, bool SEP>
 __global__ void __launch_bounds__(32 * (BY + 1), MINB)
     sweep3d_pair_kernel(const __grid_constant__ CUtensorMap tm_uh,
@@ -448,11 +464,15 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
                         const __grid_constant__ CUtensorMap tm_c2,
                         const __grid_constant__ CUtensorMap tm_ut,
                         const __grid_constant__ CUtensorMap tm_gr,
-                   const __grid_constant__ SweepArgs a,
-                        const int Px, const int Py, const long long py, const long long pz) {
+                        const __grid_constant__ CUtensorMap tm_up,
+                        const __grid_constant__ SweepArgs a, const int Px, const int Py,
+                        const long long py, const long long pz, const int ntx, const int nty,
+                        const int nitems) {
     using T = Tile<R, BY, NY, GRAD, SEP>;
     constexpr int Q = T::Q;
     constexpr int WL = (R + 1) & ~1;  // x window [x - WL, x + 1 + WL], 8-byte aligned
+    constexpr int P = T::PRO_P, PS = T::PRO_S;
+    constexpr bool SST = UN % S == 0;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     float* smem = reinterpret_cast<float*>(smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u));
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * T::SF);
@@ -461,29 +481,14 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
 
     const int lx = threadIdx.x;
     const int tid = threadIdx.y * 32 + lx;
-    const int x0 = blockIdx.x * T::TX;
-    const int y0 = R + blockIdx.y * T::TY;
-    const int zb = a.zlo + blockIdx.z * a.zchunk;
-    const int ze = min(zb + a.zchunk, a.zhi);
-    if (zb >= ze) return;
-    const int n = ze - zb;
-
-    // SEP: the producer also stages -ez[z], ordered before the consumers'
-    // acquire by the release of its arrive.
-    auto issue = [&](int stage, int z, float nez) {
-        float* sb = smem + stage * T::SF;
-        uint64_t* bar = &full[stage];
-        if constexpr (SEP) sb[T::O_NEZ] = nez;
-        mbar_arrive_expect_tx(bar, T::BYTES);
-        tma_load_4d(sb, &tm_uh, x0 - T::RA, y0 - R, z, a.row_u1, bar);
-        tma_load_4d(sb + T::O_U1C, &tm_uc, x0, y0, z + R, a.row_u1, bar);
-        tma_load_4d(sb + T::O_U2, &tm_uc, x0, y0, z, a.row_u2, bar);
-        if constexpr (!SEP) tma_load_4d(sb + T::O_C1, &tm_c1, x0, y0, z, 0, bar);
-        tma_load_4d(sb + T::O_C2, &tm_c2, x0, y0, z, 0, bar);
-        if constexpr (GRAD) {
-            tma_load_4d(sb + T::O_UT, &tm_ut, x0, y0, z, a.row_ut, bar);
-            tma_load_4d(sb + T::O_GR, &tm_gr, x0, y0, z, 0, bar);
-        }
+    // item -> tile origin (x0, y0) and z range [zb, ze)
+    auto decode = [&](int item, int& x0, int& y0, int& zb, int& ze) {
+        const int r = item / ntx;
+        x0 = (item - r * ntx) * T::TX;
+        const int tz = r / nty;
+        y0 = R + (r - tz * nty) * T::TY;
+        zb = a.zlo + tz * a.zchunk;
+        ze = min(zb + a.zchunk, a.zhi);
     };
 
     pdl_trigger();
@@ -496,162 +501,232 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
         fence_barrier_init();
     }
     __syncthreads();
-    if (threadIdx.y == BY) {
+    if (threadIdx.y == BY) {  // producer warp: one lane streams every item's stages
         pdl_wait();
         if (lx == 0) {
-            const float* ez = SEP ? a.ez + zb : nullptr;
-            float nxt = SEP ? -__ldg(ez) : 0.0f;
-            for (int j = 0; j < n; ++j) {
-                const int st = j % S;
-                const float cur = nxt;
-                if (SEP && j + 1 < n) nxt = -__ldg(ez + j + 1);
-                if (j >= S) mbar_wait(&empty[st], static_cast<uint32_t>((j / S - 1) & 1));
-                issue(st, zb + j, cur);
+            uint32_t j = 0;  // stage sequence number across items
+            auto acquire = [&]() {
+                const int st = static_cast<int>(j % S);
+                if (j >= S) mbar_wait(&empty[st], ((j / S) - 1) & 1);
+                return st;
+            };
+            for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+                int x0, y0, zb, ze;
+                decode(item, x0, y0, zb, ze);
+                const int n = ze - zb;
+                if (n <= 0) continue;
+                if constexpr (SST) {
+                    while ((j + PS) % S != 0) {  // skip stage: completes on the arrive alone
+                        mbar_arrive(&full[acquire()]);
+                        ++j;
+                    }
+                }
+                for (int s = 0; s < PS; ++s) {
+                    const int st = acquire();
+                    mbar_arrive_expect_tx(&full[st], T::PRO_BYTES);
+                    tma_load_4d(smem + st * T::SF, &tm_up, x0, y0, zb - R + s * P, a.row_u1,
+                                &full[st]);
+                    ++j;
+                }
+                const float* ezp = SEP ? a.ez + zb : nullptr;
+                float nxt = 0.0f;
+                if constexpr (SEP) nxt = -__ldg(ezp);
+#pragma unroll 1
+                for (int i = 0; i < n; ++i) {
+                    const float cur = nxt;
+                    if constexpr (SEP)
+                        if (i + 1 < n) nxt = -__ldg(ezp + i + 1);
+                    const int st = acquire();
+                    float* sb = smem + st * T::SF;
+                    uint64_t* bar = &full[st];
+                    const int z = zb + i;
+                    // SEP: -ez[z] rides in the stage, ordered before the consumers'
+                    // acquire by the release of this arrive.
+                    if constexpr (SEP) sb[T::O_NEZ] = cur;
+                    mbar_arrive_expect_tx(bar, T::BYTES);
+                    tma_load_4d(sb, &tm_uh, x0 - T::RA, y0 - R, z, a.row_u1, bar);
+                    tma_load_4d(sb + T::O_U1C, &tm_uc, x0, y0, z + R, a.row_u1, bar);
+                    tma_load_4d(sb + T::O_U2, &tm_uc, x0, y0, z, a.row_u2, bar);
+                    if constexpr (!SEP) tma_load_4d(sb + T::O_C1, &tm_c1, x0, y0, z, 0, bar);
+                    tma_load_4d(sb + T::O_C2, &tm_c2, x0, y0, z, 0, bar);
+                    if constexpr (GRAD) {
+                        tma_load_4d(sb + T::O_UT, &tm_ut, x0, y0, z, a.row_ut, bar);
+                        tma_load_4d(sb + T::O_GR, &tm_gr, x0, y0, z, 0, bar);
+                    }
+                    ++j;
+                }
             }
         }
         return;
     }
 
-    const int cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
     pdl_wait();
-    if (a.smp_base) sample_cta<NT>(a, py, pz, cta, gridDim.x * gridDim.y * gridDim.z, tid);
+    if (a.smp_base) sample_cta<NT>(a, py, pz, blockIdx.x, gridDim.x, tid);
 
     const int px = lx & 15, gy = lx >> 4;
     const int r0 = (threadIdx.y * 2 + gy) * NY;  // first tile row of this thread
-    const int x = x0 + 2 * px;
+    const int cidx = r0 * T::TX + 2 * px;
     constexpr bool ROT = UN == Q;
     constexpr int QS = ROT ? Q : Q + UN - 1;  // queue slots
-    float2 q[NY][QS];
-    bool vy[NY];  // rows inside the allocation (halo cells store 0, see sweep3d_kernel)
-#pragma unroll
-    for (int j = 0; j < NY; ++j) {
-        const int y = y0 + r0 + j;
-        vy[j] = y < Py;
-        const float* c = a.u1 + static_cast<long long>(y) * py + x;
-#pragma unroll
-        for (int t = 0; t < 2 * R; ++t) {
-            const long long o = static_cast<long long>(zb - R + t) * pz;
-            q[j][t] = vy[j] ? __ldg(reinterpret_cast<const float2*>(c + o)) : f2(0.0f, 0.0f);
-        }
-    }
-
     const float2 neg2nd = f2(a.neg2nd, a.neg2nd);
     const float2 mone = f2(-1.0f, -1.0f);
     float2 wk[R + 1];
 #pragma unroll
     for (int k = 0; k <= R; ++k) wk[k] = f2(a.w[k], a.w[k]);
     const float2 nidt2 = f2(a.nidt2, a.nidt2);
-    float2 nexy[NY];  // SEP: -max(ey[y], ex[x]) of this thread's points (fixed along z)
-#pragma unroll
-    for (int j = 0; j < NY; ++j) {
-        const int y = y0 + r0 + j;
-        const float eyv = SEP && y < Py ? __ldg(a.ey + y) : 0.0f;
-        nexy[j] = f2(-fmaxf(eyv, SEP && x < Px ? __ldg(a.ex + x) : 0.0f),
-                     -fmaxf(eyv, SEP && x + 1 < Px ? __ldg(a.ex + x + 1) : 0.0f));
-    }
-    char* cur = reinterpret_cast<char*>(a.out + static_cast<long long>(zb) * pz +
-                                        static_cast<long long>(y0 + r0) * py + x);
     const long long rowb = py * 4, planeb = pz * 4;
     const long long gdiff = GRAD ? reinterpret_cast<char*>(a.grad) - reinterpret_cast<char*>(a.out) : 0;
+    uint32_t j = 0;  // stage sequence number, as the producer's
 
-    // With UN a multiple of S every unrolled phase uses a fixed stage, so the
-    // stage addresses are compile-time offsets.
-    constexpr bool SST = UN % S == 0;
-    int stage = 0;
-    uint32_t phase = 0;
-    auto plane = [&](auto ph_c, const int i) {
-        constexpr int PH = decltype(ph_c)::value;
-        auto slot = [](int off) { return ROT ? ((PH + off + R) % Q + Q) % Q : PH + R + off; };
-        const int st = SST ? PH % S : stage;
-        mbar_wait(&full[st], phase);
-        const float* H = smem + st * T::SF;
-        const float* Cq = H + T::O_U1C;
-        const float* U2 = H + T::O_U2;
-        const float* C1 = H + T::O_C1;
-        const float* C2 = H + T::O_C2;
-        const float* UT = H + T::O_UT;
-        const float* GR = H + T::O_GR;
-        const int cidx = r0 * T::TX + 2 * px;
-#pragma unroll
-        for (int j = 0; j < NY; ++j) q[j][slot(R)] = ld2(Cq + cidx + j * T::TX);
-
-        const float* hp = H + (r0 + R) * T::BW + T::RA + 2 * px;  // (row r0, column x)
-        float2 yu[R], yd[R];  // rows r0 - k and r0 + NY - 1 + k
-#pragma unroll
-        for (int k = 1; k <= R; ++k) {
-            yu[k - 1] = ld2(hp - k * T::BW);
-            yd[k - 1] = ld2(hp + (NY - 1 + k) * T::BW);
-        }
-        const float nez = SEP ? H[T::O_NEZ] : 0.0f;  // -ez[z], staged by the producer
-
-#pragma unroll
-        for (int j = 0; j < NY; ++j) {
-            float w[2 * WL + 2];
-#pragma unroll
-            for (int m = 0; m <= WL; ++m) {
-                const float2 v = ld2(hp + j * T::BW - WL + 2 * m);
-                w[2 * m] = v.x;
-                w[2 * m + 1] = v.y;
+    for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+        int x0, y0, zb, ze;
+        decode(item, x0, y0, zb, ze);
+        const int n = ze - zb;
+        if (n <= 0) continue;
+        if constexpr (SST) {
+            while ((j + PS) % S != 0) {
+                const int st = static_cast<int>(j % S);
+                mbar_wait(&full[st], (j / S) & 1);
+                __syncwarp();
+                if (lx == 0) mbar_arrive(&empty[st]);
+                ++j;
             }
-            const float2 c0 = q[j][slot(0)];
-            // Two partial sums (odd / even k) halve the dependent FFMA2 chain.
-            float2 lap = f2(0.0f, 0.0f), lap2 = f2(0.0f, 0.0f);
+        }
+        // Queue slot of plane zb - R + t is t (t < 2R): the prologue boxes.
+        float2 q[NY][QS];
+#pragma unroll
+        for (int s = 0; s < PS; ++s) {
+            const int st = static_cast<int>(j % S);
+            mbar_wait(&full[st], (j / S) & 1);
+            const float* B = smem + st * T::SF + cidx;
+#pragma unroll
+            for (int t = 0; t < P; ++t)
+                if (s * P + t < 2 * R)
+#pragma unroll
+                    for (int jj = 0; jj < NY; ++jj)
+                        q[jj][s * P + t] = ld2(B + t * T::CF + jj * T::TX);
+            __syncwarp();
+            if (lx == 0) mbar_arrive(&empty[st]);
+            ++j;
+        }
+
+        const int x = x0 + 2 * px;
+        bool vy[NY];  // rows inside the allocation (halo cells store 0, see sweep3d_kernel)
+        float2 nexy[NY];  // SEP: -max(ey[y], ex[x]) of this thread's points (fixed along z)
+#pragma unroll
+        for (int jj = 0; jj < NY; ++jj) {
+            const int y = y0 + r0 + jj;
+            vy[jj] = y < Py;
+            const float eyv = SEP && y < Py ? __ldg(a.ey + y) : 0.0f;
+            nexy[jj] = f2(-fmaxf(eyv, SEP && x < Px ? __ldg(a.ex + x) : 0.0f),
+                          -fmaxf(eyv, SEP && x + 1 < Px ? __ldg(a.ex + x + 1) : 0.0f));
+        }
+        char* cur = reinterpret_cast<char*>(a.out + static_cast<long long>(zb) * pz +
+                                            static_cast<long long>(y0 + r0) * py + x);
+
+        int stage = static_cast<int>(j % S);  // 0 with SST
+        uint32_t phase = (j / S) & 1;
+        auto plane = [&](auto ph_c, const int i) {
+            constexpr int PH = decltype(ph_c)::value;
+            auto slot = [](int off) { return ROT ? ((PH + off + R) % Q + Q) % Q : PH + R + off; };
+            const int st = SST ? PH % S : stage;
+            mbar_wait(&full[st], phase);
+            const float* H = smem + st * T::SF;
+            const float* Cq = H + T::O_U1C;
+            const float* U2 = H + T::O_U2;
+            const float* C1 = H + T::O_C1;
+            const float* C2 = H + T::O_C2;
+            const float* UT = H + T::O_UT;
+            const float* GR = H + T::O_GR;
+#pragma unroll
+            for (int jj = 0; jj < NY; ++jj) q[jj][slot(R)] = ld2(Cq + cidx + jj * T::TX);
+
+            const float* hp = H + (r0 + R) * T::BW + T::RA + 2 * px;  // (row r0, column x)
+            float2 yu[R], yd[R];  // rows r0 - k and r0 + NY - 1 + k
 #pragma unroll
             for (int k = 1; k <= R; ++k) {
-                const float2 ym = j - k >= 0 ? q[(j - k) >= 0 ? j - k : 0][slot(0)] : yu[k - j - 1];
-                const float2 yp = j + k < NY ? q[(j + k) < NY ? j + k : 0][slot(0)] : yd[j + k - NY];
-                const float2 xs = add2(f2(w[WL - k], w[WL - k + 1]), f2(w[WL + k], w[WL + k + 1]));
-                const float2 zs = add2(q[j][slot(-k)], q[j][slot(k)]);
-                float2 sk = add2(add2(xs, add2(ym, yp)), zs);
-                sk = fma2(neg2nd, c0, sk);
-                if (R >= 5 && (k & 1) == 0)
-                    lap2 = fma2(wk[k], sk, lap2);
-                else
-                    lap = fma2(wk[k], sk, lap);
+                yu[k - 1] = ld2(hp - k * T::BW);
+                yd[k - 1] = ld2(hp + (NY - 1 + k) * T::BW);
             }
-            if constexpr (R >= 5) lap = add2(lap, lap2);
-            const int ci = cidx + j * T::TX;
-            const float2 d = fma2(ld2(U2 + ci), mone, c0);
-            const float2 c2v = ld2(C2 + ci);
-            const float2 c1v = SEP ? fma2(f2(fminf(nez, nexy[j].x), fminf(nez, nexy[j].y)), c2v,
-                                          f2(1.0f, 1.0f))
-                                   : ld2(C1 + ci);
-            const float2 inc = fma2(c1v, d, mul2(c2v, lap));
-            const float2 o = add2(c0, inc);
-            char* pj = cur + j * rowb;
-            if (vy[j]) st2(reinterpret_cast<float*>(pj), o);
-            if constexpr (GRAD) {
-                const float2 vtt = fma2(d, mone, inc);
-                const float2 coef = mul2(nidt2, ld2(UT + ci));
-                if (vy[j]) st2(reinterpret_cast<float*>(pj + gdiff), fma2(coef, vtt, ld2(GR + ci)));
+            const float nez = SEP ? H[T::O_NEZ] : 0.0f;  // -ez[z], staged by the producer
+
+#pragma unroll
+            for (int jj = 0; jj < NY; ++jj) {
+                float w[2 * WL + 2];
+#pragma unroll
+                for (int m = 0; m <= WL; ++m) {
+                    const float2 v = ld2(hp + jj * T::BW - WL + 2 * m);
+                    w[2 * m] = v.x;
+                    w[2 * m + 1] = v.y;
+                }
+                const float2 c0 = q[jj][slot(0)];
+                // Two partial sums (odd / even k) halve the dependent FFMA2 chain.
+                float2 lap = f2(0.0f, 0.0f), lap2 = f2(0.0f, 0.0f);
+#pragma unroll
+                for (int k = 1; k <= R; ++k) {
+                    const float2 ym =
+                        jj - k >= 0 ? q[(jj - k) >= 0 ? jj - k : 0][slot(0)] : yu[k - jj - 1];
+                    const float2 yp =
+                        jj + k < NY ? q[(jj + k) < NY ? jj + k : 0][slot(0)] : yd[jj + k - NY];
+                    const float2 xs =
+                        add2(f2(w[WL - k], w[WL - k + 1]), f2(w[WL + k], w[WL + k + 1]));
+                    const float2 zs = add2(q[jj][slot(-k)], q[jj][slot(k)]);
+                    float2 sk = add2(add2(xs, add2(ym, yp)), zs);
+                    sk = fma2(neg2nd, c0, sk);
+                    if (R >= 5 && (k & 1) == 0)
+                        lap2 = fma2(wk[k], sk, lap2);
+                    else
+                        lap = fma2(wk[k], sk, lap);
+                }
+                if constexpr (R >= 5) lap = add2(lap, lap2);
+                const int ci = cidx + jj * T::TX;
+                const float2 d = fma2(ld2(U2 + ci), mone, c0);
+                const float2 c2v = ld2(C2 + ci);
+                const float2 c1v =
+                    SEP ? fma2(f2(fminf(nez, nexy[jj].x), fminf(nez, nexy[jj].y)), c2v,
+                               f2(1.0f, 1.0f))
+                        : ld2(C1 + ci);
+                const float2 inc = fma2(c1v, d, mul2(c2v, lap));
+                const float2 o = add2(c0, inc);
+                char* pj = cur + jj * rowb;
+                if (vy[jj]) st2(reinterpret_cast<float*>(pj), o);
+                if constexpr (GRAD) {
+                    const float2 vtt = fma2(d, mone, inc);
+                    const float2 coef = mul2(nidt2, ld2(UT + ci));
+                    if (vy[jj])
+                        st2(reinterpret_cast<float*>(pj + gdiff), fma2(coef, vtt, ld2(GR + ci)));
+                }
+            }
+            cur += planeb;
+
+            __syncwarp();
+            if (lx == 0) mbar_arrive(&empty[st]);
+            if constexpr (SST) {
+                if constexpr (PH % S == S - 1) phase ^= 1u;
+            } else if (++stage == S) {
+                stage = 0;
+                phase ^= 1u;
+            }
+        };
+
+        for (int base = 0; base < n; base += UN) {
+            [&]<int... PP>(std::integer_sequence<int, PP...>) {
+                ((base + PP < n ? (plane(IC<PP>{}, base + PP), true) : false) && ...);
+            }(std::make_integer_sequence<int, UN>{});
+            if constexpr (!ROT) {  // drop the UN oldest planes
+#pragma unroll
+                for (int jj = 0; jj < NY; ++jj)
+#pragma unroll
+                    for (int t = 0; t < 2 * R; ++t) q[jj][t] = q[jj][t + UN];
             }
         }
-        cur += planeb;
-
-        __syncwarp();
-        if (lx == 0) mbar_arrive(&empty[st]);
-        if constexpr (SST) {
-            if constexpr (PH % S == S - 1) phase ^= 1u;
-        } else if (++stage == S) {
-            stage = 0;
-            phase ^= 1u;
+        j += static_cast<uint32_t>(n);
+        // Fused Inject once every consumer warp has stored this item's planes
+        // (named barrier over the consumer warps only).
+        if (a.inj_tab && __ldg(a.inj_tab + item + 1) > __ldg(a.inj_tab + item)) {
+            named_barrier_sync(1, NT);
+            inject_cta<GRAD, NT>(a, item, tid);
         }
-    };
-
-    for (int base = 0; base < n; base += UN) {
-        [&]<int... P>(std::integer_sequence<int, P...>) {
-            ((base + P < n ? (plane(IC<P>{}, base + P), true) : false) && ...);
-        }(std::make_integer_sequence<int, UN>{});
-        if constexpr (!ROT) {  // drop the UN oldest planes
-#pragma unroll
-            for (int j = 0; j < NY; ++j)
-#pragma unroll
-                for (int t = 0; t < 2 * R; ++t) q[j][t] = q[j][t + UN];
-        }
-    }
-    if (a.inj_tab) {
-        named_barrier_sync(1, NT);
-        inject_cta<GRAD, NT>(a, cta, tid);
     }
 }
 
@@ -685,12 +760,31 @@ cudaError_t launch3d_pair_t(const FieldGeom& g, const SweepConfig& cfg, const Sw
     auto kern = sweep3d_pair_kernel<R, BY, NY, S, GRAD, MINB, UN, SEP>;
     if (!occ && (a.ez != nullptr) != SEP) return cudaErrorInvalidValue;  // layout mismatch
     const size_t smem = sweep3d_smem_bytes(R, cfg, GRAD);
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-    if (occ) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, kern, 32 * (BY + 1), smem);
+    static int resident = 0, sms = 0;  // per instantiation: CTAs per SM at this smem size
+    static size_t resident_smem = 0;
+    if (occ || resident_smem != smem) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        int r = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, kern, 32 * (BY + 1), smem);
+        if (e != cudaSuccess) return e;
+        if (occ) {
+            *occ = r;
+            return cudaSuccess;
+        }
+        int dev = 0;
+        if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+        if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess)
+            return e;
+        resident = r;
+        resident_smem = smem;
+    }
+    if (resident < 1) return cudaErrorInvalidConfiguration;
+    const int nitems = cfg.tiles_x * cfg.tiles_y * cfg.zchunks;
+    const int ctas = cfg.ctas > 0 ? std::min(cfg.ctas, nitems) : std::min(nitems, resident * sms);
     cudaLaunchConfig_t lc{};
-    lc.gridDim = dim3(cfg.tiles_x, cfg.tiles_y, cfg.zchunks);
+    lc.gridDim = dim3(static_cast<unsigned>(ctas));  // persistent: items c, c + ctas, ...
     lc.blockDim = dim3(32, BY + 1);
     lc.dynamicSmemBytes = smem;
     lc.stream = s;
@@ -699,8 +793,8 @@ cudaError_t launch3d_pair_t(const FieldGeom& g, const SweepConfig& cfg, const Sw
     at[0].val.programmaticStreamSerializationAllowed = cfg.pdl ? 1 : 0;
     lc.attrs = at;
     lc.numAttrs = 1;
-    return cudaLaunchKernelEx(&lc, kern, m.uh, m.uc, m.c1, m.c2, m.ut, m.gr, a, g.Px, g.Py,
-                              g.py, g.pz);
+    return cudaLaunchKernelEx(&lc, kern, m.uh, m.uc, m.c1, m.c2, m.ut, m.gr, m.up, a, g.Px, g.Py,
+                              g.py, g.pz, cfg.tiles_x, cfg.tiles_y, nitems);
 }
 
 template <int R, bool GRAD>
