@@ -642,43 +642,52 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
             for (int jj = 0; jj < NY; ++jj) q[jj][slot(R)] = ld2(Cq + cidx + jj * T::TX);
 
             const float* hp = H + (r0 + R) * T::BW + T::RA + 2 * px;  // (row r0, column x)
-            float2 yu[R], yd[R];  // rows r0 - k and r0 + NY - 1 + k
+            const float nez = SEP ? H[T::O_NEZ] : 0.0f;  // -ez[z], staged by the producer
+            // x windows of every row, then the k loop outermost: the y
+            // neighbours outside this thread's rows (yu[m] = row r0 - 1 - m,
+            // yd[m] = row r0 + NY + m) are loaded at k = m + 1 and stay live for
+            // NY iterations only, instead of all 2R of them for the whole plane.
+            float w[NY][2 * WL + 2];
+#pragma unroll
+            for (int jj = 0; jj < NY; ++jj)
+#pragma unroll
+                for (int m = 0; m <= WL; ++m) {
+                    const float2 v = ld2(hp + jj * T::BW - WL + 2 * m);
+                    w[jj][2 * m] = v.x;
+                    w[jj][2 * m + 1] = v.y;
+                }
+            float2 yu[R], yd[R];
+            // Two partial sums (odd / even k) halve the dependent FFMA2 chain.
+            float2 lap[NY], lap2[NY];
+#pragma unroll
+            for (int jj = 0; jj < NY; ++jj) lap[jj] = lap2[jj] = f2(0.0f, 0.0f);
 #pragma unroll
             for (int k = 1; k <= R; ++k) {
                 yu[k - 1] = ld2(hp - k * T::BW);
                 yd[k - 1] = ld2(hp + (NY - 1 + k) * T::BW);
-            }
-            const float nez = SEP ? H[T::O_NEZ] : 0.0f;  // -ez[z], staged by the producer
-
 #pragma unroll
-            for (int jj = 0; jj < NY; ++jj) {
-                float w[2 * WL + 2];
-#pragma unroll
-                for (int m = 0; m <= WL; ++m) {
-                    const float2 v = ld2(hp + jj * T::BW - WL + 2 * m);
-                    w[2 * m] = v.x;
-                    w[2 * m + 1] = v.y;
-                }
-                const float2 c0 = q[jj][slot(0)];
-                // Two partial sums (odd / even k) halve the dependent FFMA2 chain.
-                float2 lap = f2(0.0f, 0.0f), lap2 = f2(0.0f, 0.0f);
-#pragma unroll
-                for (int k = 1; k <= R; ++k) {
+                for (int jj = 0; jj < NY; ++jj) {
+                    const float2 c0 = q[jj][slot(0)];
                     const float2 ym =
                         jj - k >= 0 ? q[(jj - k) >= 0 ? jj - k : 0][slot(0)] : yu[k - jj - 1];
                     const float2 yp =
                         jj + k < NY ? q[(jj + k) < NY ? jj + k : 0][slot(0)] : yd[jj + k - NY];
-                    const float2 xs =
-                        add2(f2(w[WL - k], w[WL - k + 1]), f2(w[WL + k], w[WL + k + 1]));
+                    const float2 xs = add2(f2(w[jj][WL - k], w[jj][WL - k + 1]),
+                                           f2(w[jj][WL + k], w[jj][WL + k + 1]));
                     const float2 zs = add2(q[jj][slot(-k)], q[jj][slot(k)]);
                     float2 sk = add2(add2(xs, add2(ym, yp)), zs);
                     sk = fma2(neg2nd, c0, sk);
                     if (R >= 5 && (k & 1) == 0)
-                        lap2 = fma2(wk[k], sk, lap2);
+                        lap2[jj] = fma2(wk[k], sk, lap2[jj]);
                     else
-                        lap = fma2(wk[k], sk, lap);
+                        lap[jj] = fma2(wk[k], sk, lap[jj]);
                 }
-                if constexpr (R >= 5) lap = add2(lap, lap2);
+            }
+
+#pragma unroll
+            for (int jj = 0; jj < NY; ++jj) {
+                const float2 c0 = q[jj][slot(0)];
+                const float2 lp = R >= 5 ? add2(lap[jj], lap2[jj]) : lap[jj];
                 const int ci = cidx + jj * T::TX;
                 const float2 d = fma2(ld2(U2 + ci), mone, c0);
                 const float2 c2v = ld2(C2 + ci);
@@ -686,7 +695,7 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
                     SEP ? fma2(f2(fminf(nez, nexy[jj].x), fminf(nez, nexy[jj].y)), c2v,
                                f2(1.0f, 1.0f))
                         : ld2(C1 + ci);
-                const float2 inc = fma2(c1v, d, mul2(c2v, lap));
+                const float2 inc = fma2(c1v, d, mul2(c2v, lp));
                 const float2 o = add2(c0, inc);
                 char* pj = cur + jj * rowb;
                 if (vy[jj]) st2(reinterpret_cast<float*>(pj), o);
@@ -804,7 +813,7 @@ cudaError_t launch3d_r(const FieldGeom& g, const SweepConfig& cfg, const SweepMa
     // Pair-mapping variants (by, ny, stages); the register budget (resident
     // CTAs the kernel is compiled for) follows from the z queue, ny (2R+1)
     // float2 per thread.
-    constexpr int MB2 = R <= 4 ? 4 : (R <= 6 ? 3 : 2);  // ny = 2, 4 warps
+    constexpr int MB2 = R <= 4 ? 4 : 3;  // ny = 2, 4 warps
 // BOTH: also compiled for streamed c1 (non-separable damping); the other
 // variants exist for the separable layout only.
 #define SFDB_P(BY, NY, S, MINB, ROTV, BOTH)                                                   \
