@@ -213,6 +213,9 @@ void choose_config(sfdb200_plan& p) {
     }
     if (best < 0) fail(SFDB200_ECUDA, "no sweep variant fits this device");
     pick.pdl = env_int("SFDB200_PDL", 1);
+    // Test knob: cap the persistent grid so every CTA runs many (tile, z chunk)
+    // items (the multi-item path of sweep3d_pair_kernel on small grids).
+    pick.ctas = env_int("SFDB200_CTAS", 0);
     p.cfg = pick;
 }
 
@@ -424,6 +427,7 @@ void autotune(sfdb200_plan& p) {
             c.pair = v.pair;
             c.rot = v.rot;
             c.sep = p.sep_layout;
+            c.ctas = start.ctas;
             c.tiles_y = static_cast<int>((p.g.Py - 2 * R + c.ty() - 1) / c.ty());
             c.smem_bytes = sweep3d_smem_bytes(R, c, p.grad_kind());
             c.zlen = (zupd + zc - 1) / zc;

@@ -60,3 +60,33 @@ def test_gradient_variant(tile):
     go, _ = O.gradient(model.padded, w.space_order, w.h, w.dt, w.nt, model.m, model.damp, u,
                        rec.idx, rec.w, resid)
     assert O.rel_l2(g.grad, go) <= TOL, tile
+
+
+@pytest.mark.parametrize("tile,ctas,zc", [("4,2,4,4,1", 3, 3), ("4,2,4,1,1", 5, 3), ("4,2,4,0,1", 7, 2),
+                                          ("4,2,3,3,1", 2, 3), ("4,2,5,5,1", 4, 2), ("4,2,4,4,1", 1, 1)])
+def test_persistent_multi_item(tile, ctas, zc):
+    """Few persistent CTAs, each walking many (tile, z chunk) items with the
+    TMA ring running across items (skip stages, ring-staged queue prologue,
+    per-item injection): forward and gradient against the oracle."""
+    os.environ["SFDB200_CTAS"] = str(ctas)
+    os.environ["SFDB200_ZCHUNKS"] = str(zc)
+    try:
+        w = configs.cfg2(n=30, nt=62, nbpml=8, nrec_side=7)
+        model = S.make_model(w.interior, w.h, w.nbpml, w.space_order, w.m_interior)
+        src = S.locate_points(model, w.src_coords)
+        rec = S.locate_points(model, w.rec_coords)
+        _forced(tile)
+        f = S.forward(model, src, w.wavelet, rec, w.nt, w.dt, False)
+        u, r = O.forward(model.padded, w.space_order, w.h, w.dt, w.nt, model.m, model.damp,
+                         src.idx, src.w, w.wavelet, rec.idx, rec.w)
+        assert O.rel_l2(f.u, u) <= TOL and O.rel_l2(f.record.data, r) <= TOL
+        us, rs = O.forward(model.padded, w.space_order, w.h, w.dt, w.nt, model.m, model.damp,
+                           src.idx, src.w, w.wavelet, rec.idx, rec.w, save=True)
+        resid = O._f64(np.random.default_rng(3).standard_normal(rs.shape).astype(np.float32))
+        g = S.gradient(model, rec, S.ShotRecord(w.nt, w.dt, rec.npoints, resid), us, w.nt, w.dt)
+        go, _ = O.gradient(model.padded, w.space_order, w.h, w.dt, w.nt, model.m, model.damp, us,
+                           rec.idx, rec.w, resid)
+        assert O.rel_l2(g.grad, go) <= TOL
+    finally:
+        os.environ.pop("SFDB200_CTAS", None)
+        os.environ.pop("SFDB200_ZCHUNKS", None)
