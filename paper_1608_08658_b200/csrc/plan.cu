@@ -512,6 +512,8 @@ void do_upload(sfdb200_plan& p, void** argv) {
             p.hist = nullptr;
             p.hist_rows = rows;
             p.hist = dalloc<float>(static_cast<size_t>(rows * p.g.slot));
+            // halo / pitch cells are read by the sweep but never written
+            ck(cudaMemsetAsync(p.hist, 0, rows * p.g.slot * 4, p.stream), "memset");
             p.own_hist = true;
         }
     }

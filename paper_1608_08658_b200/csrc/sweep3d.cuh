@@ -611,12 +611,16 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
         }
 
         const int x = x0 + 2 * px;
-        bool vy[NY];  // rows inside the allocation (halo cells store 0, see sweep3d_kernel)
+        // Store only the 32-byte sectors that hold updated cells (whole sectors:
+        // a partial one costs L2 a DRAM fill).  The halo / pitch cells left out
+        // are zeroed once and stay zero: their coefficients are zero and no
+        // sparse corner lies there.
+        bool vy[NY];
         float2 nexy[NY];  // SEP: -max(ey[y], ex[x]) of this thread's points (fixed along z)
 #pragma unroll
         for (int jj = 0; jj < NY; ++jj) {
             const int y = y0 + r0 + jj;
-            vy[jj] = y < Py;
+            vy[jj] = y < Py - R && (x & ~7) + 8 > R && (x & ~7) < Px - R;
             const float eyv = SEP && y < Py ? __ldg(a.ey + y) : 0.0f;
             nexy[jj] = f2(-fmaxf(eyv, SEP && x < Px ? __ldg(a.ex + x) : 0.0f),
                           -fmaxf(eyv, SEP && x + 1 < Px ? __ldg(a.ex + x + 1) : 0.0f));
