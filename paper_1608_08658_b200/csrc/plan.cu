@@ -480,6 +480,21 @@ void do_upload(sfdb200_plan& p, void** argv) {
     ck(cudaMemcpyAsync(p.staging + cells, damp + off, cells * 8, cudaMemcpyHostToDevice,
                        p.stream), "H2D damp");
     ck(launch_coeffs(p.g, p.staging, p.staging + cells, d.dt, p.c1, p.c2, p.stream), "coeffs");
+    // Host work while the model is in flight: the sparse sets' data hashes
+    // (the tables are rebuilt only when they change).
+    unsigned long long hsrc = 0, hrec = 0;
+    if (grad) {
+        if (p.rec.n)
+            hrec = sparse_data_hash(p, p.rec.n, static_cast<const long*>(argv[5]),
+                                    static_cast<const double*>(argv[6]), m);
+    } else {
+        if (p.src.n)
+            hsrc = sparse_data_hash(p, p.src.n, static_cast<const long*>(argv[3]),
+                                    static_cast<const double*>(argv[4]), m);
+        if (p.rec.n)
+            hrec = sparse_data_hash(p, p.rec.n, static_cast<const long*>(argv[6]),
+                                    static_cast<const double*>(argv[7]), m);
+    }
     p.sep_damp = false;
     if (p.g.ndim == 3 && env_int("SFDB200_SEPDAMP", 1)) {
         float* ez = p.eprof;
@@ -532,7 +547,7 @@ void do_upload(sfdb200_plan& p, void** argv) {
         upload_trace(p, p.rec, static_cast<const double*>(argv[7]));
         const auto tables = [&] {
             upload_sparse(p, p.rec, static_cast<const long*>(argv[5]),
-                          static_cast<const double*>(argv[6]), m);
+                          static_cast<const double*>(argv[6]), m, hrec);
         };
         tables();
         refine_with_sparse(p, tables);
@@ -542,9 +557,9 @@ void do_upload(sfdb200_plan& p, void** argv) {
         else upload_trace(p, p.rec, static_cast<const double*>(argv[8]));
         const auto tables = [&] {
             upload_sparse(p, p.src, static_cast<const long*>(argv[3]),
-                          static_cast<const double*>(argv[4]), m);
+                          static_cast<const double*>(argv[4]), m, hsrc);
             upload_sparse(p, p.rec, static_cast<const long*>(argv[6]),
-                          static_cast<const double*>(argv[7]), m);
+                          static_cast<const double*>(argv[7]), m, hrec);
         };
         tables();
         refine_with_sparse(p, tables);

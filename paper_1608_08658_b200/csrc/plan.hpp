@@ -229,7 +229,11 @@ namespace sfdb200 {
 // sparse.cpp: host-side sparse tables for one set (corner offsets in the
 // local device layout, ownership by rank, fused per-CTA tables).
 void upload_sparse(sfdb200_plan& p, SparseDev& s, const long* idx, const double* w,
-                   const double* m_global);
+                   const double* m_global, unsigned long long data_hash = 0);
+// Hash of a set's indices, weights and m at its corners (computed on the host
+// while the model's H2D copy is in flight).
+unsigned long long sparse_data_hash(const sfdb200_plan& p, long n, const long* idx,
+                                    const double* w, const double* m_global);
 
 // comm.cpp: NCCL (loaded at run time) for the ghost-plane exchange.
 Comm* comm_create(const void* id128, int world, int rank, int device);

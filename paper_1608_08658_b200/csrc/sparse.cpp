@@ -77,52 +77,63 @@ struct Corner {
 
 namespace {
 
-// Fingerprint of everything the tables depend on: indices, weights, m at the
-// corners (inject coefficients) and the sweep tiling.
-unsigned long long fingerprint(const sfdb200_plan& p, long n, const long* idx, const double* w,
-                               const double* m) {
-    const sfdb200_desc& gd = p.gd;
-    const int nd = gd.ndim, C = 1 << nd;
-    unsigned long long h = 0x9e3779b97f4a7c15ULL;
-    auto mix = [&](unsigned long long v) {
-        h ^= v + 0x9e3779b97f4a7c15ULL + (h << 6) + (h >> 2);
-        h *= 0xff51afd7ed558ccdULL;
-    };
-    auto bits = [](double d) {
-        unsigned long long u;
-        std::memcpy(&u, &d, 8);
-        return u;
-    };
-    mix(static_cast<unsigned long long>(n));
-    mix(static_cast<unsigned long long>(p.cfg.ty()) << 32 ^ static_cast<unsigned>(p.cfg.zlen));
-    mix(static_cast<unsigned long long>(p.cfg.zchunks) << 32 ^ static_cast<unsigned>(p.cfg.tiles_x));
-    mix(bits(gd.dt));
-    for (long i = 0; i < n * nd; ++i) mix(static_cast<unsigned long long>(idx[i]));
-    for (long i = 0; i < n * C; ++i) mix(bits(w[i]));
-    for (long q = 0; q < n; ++q)
-        for (int c = 0; c < C; ++c) {
-            long long dense = 0;
-            for (int k = 0; k < nd; ++k) {
-                const long pos = idx[q * nd + k] + ((c >> (nd - 1 - k)) & 1);
-                if (pos < 0 || pos >= gd.padded[k]) return 0;  // let the builder report it
-                dense = dense * gd.padded[k] + pos;
-            }
-            mix(bits(m[dense]));
-        }
+unsigned long long mix64(unsigned long long h, unsigned long long v) {
+    h ^= v + 0x9e3779b97f4a7c15ULL + (h << 6) + (h >> 2);
+    return h * 0xff51afd7ed558ccdULL;
+}
+
+// Fingerprint of the tables' inputs: the data hash (sparse_data_hash) and
+// the sweep tiling the fused tables depend on.
+unsigned long long fingerprint(const sfdb200_plan& p, unsigned long long data) {
+    if (!data) return 0;
+    unsigned long long h = mix64(data, static_cast<unsigned long long>(p.cfg.ty()) << 32 ^
+                                           static_cast<unsigned>(p.cfg.zlen));
+    h = mix64(h, static_cast<unsigned long long>(p.cfg.zchunks) << 32 ^
+                     static_cast<unsigned>(p.cfg.tiles_x));
     return h | 1ULL;
 }
 
 }  // namespace
 
+// Hash of indices, weights and m at the corners (the inject coefficients);
+// 0 when a corner lies outside the grid (the table builder reports it).
+unsigned long long sparse_data_hash(const sfdb200_plan& p, long n, const long* idx,
+                                    const double* w, const double* m) {
+    const sfdb200_desc& gd = p.gd;
+    const int nd = gd.ndim, C = 1 << nd;
+    unsigned long long h = 0x9e3779b97f4a7c15ULL;
+    auto bits = [](double d) {
+        unsigned long long u;
+        std::memcpy(&u, &d, 8);
+        return u;
+    };
+    h = mix64(h, static_cast<unsigned long long>(n));
+    h = mix64(h, bits(gd.dt));
+    for (long i = 0; i < n * nd; ++i) h = mix64(h, static_cast<unsigned long long>(idx[i]));
+    for (long i = 0; i < n * C; ++i) h = mix64(h, bits(w[i]));
+    for (long q = 0; q < n; ++q)
+        for (int c = 0; c < C; ++c) {
+            long long dense = 0;
+            for (int k = 0; k < nd; ++k) {
+                const long pos = idx[q * nd + k] + ((c >> (nd - 1 - k)) & 1);
+                if (pos < 0 || pos >= gd.padded[k]) return 0;
+                dense = dense * gd.padded[k] + pos;
+            }
+            h = mix64(h, bits(m[dense]));
+        }
+    return h | 1ULL;
+}
+
 void upload_sparse(sfdb200_plan& p, SparseDev& s, const long* idx, const double* w,
-                   const double* m) {
+                   const double* m, unsigned long long data_hash) {
     if (s.n == 0) {
         s.free_tables();
         return;
     }
     // Re-running a plan on the same points (repeated shots, FWI iterations)
     // reuses the device tables.
-    const unsigned long long key = fingerprint(p, s.n, idx, w, m);
+    const unsigned long long key =
+        fingerprint(p, data_hash ? data_hash : sparse_data_hash(p, s.n, idx, w, m));
     if (key && key == s.key) return;
     s.free_tables();
     const sfdb200_desc& gd = p.gd;
