@@ -308,15 +308,6 @@ size_t sweep3d_smem_bytes(int R, const SweepConfig& cfg, bool grad) {
     return static_cast<size_t>(cfg.stages) * SF * 4 + cfg.stages * 16 + 128;
 }
 
-int sweep3d_prologue_planes(int R, const SweepConfig& cfg, bool grad) {
-    const int TY = cfg.ty();
-    const int HF = ((TY + 2 * R) * cfg.bw(R) + 31) & ~31;
-    const int CF = TY * 32;
-    const bool sep = cfg.pair && cfg.sep;
-    const int SF = HF + ((grad ? 6 : 4) - (sep ? 1 : 0)) * CF + (sep ? 32 : 0);
-    return std::min(2 * R, SF / CF);
-}
-
 static cudaError_t dispatch3d(const FieldGeom& g, const SweepConfig& cfg, const SweepMaps& m,
                               const SweepArgs& a, bool grad, cudaStream_t s, int* occ) {
 #define SFDB_R_CASE(RR)                                                   \

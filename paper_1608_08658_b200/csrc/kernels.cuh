@@ -81,7 +81,6 @@ struct SweepMaps {          // TMA descriptors (3-D only)
     CUtensorMap c1, c2;     // coefficient fields, centre box
     CUtensorMap ut;         // GRAD: history rows, centre box
     CUtensorMap gr;         // GRAD: the gradient field, centre box
-    CUtensorMap up;         // u1 rows, prologue box (32, TY, P, 1): pair kernel queue prologue
 };
 
 struct SweepConfig {        // 3-D tiling, chosen by choose_config()
@@ -97,7 +96,8 @@ struct SweepConfig {        // 3-D tiling, chosen by choose_config()
     int pair = 0;           // thread owns column pairs x, x+1 (sweep3d_pair_kernel)
     int sep = 1;            // pair mapping: separable-damping stage layout (no c1 box);
                             // must match SweepArgs::ez != nullptr
-    int ctas = 0;           // pair mapping: persistent CTAs (0 = every resident slot)
+    int ctas = 0;           // pair mapping: 0 = one CTA per (tile, z chunk) item, > 0 = that
+                            // many persistent CTAs, < 0 = one per resident slot
     int tiles_x = 0, tiles_y = 0;
     size_t smem_bytes = 0;
     int ty() const { return 2 * by * ny; }
@@ -105,8 +105,7 @@ struct SweepConfig {        // 3-D tiling, chosen by choose_config()
 };
 
 size_t sweep3d_smem_bytes(int R, const SweepConfig& cfg, bool grad);
-// Planes per prologue box of the pair kernel (sweep3d.cuh Tile::PRO_P).
-int sweep3d_prologue_planes(int R, const SweepConfig& cfg, bool grad);
+
 cudaError_t launch_sweep3d(const FieldGeom& g, const SweepConfig& cfg, const SweepMaps& maps,
                            const SweepArgs& a, bool grad, cudaStream_t s);
 // Per-radius instantiations (sweep3d_r<R>.cu); occ != nullptr queries the

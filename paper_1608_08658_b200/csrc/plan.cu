@@ -99,14 +99,14 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 // 4-D fp32 tensor map over [rows][z][y][x] (x pitched), zero OOB fill.
 CUtensorMap make_map(const float* base, const FieldGeom& g, long long rows, unsigned box_x,
-                     unsigned box_y, unsigned box_z = 1) {
+                     unsigned box_y) {
     CUtensorMap m;
     const cuuint64_t dims[4] = {static_cast<cuuint64_t>(g.Px), static_cast<cuuint64_t>(g.Py),
                                 static_cast<cuuint64_t>(g.Pz), static_cast<cuuint64_t>(rows)};
     const cuuint64_t strides[3] = {static_cast<cuuint64_t>(g.py) * 4,
                                    static_cast<cuuint64_t>(g.pz) * 4,
                                    static_cast<cuuint64_t>(g.slot) * 4};
-    const cuuint32_t box[4] = {box_x, box_y, box_z, 1};
+    const cuuint32_t box[4] = {box_x, box_y, 1, 1};
     const cuuint32_t estr[4] = {1, 1, 1, 1};
     const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
                                    const_cast<float*>(base), dims, strides, box, estr,
@@ -225,8 +225,6 @@ void build_maps(sfdb200_plan& p) {
     const unsigned TY = static_cast<unsigned>(p.cfg.ty());
     p.maps.uh = make_map(p.field, p.g, p.rows, static_cast<unsigned>(p.cfg.bw(R)), TY + 2 * R);
     p.maps.uc = make_map(p.field, p.g, p.rows, 32, TY);
-    p.maps.up = make_map(p.field, p.g, p.rows, 32, TY,
-                         static_cast<unsigned>(sweep3d_prologue_planes(R, p.cfg, p.grad_kind())));
     p.maps.c1 = make_map(p.c1, p.g, 1, 32, TY);
     p.maps.c2 = make_map(p.c2, p.g, 1, 32, TY);
     if (p.grad_kind() && p.hist) p.maps.ut = make_map(p.hist, p.g, p.hist_rows, 32, TY);
@@ -1024,8 +1022,6 @@ void do_execute_checkpointed(sfdb200_plan& p) {
     seg.uh = make_map(p.hist, p.g, p.hist_rows, static_cast<unsigned>(fp.cfg.bw(p.g.R)),
                       TY + 2 * p.g.R);
     seg.uc = make_map(p.hist, p.g, p.hist_rows, 32, TY);
-    seg.up = make_map(p.hist, p.g, p.hist_rows, 32, TY,
-                      static_cast<unsigned>(sweep3d_prologue_planes(p.g.R, fp.cfg, false)));
     seg.ut = seg.uc;
     seg.gr = seg.uc;
     exec_begin(p);

@@ -117,11 +117,6 @@ struct Tile {
     // Bytes the TMA boxes of one stage deliver (the mbarrier transaction count).
     static constexpr uint32_t BYTES = static_cast<uint32_t>((TY + 2 * R) * BW + NC * CF) * 4u;
     static constexpr int Q = 2 * R + 1;                        // z-queue length
-    // Pair kernel prologue: the 2R queue planes below a z chunk arrive as
-    // PRO_S boxes of PRO_P centre planes, each within one stage.
-    static constexpr int PRO_P = 2 * R < SF / CF ? 2 * R : SF / CF;
-    static constexpr int PRO_S = (2 * R + PRO_P - 1) / PRO_P;
-    static constexpr uint32_t PRO_BYTES = static_cast<uint32_t>(PRO_P * CF) * 4u;
 };
 
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
@@ -446,16 +441,16 @@ __device__ __forceinline__ void st2(float* p, float2 v) { *reinterpret_cast<floa
 template <int R, int ROTV>
 constexpr int z_unroll() { return ROTV == 1 ? 2 * R + 1 : (ROTV == 0 ? 1 : ROTV); }
 
-// Persistent CTAs: the launch has min(items, resident slots) CTAs and CTA c
-// runs items c, c + gridDim.x, ... (item = x tile fastest, then y tile, then
-// z chunk: the hardware's own CTA order, so tiles still sweep z in step and
-// halos stay in L2).  The producer streams the next item's planes while the
-// consumers finish the current one, so the ring never drains between items,
-// and the 2R queue planes below an item's first plane arrive through the
-// ring too, as PS boxes of P planes (the prologue), instead of synchronous
-// loads.  With UN a multiple of S each item's first plane is aligned to stage
-// 0 by empty "skip" stages, so every unrolled plane phase has a fixed stage
-// and compile-time shared-memory offsets.
+// Items: CTA c runs the (x tile, y tile, z chunk) items c, c + gridDim.x, ...
+// (item = x tile fastest, then y tile, then z chunk: the hardware's own CTA
+// order, so tiles sweep z in step and halos stay in L2).  By default the grid
+// has one CTA per item; with fewer (persistent) CTAs the producer streams the
+// next item's planes while the consumers finish the current one, so the ring
+// never drains between items (measured: on cfg2 no faster than the hardware
+// handing items to free slots, and slower whenever items per CTA are not
+// integral, so it is a tuning / test option).  With UN a multiple of S each
+// item's first plane is aligned to stage 0 by empty "skip" stages, so every
+// unrolled plane phase has a fixed stage and compile-time shared-memory offsets.
 template <int R, int BY, int NY, int S, bool GRAD, int MINB, int UN, bool SEP>
 __global__ void __launch_bounds__(32 * (BY + 1), MINB)
     sweep3d_pair_kernel(const __grid_constant__ CUtensorMap tm_uh,
@@ -464,14 +459,12 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
                         const __grid_constant__ CUtensorMap tm_c2,
                         const __grid_constant__ CUtensorMap tm_ut,
                         const __grid_constant__ CUtensorMap tm_gr,
-                        const __grid_constant__ CUtensorMap tm_up,
                         const __grid_constant__ SweepArgs a, const int Px, const int Py,
                         const long long py, const long long pz, const int ntx, const int nty,
                         const int nitems) {
     using T = Tile<R, BY, NY, GRAD, SEP>;
     constexpr int Q = T::Q;
     constexpr int WL = (R + 1) & ~1;  // x window [x - WL, x + 1 + WL], 8-byte aligned
-    constexpr int P = T::PRO_P, PS = T::PRO_S;
     constexpr bool SST = UN % S == 0;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     float* smem = reinterpret_cast<float*>(smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u));
@@ -516,17 +509,10 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
                 const int n = ze - zb;
                 if (n <= 0) continue;
                 if constexpr (SST) {
-                    while ((j + PS) % S != 0) {  // skip stage: completes on the arrive alone
+                    while (j % S != 0) {  // skip stage: completes on the arrive alone
                         mbar_arrive(&full[acquire()]);
                         ++j;
                     }
-                }
-                for (int s = 0; s < PS; ++s) {
-                    const int st = acquire();
-                    mbar_arrive_expect_tx(&full[st], T::PRO_BYTES);
-                    tma_load_4d(smem + st * T::SF, &tm_up, x0, y0, zb - R + s * P, a.row_u1,
-                                &full[st]);
-                    ++j;
                 }
                 const float* ezp = SEP ? a.ez + zb : nullptr;
                 float nxt = 0.0f;
@@ -584,7 +570,7 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
         const int n = ze - zb;
         if (n <= 0) continue;
         if constexpr (SST) {
-            while ((j + PS) % S != 0) {
+            while (j % S != 0) {
                 const int st = static_cast<int>(j % S);
                 mbar_wait(&full[st], (j / S) & 1);
                 __syncwarp();
@@ -592,25 +578,21 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
                 ++j;
             }
         }
-        // Queue slot of plane zb - R + t is t (t < 2R): the prologue boxes.
+        const int x = x0 + 2 * px;
+        // Queue slot of plane zb - R + t is t (t < 2R): loaded directly (the
+        // loads overlap the producer filling the ring with the item's first
+        // planes; staging them through the ring instead delays those planes).
         float2 q[NY][QS];
 #pragma unroll
-        for (int s = 0; s < PS; ++s) {
-            const int st = static_cast<int>(j % S);
-            mbar_wait(&full[st], (j / S) & 1);
-            const float* B = smem + st * T::SF + cidx;
+        for (int jj = 0; jj < NY; ++jj) {
+            const int y = y0 + r0 + jj;
+            const float* c = a.u1 + static_cast<long long>(y) * py + x;
 #pragma unroll
-            for (int t = 0; t < P; ++t)
-                if (s * P + t < 2 * R)
-#pragma unroll
-                    for (int jj = 0; jj < NY; ++jj)
-                        q[jj][s * P + t] = ld2(B + t * T::CF + jj * T::TX);
-            __syncwarp();
-            if (lx == 0) mbar_arrive(&empty[st]);
-            ++j;
+            for (int t = 0; t < 2 * R; ++t) {
+                const long long o = static_cast<long long>(zb - R + t) * pz;
+                q[jj][t] = y < Py ? __ldg(reinterpret_cast<const float2*>(c + o)) : f2(0.0f, 0.0f);
+            }
         }
-
-        const int x = x0 + 2 * px;
         // Store only the 32-byte sectors that hold updated cells (whole sectors:
         // a partial one costs L2 a DRAM fill).  The halo / pitch cells left out
         // are zeroed once and stay zero: their coefficients are zero and no
@@ -795,9 +777,13 @@ cudaError_t launch3d_pair_t(const FieldGeom& g, const SweepConfig& cfg, const Sw
     }
     if (resident < 1) return cudaErrorInvalidConfiguration;
     const int nitems = cfg.tiles_x * cfg.tiles_y * cfg.zchunks;
-    const int ctas = cfg.ctas > 0 ? std::min(cfg.ctas, nitems) : std::min(nitems, resident * sms);
+    // cfg.ctas: 0 = one CTA per item (the hardware hands items to free slots
+    // dynamically), > 0 = that many persistent CTAs, < 0 = one per resident slot.
+    const int ctas = cfg.ctas > 0   ? std::min(cfg.ctas, nitems)
+                     : cfg.ctas < 0 ? std::min(nitems, resident * sms)
+                                    : nitems;
     cudaLaunchConfig_t lc{};
-    lc.gridDim = dim3(static_cast<unsigned>(ctas));  // persistent: items c, c + ctas, ...
+    lc.gridDim = dim3(static_cast<unsigned>(ctas));  // CTA c: items c, c + ctas, ...
     lc.blockDim = dim3(32, BY + 1);
     lc.dynamicSmemBytes = smem;
     lc.stream = s;
@@ -806,7 +792,7 @@ cudaError_t launch3d_pair_t(const FieldGeom& g, const SweepConfig& cfg, const Sw
     at[0].val.programmaticStreamSerializationAllowed = cfg.pdl ? 1 : 0;
     lc.attrs = at;
     lc.numAttrs = 1;
-    return cudaLaunchKernelEx(&lc, kern, m.uh, m.uc, m.c1, m.c2, m.ut, m.gr, m.up, a, g.Px, g.Py,
+    return cudaLaunchKernelEx(&lc, kern, m.uh, m.uc, m.c1, m.c2, m.ut, m.gr, a, g.Px, g.Py,
                               g.py, g.pz, cfg.tiles_x, cfg.tiles_y, nitems);
 }
 
