@@ -47,6 +47,10 @@ struct SweepArgs {
     float* grad;            // GRAD
     int row_out, row_u1, row_u2, row_ut;  // row coordinates for the tensor maps
     int zlo, zhi, zchunk;   // updated z range and planes per CTA
+    // Bit k set: z chunk k streams downward (pair kernel; sweep3d.cuh
+    // zdown_mask), so that chunks sharing a boundary read its planes at the
+    // same time and the queue prologue hits L2.
+    unsigned long long zdown;
     float w[kMaxRadius + 1];  // w_k / h^2
     float neg2nd;           // -2 * ndim
     float nidt2;            // -1 / dt^2

@@ -474,14 +474,18 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
 
     const int lx = threadIdx.x;
     const int tid = threadIdx.y * 32 + lx;
-    // item -> tile origin (x0, y0) and z range [zb, ze)
-    auto decode = [&](int item, int& x0, int& y0, int& zb, int& ze) {
+    // item -> tile origin (x0, y0), z range [zb, ze) and direction: planes
+    // z0, z0 + dz, ... (dz = -1: the chunk streams downward, a.zdown)
+    auto decode = [&](int item, int& x0, int& y0, int& zb, int& ze, int& z0, int& dz) {
         const int r = item / ntx;
         x0 = (item - r * ntx) * T::TX;
         const int tz = r / nty;
         y0 = R + (r - tz * nty) * T::TY;
         zb = a.zlo + tz * a.zchunk;
         ze = min(zb + a.zchunk, a.zhi);
+        const bool dn = tz < 64 && ((a.zdown >> tz) & 1ull);
+        z0 = dn ? ze - 1 : zb;
+        dz = dn ? -1 : 1;
     };
 
     pdl_trigger();
@@ -504,8 +508,8 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
                 return st;
             };
             for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
-                int x0, y0, zb, ze;
-                decode(item, x0, y0, zb, ze);
+                int x0, y0, zb, ze, z0, dz;
+                decode(item, x0, y0, zb, ze, z0, dz);
                 const int n = ze - zb;
                 if (n <= 0) continue;
                 if constexpr (SST) {
@@ -514,24 +518,24 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
                         ++j;
                     }
                 }
-                const float* ezp = SEP ? a.ez + zb : nullptr;
+                const float* ezp = SEP ? a.ez + z0 : nullptr;
                 float nxt = 0.0f;
                 if constexpr (SEP) nxt = -__ldg(ezp);
 #pragma unroll 1
                 for (int i = 0; i < n; ++i) {
                     const float cur = nxt;
                     if constexpr (SEP)
-                        if (i + 1 < n) nxt = -__ldg(ezp + i + 1);
+                        if (i + 1 < n) nxt = -__ldg(ezp + dz * (i + 1));
                     const int st = acquire();
                     float* sb = smem + st * T::SF;
                     uint64_t* bar = &full[st];
-                    const int z = zb + i;
+                    const int z = z0 + dz * i;
                     // SEP: -ez[z] rides in the stage, ordered before the consumers'
                     // acquire by the release of this arrive.
                     if constexpr (SEP) sb[T::O_NEZ] = cur;
                     mbar_arrive_expect_tx(bar, T::BYTES);
                     tma_load_4d(sb, &tm_uh, x0 - T::RA, y0 - R, z, a.row_u1, bar);
-                    tma_load_4d(sb + T::O_U1C, &tm_uc, x0, y0, z + R, a.row_u1, bar);
+                    tma_load_4d(sb + T::O_U1C, &tm_uc, x0, y0, z + dz * R, a.row_u1, bar);
                     tma_load_4d(sb + T::O_U2, &tm_uc, x0, y0, z, a.row_u2, bar);
                     if constexpr (!SEP) tma_load_4d(sb + T::O_C1, &tm_c1, x0, y0, z, 0, bar);
                     tma_load_4d(sb + T::O_C2, &tm_c2, x0, y0, z, 0, bar);
@@ -565,8 +569,8 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
     uint32_t j = 0;  // stage sequence number, as the producer's
 
     for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
-        int x0, y0, zb, ze;
-        decode(item, x0, y0, zb, ze);
+        int x0, y0, zb, ze, z0, dz;
+        decode(item, x0, y0, zb, ze, z0, dz);
         const int n = ze - zb;
         if (n <= 0) continue;
         if constexpr (SST) {
@@ -579,9 +583,11 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
             }
         }
         const int x = x0 + 2 * px;
-        // Queue slot of plane zb - R + t is t (t < 2R): loaded directly (the
-        // loads overlap the producer filling the ring with the item's first
-        // planes; staging them through the ring instead delays those planes).
+        // Queue slot of plane z0 + dz (t - R) is t (t < 2R), loaded directly
+        // (the loads overlap the producer filling the ring with the item's
+        // first planes; staging them through the ring delays those planes).
+        // Streaming down mirrors the queue; the per-k sums q[-k] + q[+k] are
+        // commutative, so both directions give the same bits.
         float2 q[NY][QS];
 #pragma unroll
         for (int jj = 0; jj < NY; ++jj) {
@@ -589,7 +595,7 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
             const float* c = a.u1 + static_cast<long long>(y) * py + x;
 #pragma unroll
             for (int t = 0; t < 2 * R; ++t) {
-                const long long o = static_cast<long long>(zb - R + t) * pz;
+                const long long o = static_cast<long long>(z0 + dz * (t - R)) * pz;
                 q[jj][t] = y < Py ? __ldg(reinterpret_cast<const float2*>(c + o)) : f2(0.0f, 0.0f);
             }
         }
@@ -607,8 +613,9 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
             nexy[jj] = f2(-fmaxf(eyv, SEP && x < Px ? __ldg(a.ex + x) : 0.0f),
                           -fmaxf(eyv, SEP && x + 1 < Px ? __ldg(a.ex + x + 1) : 0.0f));
         }
-        char* cur = reinterpret_cast<char*>(a.out + static_cast<long long>(zb) * pz +
+        char* cur = reinterpret_cast<char*>(a.out + static_cast<long long>(z0) * pz +
                                             static_cast<long long>(y0 + r0) * py + x);
+        const long long stepb = dz * planeb;
 
         int stage = static_cast<int>(j % S);  // 0 with SST
         uint32_t phase = (j / S) & 1;
@@ -692,7 +699,7 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
                         st2(reinterpret_cast<float*>(pj + gdiff), fma2(coef, vtt, ld2(GR + ci)));
                 }
             }
-            cur += planeb;
+            cur += stepb;
 
             __syncwarp();
             if (lx == 0) mbar_arrive(&empty[st]);
@@ -723,6 +730,36 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
             inject_cta<GRAD, NT>(a, item, tid);
         }
     }
+}
+
+// Directions of the z chunks (SweepArgs::zdown) for a launch of `tiles` x
+// `zchunks` items, item = tile + tiles * chunk, `slots` resident at a time.
+// A chunk runs in wave (middle item) / slots.  The boundary between chunks k
+// and k+1 is read once from DRAM when the two read its planes at the same
+// time: same wave and both start there (k down, k+1 up) or both end there
+// (k up, k+1 down); k one wave before k+1 and both up (k ends where k+1
+// starts); k one wave after k+1 and both down.  Exhaustive over <= 12 chunks.
+inline unsigned long long zdown_mask(int tiles, int zchunks, long long slots) {
+    if (zchunks < 2 || zchunks > 12 || slots < 1) return 0;
+    int wave[12];
+    for (int k = 0; k < zchunks; ++k)
+        wave[k] = static_cast<int>((static_cast<long long>(tiles) * k + tiles / 2) / slots);
+    int best = -1;
+    unsigned long long pick = 0;
+    for (unsigned long long m = 0; m < (1ull << zchunks); ++m) {
+        int ok = 0;
+        for (int k = 0; k + 1 < zchunks; ++k) {
+            const bool dk = (m >> k) & 1, dn = (m >> (k + 1)) & 1;
+            if (wave[k] == wave[k + 1]) ok += dk != dn;
+            else if (wave[k] + 1 == wave[k + 1]) ok += !dk && !dn;
+            else if (wave[k] == wave[k + 1] + 1) ok += dk && dn;
+        }
+        if (ok > best) {
+            best = ok;
+            pick = m;
+        }
+    }
+    return pick;
 }
 
 // occ != nullptr: report resident CTAs per SM instead of launching.
@@ -792,7 +829,10 @@ cudaError_t launch3d_pair_t(const FieldGeom& g, const SweepConfig& cfg, const Sw
     at[0].val.programmaticStreamSerializationAllowed = cfg.pdl ? 1 : 0;
     lc.attrs = at;
     lc.numAttrs = 1;
-    return cudaLaunchKernelEx(&lc, kern, m.uh, m.uc, m.c1, m.c2, m.ut, m.gr, a, g.Px, g.Py,
+    SweepArgs b = a;
+    b.zdown = zdown_mask(cfg.tiles_x * cfg.tiles_y, cfg.zchunks,
+                         ctas < nitems ? ctas : static_cast<long long>(resident) * sms);
+    return cudaLaunchKernelEx(&lc, kern, m.uh, m.uc, m.c1, m.c2, m.ut, m.gr, b, g.Px, g.Py,
                               g.py, g.pz, cfg.tiles_x, cfg.tiles_y, nitems);
 }
 
