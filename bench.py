@@ -203,10 +203,21 @@ def cpu_baseline(w, steps_hint):
 
 
 def run_reference(args):
+    """The reference's own CPU path on this host (rank 0 only under torchrun),
+    on our arm's workload: at N > 1 with weak scaling that is the cfg2 model
+    stacked N times along z (the global problem the N ranks share)."""
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
-    w = make_workload(args.workload, args.time_steps)
+    if world > 1 and args.workload == "cfg2" and args.scaling == "weak":
+        from paper_1608_08658_b200 import configs
+        w = configs.cfg2_stacked(world)
+        if args.time_steps:
+            w.nt = args.time_steps + 2
+        w.wavelet = np.ascontiguousarray(w.wavelet[:w.nt].reshape(w.nt, -1))
+    else:
+        w = make_workload(args.workload, args.time_steps)
     vals = []
     cb = None
     for i in range(args.warmup + args.steps):
@@ -219,7 +230,9 @@ def run_reference(args):
             "unit": "Gpts/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": cb["seconds"] * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": config_of(w, 1, {"sample": cb["sample"]}), "cpu_baseline": cb,
+            "config": config_of(w, world, {"sample": cb["sample"],
+                                           "parallelism": f"reference CPU path, {cb['cores']} host threads"}),
+            "cpu_baseline": cb,
             "e2e": {"value": v, "unit": "Gpts/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
