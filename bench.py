@@ -443,7 +443,13 @@ def run_fwi(args):
         g.bind_checkpoints(fwd)  # history recomputed per segment (one extra forward sweep/step)
     else:
         g.bind_history(fwd)
-    gargv = [None, None, bg.m, bg.damp, grad, rec.idx, rec.w, resid]
+    # pinned host buffers for everything the e2e leg moves (model, residual, gradient)
+    def pinned_copy(a):
+        t = torch.empty(a.shape, dtype=torch.float64, pin_memory=True).numpy()
+        t[...] = a
+        return t
+    gargv = [None, None, pinned_copy(bg.m), pinned_copy(bg.damp), pinned_copy(grad),
+             L.i64(rec.idx), L.f64(rec.w), pinned_copy(resid)]
     g.upload(gargv)
     for _ in range(args.warmup):
         g.execute()
