@@ -101,7 +101,7 @@ def config_of(w, n, extra=None):
          "padded": w.padded, "space_order": w.space_order, "time_steps": w.steps,
          "points_per_step": w.points_per_step, "nsrc": len(w.src_coords),
          "nrec": len(w.rec_coords),
-         "parallelism": f"z-slab x{n} (NCCL ghost exchange overlapped with the interior sweep)"
+         "parallelism": f"z-slab x{n} (ghost planes exchanged every step, overlapped with the interior sweep)"
                         if n > 1 else "1 GPU",
          "l2": "inputs larger than L2 (each fp32 field 4*prod(padded) B > 126 MB)"
                if 4 * int(np.prod(w.padded)) > 126e6 else "working set fits L2"}
@@ -265,7 +265,8 @@ def run_ours(args):
     comm = None
     if world > 1:
         # torch.distributed is the plumbing (rendezvous, barriers, the max over
-        # ranks); the ghost exchange runs on libsfdb200's own NCCL communicator.
+        # ranks); the ghost exchange is libsfdb200's own (fused P2P stores, or its
+        # NCCL communicator as the fallback).
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         uid = [L.Comm.unique_id() if rank == 0 else None]
@@ -288,6 +289,31 @@ def run_ours(args):
                   rec.npoints, False, local, comm=comm)
     stream = torch.cuda.Stream()
     plan.set_stream(stream.cuda_stream)
+    exchange = None
+    if world > 1:
+        # Fused P2P ghost exchange (default): the boundary sweeps store into the
+        # neighbours' ghost planes over NVLink; NCCL send/recv otherwise.
+        exchange = "nccl send/recv on a comm stream, overlapped with the interior sweep"
+        if os.environ.get("SFDB200_EXCHANGE", "p2p") == "p2p":
+            blobs = [None] * world
+            dist.all_gather_object(blobs, plan.ipc_export())
+            try:
+                plan.ipc_import(blobs[rank - 1] if rank > 0 else None,
+                                blobs[rank + 1] if rank < world - 1 else None)
+                ok = 1
+            except L.SfdError as e:
+                print(f"rank {rank}: P2P exchange unavailable ({e}); using NCCL", file=sys.stderr)
+                ok = 0
+            flag = torch.tensor([ok], device="cuda")
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            if int(flag.item()) == 1:
+                exchange = ("fused P2P: boundary sweeps store into the neighbours' ghost planes "
+                            "(CUDA IPC over NVLink), step counters via stream memory ops")
+            else:  # every rank must use the same exchange
+                plan.close()
+                plan = L.Plan(L.FORWARD, nd, model.padded, w.space_order, w.nt, w.dt, w.h,
+                              src.npoints, rec.npoints, False, local, comm=comm)
+                plan.set_stream(stream.cuda_stream)
 
     # Pinned host buffers in the reference's layout (fp64 grids, long idx).
     def pinned(shape, dtype):
@@ -388,7 +414,8 @@ def run_ours(args):
                 "ms_per_step": ms / args.steps, "higher_is_better": True,
                 "scaling": "strong" if (world > 1 and args.scaling == "strong") else "weak",
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "config": config_of(w, world, {"sweep": plan.info()}), "roofline": roof, "cpu_baseline": cb,
+                "config": config_of(w, world, {"sweep": plan.info(), "exchange": exchange}),
+                "roofline": roof, "cpu_baseline": cb,
                 "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary}
         print(json.dumps(line))
     plan.close()

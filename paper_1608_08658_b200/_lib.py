@@ -63,6 +63,10 @@ _SIGS = {
     "sfdb200_comm_destroy": (_i, [_P]),
     "sfdb200_comm_create_loopback": (_i, [_i, _i, _i, _P]),
     "sfdb200_execute_group": (_i, [_P, _i]),
+    "sfdb200_plan_ipc_export": (_i, [_P, _P]),
+    "sfdb200_plan_ipc_import": (_i, [_P, _P, _P]),
+    "sfdb200_plan_peer_group": (_i, [_P, _i]),
+    "sfdb200_p2p_selftest": (_i, [_i]),
     "sfdb200_plan_create_dist": (_i, [_P, _P, _P]),
     "sfdb200_slab": (_i, [_L, _i, _i, _i, _lp, _lp]),
     "sfdb200_plan_slab": (_i, [_P, _lp, _lp, _lp]),
@@ -225,6 +229,19 @@ class Plan:
     def d2h_bytes(self):
         return lib().sfdb200_d2h_bytes(self.handle)
 
+    def ipc_export(self) -> bytes:
+        """This rank's blob for the fused P2P ghost exchange (sfdb200_plan_ipc_export)."""
+        buf = C.create_string_buffer(IPC_BYTES)
+        check(lib().sfdb200_plan_ipc_export(self.handle, buf))
+        return buf.raw
+
+    def ipc_import(self, lower, upper):
+        """Open the neighbours' blobs (None at a slab end) and switch to the P2P
+        exchange; raises InvalidArgument (plan keeps NCCL) without peer access."""
+        lo = C.create_string_buffer(bytes(lower), IPC_BYTES) if lower is not None else None
+        hi = C.create_string_buffer(bytes(upper), IPC_BYTES) if upper is not None else None
+        check(lib().sfdb200_plan_ipc_import(self.handle, lo, hi))
+
 
 class Comm:
     """sfdb200_comm: the z-slab ranks' NCCL communicator (one per GPU process)."""
@@ -254,6 +271,16 @@ class Comm:
         if self.handle:
             lib().sfdb200_comm_destroy(self.handle)
             self.handle = None
+
+
+IPC_BYTES = 256  # SFDB200_IPC_BYTES
+
+
+def peer_group(plans):
+    """Loopback harness: the emulated ranks store into each other's ghost
+    planes from their boundary sweeps (the fused P2P exchange on one GPU)."""
+    arr = (C.c_void_p * len(plans))(*[p.handle.value for p in plans])
+    check(lib().sfdb200_plan_peer_group(arr, len(plans)))
 
 
 def execute_group(plans):

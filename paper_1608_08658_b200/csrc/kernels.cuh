@@ -77,6 +77,10 @@ struct SweepArgs {
     const int* inj_pt;
     const unsigned char* inj_gm;  // GRAD: corner inside the updated region
     const float* inj_row;         // trace row of this step
+    // Fused P2P ghost exchange (p2p.cpp): non-zero in the boundary launches,
+    // every stored value is also stored at byte offset peer_delta (the
+    // neighbour's ghost copy of the plane, through its IPC mapping).
+    long long peer_delta;
 };
 
 struct SweepMaps {          // TMA descriptors (3-D only)
@@ -226,6 +230,10 @@ int loop2d_blocks_per_sm(int R, bool grad);
 cudaError_t launch_inject(float* field, const long long* off, const float* coef, const int* pt,
                           const float* row, long n, float* grad, const float* ut,
                           const unsigned char* gmask, float nidt2, cudaStream_t s);
+// P2P mirrors: field[off[i]] copied to (side[i] ? hi : lo)[off[i]] (the
+// neighbours' ghost copies of injected corners in the sent planes).
+cudaError_t launch_mirror(const float* field, const long long* off, const unsigned char* side,
+                          long n, float* lo, float* hi, cudaStream_t s);
 // pt (optional): output index of each sampled point (a subset of the set).
 cudaError_t launch_sample(const float* field, const long long* off, const float* w,
                           const int* pt, float* row, long npoints, int corners, cudaStream_t s);

@@ -1,0 +1,191 @@
+// Fused P2P ghost exchange between z-slab ranks over NVLink.
+//
+// The NCCL path (comm.cpp) sweeps the R planes next to each neighbour, then
+// sends them with ncclSend/ncclRecv while the interior runs.  Here the two
+// boundary sweeps store every plane twice: into this rank's row and, through a
+// CUDA IPC mapping of the neighbour's field, straight into the neighbour's
+// ghost planes of the same row (sweep3d.cuh, SweepArgs::peer_delta), so the
+// transfer happens inside the sweep, tile by tile.  Injections that land in
+// the sent planes are mirrored by a tiny copy after them.  Ordering between
+// the two processes uses one 32-bit step counter per direction in the
+// receiver's memory, written with cuStreamWriteValue32 after the boundary work
+// of a step (the write is fenced behind the earlier peer stores) and waited on
+// with cuStreamWaitValue32 (GEQ) before the receiver's next step:
+//
+//   exec_begin:  zero rows -> signal B (ready) -> wait neighbours >= B
+//   step i:      wait >= B + i -> boundary sweeps (+ peer stores) ->
+//                inject (+ mirrors) -> signal B + i + 1 -> interior sweep
+//   exec_end:    wait >= B + steps        (their last stores into my ghosts)
+//
+// B advances by steps + 1 per execute on every rank, so counters never reset.
+// A neighbour can be at most one step ahead, and then writes the ghost planes
+// of a row this rank no longer reads (row t % 3 while this rank reads row
+// (t - 2) % 3 ghosts), so there is no write-after-read hazard.
+#include <cuda.h>
+
+#include <cstdint>
+#include <cstring>
+#include <string>
+
+#include "plan.hpp"
+
+namespace sfdb200 {
+namespace {
+
+struct Blob {  // SFDB200_IPC_BYTES, plain bytes exchanged by the caller
+    cudaIpcMemHandle_t field;
+    cudaIpcMemHandle_t flags;
+    int device;
+    int pz;
+    long long slot;
+    int rank, world;
+};
+static_assert(sizeof(Blob) <= SFDB200_IPC_BYTES, "IPC blob too large");
+
+typedef CUresult (*PFN_wait32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+typedef CUresult (*PFN_write32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+
+template <class F>
+F driver_fn(const char* name) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !p)
+        fail(SFDB200_ECUDA, std::string(name) + " is unavailable");
+    return reinterpret_cast<F>(p);
+}
+
+}  // namespace
+
+long long p2p_delta(const sfdb200_plan& p, int side, long long row) {
+    const FieldGeom& g = p.g;
+    const int R = g.R;
+    // lower: my planes [R, 2R) -> its planes [Pz' - R, Pz'); upper: my planes
+    // [Pz - 2R, Pz - R) -> its planes [0, R)
+    const long long dplanes = side == 0 ? p.peer_pz[0] - 2LL * R : -(g.Pz - 2LL * R);
+    const auto mine = reinterpret_cast<std::uintptr_t>(p.field + row * g.slot);
+    const auto theirs = reinterpret_cast<std::uintptr_t>(p.peer_field[side] + row * p.peer_slot[side]) +
+                        static_cast<std::uintptr_t>(dplanes * g.pz * 4);
+    return static_cast<long long>(theirs - mine);
+}
+
+float* p2p_mirror_base(const sfdb200_plan& p, int side, long long row) {
+    const long long d = p2p_delta(p, side, row);
+    return reinterpret_cast<float*>(reinterpret_cast<std::uintptr_t>(p.field + row * p.g.slot) +
+                                    static_cast<std::uintptr_t>(d));
+}
+
+void p2p_export(const sfdb200_plan& p, void* out) {
+    if (!p.dist() || p.g.ndim != 3) fail(SFDB200_EINVAL, "P2P exchange needs a 3-D z-slab plan");
+    Blob b{};
+    ck(cudaIpcGetMemHandle(&b.field, p.field), "cudaIpcGetMemHandle");
+    ck(cudaIpcGetMemHandle(&b.flags, p.flags), "cudaIpcGetMemHandle");
+    b.device = p.d.device;
+    b.pz = p.g.Pz;
+    b.slot = p.g.slot;
+    b.rank = p.rank;
+    b.world = p.world;
+    std::memset(out, 0, SFDB200_IPC_BYTES);
+    std::memcpy(out, &b, sizeof b);
+}
+
+void p2p_import(sfdb200_plan& p, const void* lower, const void* upper) {
+    if (!p.dist() || p.g.ndim != 3) fail(SFDB200_EINVAL, "P2P exchange needs a 3-D z-slab plan");
+    const void* blobs[2] = {lower, upper};
+    const int want[2] = {p.rank - 1, p.rank + 1};
+    Blob b[2]{};
+    for (int side = 0; side < 2; ++side) {
+        const bool has = side == 0 ? p.rank > 0 : p.rank < p.world - 1;
+        if (has != (blobs[side] != nullptr))
+            fail(SFDB200_EINVAL, "P2P import: neighbour blob missing or unexpected");
+        if (!has) continue;
+        std::memcpy(&b[side], blobs[side], sizeof(Blob));
+        if (b[side].rank != want[side] || b[side].world != p.world)
+            fail(SFDB200_EINVAL, "P2P import: blob is not the neighbour's");
+        int can = 0;
+        ck(cudaDeviceCanAccessPeer(&can, p.d.device, b[side].device), "cudaDeviceCanAccessPeer");
+        if (!can) fail(SFDB200_EINVAL, "P2P import: neighbour device is not peer-accessible");
+    }
+    p2p_release(p);
+    for (int side = 0; side < 2; ++side) {
+        if (!blobs[side]) continue;
+        void* f = nullptr;
+        void* fl = nullptr;
+        ck(cudaIpcOpenMemHandle(&f, b[side].field, cudaIpcMemLazyEnablePeerAccess),
+           "cudaIpcOpenMemHandle");
+        ck(cudaIpcOpenMemHandle(&fl, b[side].flags, cudaIpcMemLazyEnablePeerAccess),
+           "cudaIpcOpenMemHandle");
+        p.peer_field[side] = static_cast<float*>(f);
+        p.peer_flags[side] = static_cast<unsigned int*>(fl);
+        p.peer_slot[side] = b[side].slot;
+        p.peer_pz[side] = b[side].pz;
+        p.peer_ipc[side] = true;
+    }
+    p.p2p = true;
+    p.p2p_sync = true;
+}
+
+void p2p_release(sfdb200_plan& p) {
+    for (int side = 0; side < 2; ++side) {
+        if (p.peer_ipc[side]) {
+            cudaIpcCloseMemHandle(p.peer_field[side]);
+            cudaIpcCloseMemHandle(p.peer_flags[side]);
+        }
+        p.peer_ipc[side] = false;
+        p.peer_field[side] = nullptr;
+        p.peer_flags[side] = nullptr;
+    }
+    p.p2p = false;
+    p.p2p_sync = false;
+}
+
+// I am the upper neighbour of side 0 (it reads its counter [1]) and the lower
+// neighbour of side 1 (its counter [0]).
+void p2p_signal(sfdb200_plan& p, unsigned int value, cudaStream_t s) {
+    static PFN_write32 write32 = driver_fn<PFN_write32>("cuStreamWriteValue32");
+    for (int side = 0; side < 2; ++side) {
+        if (!p.peer_flags[side]) continue;
+        unsigned int* dst = p.peer_flags[side] + (side == 0 ? 1 : 0);
+        const CUresult r = write32(reinterpret_cast<CUstream>(s),
+                                   reinterpret_cast<CUdeviceptr>(dst), value, 0);
+        if (r != CUDA_SUCCESS)
+            fail(SFDB200_ECUDA, "cuStreamWriteValue32 failed (" + std::to_string(r) + ")");
+    }
+}
+
+void p2p_wait(sfdb200_plan& p, unsigned int value, cudaStream_t s) {
+    static PFN_wait32 wait32 = driver_fn<PFN_wait32>("cuStreamWaitValue32");
+    for (int side = 0; side < 2; ++side) {
+        if (!p.peer_flags[side]) continue;
+        // counter written by the neighbour on `side`
+        const CUresult r = wait32(reinterpret_cast<CUstream>(s),
+                                  reinterpret_cast<CUdeviceptr>(p.flags + side), value,
+                                  CU_STREAM_WAIT_VALUE_GEQ);
+        if (r != CUDA_SUCCESS)
+            fail(SFDB200_ECUDA, "cuStreamWaitValue32 failed (" + std::to_string(r) + ")");
+    }
+}
+
+void p2p_selftest(int device) {
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    sfdb200_plan p;  // a bare plan: its own counters stand in for a neighbour's
+    p.flags = dalloc<unsigned int>(64);
+    cudaStream_t s;
+    ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
+    ck(cudaMemsetAsync(p.flags, 0, 64 * sizeof(unsigned int), s), "memset");
+    p.peer_flags[0] = p.flags;  // I am side 0's upper neighbour: I write its [1] ...
+    p.peer_flags[1] = p.flags;  // ... and side 1's lower neighbour: its [0]
+    for (unsigned int v = 1; v <= 3; ++v) {
+        p2p_signal(p, v, s);
+        p2p_wait(p, v, s);
+    }
+    unsigned int h[2] = {0, 0};
+    ck(cudaMemcpyAsync(h, p.flags, sizeof h, cudaMemcpyDeviceToHost, s), "D2H");
+    const cudaError_t e = cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+    p.peer_flags[0] = p.peer_flags[1] = nullptr;
+    ck(e, "stream counters");
+    if (h[0] != 3 || h[1] != 3) fail(SFDB200_ECUDA, "stream counters: unexpected values");
+}
+
+}  // namespace sfdb200

@@ -41,6 +41,8 @@ int env_int(const char* name, int dflt) {
 }  // namespace sfdb200
 
 sfdb200_plan::~sfdb200_plan() {
+    p2p_release(*this);
+    cudaFree(flags);
     cudaFree(field);
     cudaFree(c1);
     cudaFree(c2);
@@ -302,6 +304,10 @@ void create(const sfdb200_desc& gd, Comm* comm, sfdb200_plan& p) {
     if (p.grad_kind()) p.grad = dalloc<float>(static_cast<size_t>(g.slot));
     p.counter = dalloc<unsigned long long>(1);
     p.flag = dalloc<unsigned int>(1);
+    if (p.dist() && g.ndim == 3) {  // P2P step counters (p2p.cpp), written by the neighbours
+        p.flags = dalloc<unsigned int>(64);
+        ck(cudaMemsetAsync(p.flags, 0, 64 * sizeof(unsigned int), p.stream), "memset");
+    }
     if (g.ndim == 3) {
         const size_t n = static_cast<size_t>(g.Pz + g.Py + g.Px);
         p.eprof = dalloc<float>(n);
@@ -670,10 +676,21 @@ void phase_boundary(sfdb200_plan& p, StepState& st) {
         b.zlo = side == 0 ? R : g.Pz - 2 * R;
         b.zhi = b.zlo + R;
         b.zchunk = R;
+        // P2P: the sweep also stores these planes into the neighbour's ghost planes
+        if (p.p2p) b.peer_delta = p2p_delta(p, side, st.a.row_out);
         ck(launch_sweep3d(g, bcfg, p.maps, b, p.grad_kind(), p.stream), "sweep3d (boundary)");
         ++p.launches;
     }
     launch_rest_inject(p, st);
+    SparseDev& inj = p.injected();
+    if (p.p2p && inj.mir_n) {  // injected corners in the sent planes
+        ck(launch_mirror(st.a.out, inj.mir_off, inj.mir_side, inj.mir_n,
+                         p.peer_field[0] ? p2p_mirror_base(p, 0, st.a.row_out) : nullptr,
+                         p.peer_field[1] ? p2p_mirror_base(p, 1, st.a.row_out) : nullptr,
+                         p.stream),
+           "mirror");
+        ++p.launches;
+    }
 }
 
 void phase_interior(sfdb200_plan& p, long i, StepState& st) {
@@ -1069,9 +1086,21 @@ void do_execute(sfdb200_plan& p) {
         return;
     }
     StepState st;
+    // P2P exchange (p2p.cpp): every rank zeroed its rows before any neighbour
+    // stores into them; step i starts once the neighbours' step i-1 planes
+    // are in place.
+    const unsigned int B = p.flag_base;
+    if (p.p2p_sync) {
+        p2p_signal(p, B, p.stream);
+        p2p_wait(p, B, p.stream);
+    }
     for (long i = 0; i < p.steps(); ++i) {
         step_setup(p, i, st);
-        if (p.dist()) {
+        if (p.dist() && p.p2p) {
+            if (p.p2p_sync) p2p_wait(p, B + static_cast<unsigned int>(i), p.stream);
+            phase_boundary(p, st);  // boundary sweeps store into the neighbours too
+            if (p.p2p_sync) p2p_signal(p, B + static_cast<unsigned int>(i) + 1, p.stream);
+        } else if (p.dist()) {
             phase_boundary(p, st);
             ck(cudaEventRecord(p.ev_b, p.stream), "event");
             ck(cudaStreamWaitEvent(p.cstream, p.ev_b, 0), "wait");
@@ -1079,11 +1108,15 @@ void do_execute(sfdb200_plan& p) {
             ck(cudaEventRecord(p.ev_x, p.cstream), "event");
         }
         phase_interior(p, i, st);
-        if (p.dist()) ck(cudaStreamWaitEvent(p.stream, p.ev_x, 0), "wait");
+        if (p.dist() && !p.p2p) ck(cudaStreamWaitEvent(p.stream, p.ev_x, 0), "wait");
         phase_samples(p, st);
         // forward: rows < t are final once step t's sweep sampled row t-1
         if (stream_out && i % 64 == 63) flush_rows(p, 2 + i);
         take_checkpoint(p, 2 + i);
+    }
+    if (p.p2p_sync) {  // the neighbours' last stores into my ghost planes
+        p2p_wait(p, B + static_cast<unsigned int>(p.steps()), p.stream);
+        p.flag_base = B + static_cast<unsigned int>(p.steps()) + 1;
     }
     exec_end(p, st);
     p.ck_valid = p.ck_interval > 0;
@@ -1107,7 +1140,9 @@ void do_execute_group(sfdb200_plan** plans, int n) {
             step_setup(*plans[r], i, st[r]);
             phase_boundary(*plans[r], st[r]);
         }
-        for (int r = 0; r + 1 < n; ++r) {  // ghost planes between ranks r and r+1
+        // ghost planes between ranks r and r+1 (P2P peer group: already stored
+        // by the boundary sweeps)
+        for (int r = 0; r + 1 < n && !plans[0]->p2p; ++r) {
             sfdb200_plan& a = *plans[r];
             sfdb200_plan& b = *plans[r + 1];
             const int R = a.g.R;
@@ -1428,6 +1463,50 @@ int sfdb200_execute_group(sfdb200_plan** plans, int n) {
         ck(cudaSetDevice(plans[0]->d.device), "cudaSetDevice");
         do_execute_group(plans, n);
     });
+}
+
+int sfdb200_plan_ipc_export(const sfdb200_plan* p, void* out) {
+    return guarded([&] {
+        if (!p || !out) fail(SFDB200_EINVAL, "null argument");
+        ck(cudaSetDevice(p->d.device), "cudaSetDevice");
+        p2p_export(*p, out);
+    });
+}
+
+int sfdb200_plan_ipc_import(sfdb200_plan* p, const void* lower, const void* upper) {
+    return guarded([&] {
+        if (!p) fail(SFDB200_EINVAL, "null argument");
+        ck(cudaSetDevice(p->d.device), "cudaSetDevice");
+        p2p_import(*p, lower, upper);
+    });
+}
+
+int sfdb200_plan_peer_group(sfdb200_plan** plans, int n) {
+    return guarded([&] {
+        if (!plans || n < 2) fail(SFDB200_EINVAL, "a peer group needs at least two plans");
+        for (int r = 0; r < n; ++r) {
+            sfdb200_plan& p = *plans[r];
+            if (p.world != n || p.rank != r || !comm_loopback(p.comm) || p.g.ndim != 3)
+                fail(SFDB200_EINVAL, "peer group plans must be 3-D loopback ranks 0..n-1");
+        }
+        for (int r = 0; r < n; ++r) {
+            sfdb200_plan& p = *plans[r];
+            p2p_release(p);
+            for (int side = 0; side < 2; ++side) {
+                const int q = side == 0 ? r - 1 : r + 1;
+                if (q < 0 || q >= n) continue;
+                p.peer_field[side] = plans[q]->field;
+                p.peer_slot[side] = plans[q]->g.slot;
+                p.peer_pz[side] = plans[q]->g.Pz;
+            }
+            p.p2p = true;
+            p.p2p_sync = false;  // execute_group's lockstep phases order the steps
+        }
+    });
+}
+
+int sfdb200_p2p_selftest(int device) {
+    return guarded([&] { p2p_selftest(device); });
 }
 
 int sfdb200_comm_destroy(sfdb200_comm* comm) {

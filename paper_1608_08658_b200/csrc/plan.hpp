@@ -69,6 +69,11 @@ struct SparseDev {
     int* f_pt = nullptr;
     unsigned char* f_gm = nullptr;
     InjectList inj_rest;
+    // P2P exchange: rest corners inside the planes sent to a neighbour
+    // (side 0 lower, 1 upper), mirrored after the injection (launch_mirror).
+    long mir_n = 0;
+    long long* mir_off = nullptr;
+    unsigned char* mir_side = nullptr;
     // Sampling: every owned receiver (smp_all).  In the fused 3-D sweep the
     // previous row is sampled at the start of the next interior launch
     // (s_base = corner-0 offsets, weights and columns shared with smp_all);
@@ -103,6 +108,9 @@ struct SparseDev {
         f_tab = nullptr; f_off = nullptr; f_coef = nullptr; f_pt = nullptr; f_gm = nullptr;
         s_base = nullptr;
         inj_rest = InjectList{};
+        mir_n = 0;
+        mir_off = nullptr;
+        mir_side = nullptr;
         smp_all = SampleList{};
         k_n = 0;
         k_max = 0;
@@ -146,6 +154,17 @@ struct sfdb200_plan {
     sfdb200::Comm* comm = nullptr;
     cudaStream_t cstream = nullptr;
     cudaEvent_t ev_b = nullptr, ev_x = nullptr;
+    // Fused P2P ghost exchange (p2p.cpp): the boundary sweeps store into the
+    // neighbours' ghost planes; side 0 = lower neighbour (rank - 1), 1 = upper.
+    bool p2p = false;
+    bool p2p_sync = false;              // step counters (separate processes); off in loopback
+    float* peer_field[2] = {nullptr, nullptr};
+    long long peer_slot[2] = {0, 0};    // elements per row of the neighbour's field
+    int peer_pz[2] = {0, 0};            // the neighbour's local plane count
+    bool peer_ipc[2] = {false, false};  // peer_field / peer_flags opened through IPC
+    unsigned int* flags = nullptr;      // my inbound step counters [2] (written by the neighbours)
+    unsigned int* peer_flags[2] = {nullptr, nullptr};
+    unsigned int flag_base = 1;         // epoch base, advanced identically on every rank
 
     float* field = nullptr;  // u (forward) / v (adjoint, gradient), `rows` rows
     float* c1 = nullptr;
@@ -234,6 +253,19 @@ void upload_sparse(sfdb200_plan& p, SparseDev& s, const long* idx, const double*
 // while the model's H2D copy is in flight).
 unsigned long long sparse_data_hash(const sfdb200_plan& p, long n, const long* idx,
                                     const double* w, const double* m_global);
+
+// p2p.cpp: fused P2P ghost exchange.
+// Byte offset from my `row` of plane zl to the neighbour's ghost copy of it.
+long long p2p_delta(const sfdb200_plan& p, int side, long long row);
+// The neighbour's address of my local element offset 0 in `row` (mirrors).
+float* p2p_mirror_base(const sfdb200_plan& p, int side, long long row);
+void p2p_export(const sfdb200_plan& p, void* out);
+void p2p_import(sfdb200_plan& p, const void* lower, const void* upper);
+void p2p_release(sfdb200_plan& p);
+// Stream memory operations on the step counters.
+void p2p_signal(sfdb200_plan& p, unsigned int value, cudaStream_t s);
+void p2p_wait(sfdb200_plan& p, unsigned int value, cudaStream_t s);
+void p2p_selftest(int device);
 
 // comm.cpp: NCCL (loaded at run time) for the ghost-plane exchange.
 Comm* comm_create(const void* id128, int world, int rank, int device);

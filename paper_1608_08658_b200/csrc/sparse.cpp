@@ -250,6 +250,24 @@ void upload_sparse(sfdb200_plan& p, SparseDev& s, const long* idx, const double*
             r_pt.push_back(static_cast<int>(i / C));
             r_gm.push_back(k.updated ? 1 : 0);
         }
+        // Corners of the rest list inside the planes the boundary sweeps send to
+        // a neighbour: the P2P exchange mirrors them after the injection.
+        std::vector<long long> m_off;
+        std::vector<unsigned char> m_side;
+        if (p.dist())
+            for (const long long o : r_off) {
+                const long zl = static_cast<long>(o / g.pz);
+                if (p.rank > 0 && zl >= R && zl < 2 * R) {
+                    m_off.push_back(o);
+                    m_side.push_back(0);
+                } else if (p.rank < p.world - 1 && zl >= g.Pz - 2 * R && zl < g.Pz - R) {
+                    m_off.push_back(o);
+                    m_side.push_back(1);
+                }
+            }
+        s.mir_n = static_cast<long>(m_off.size());
+        s.mir_off = s.upload(m_off, st);
+        s.mir_side = s.upload(m_side, st);
         s.inj_rest.n = static_cast<long>(r_off.size());
         s.inj_rest.off = s.upload(r_off, st);
         s.inj_rest.coef = s.upload(r_coef, st);

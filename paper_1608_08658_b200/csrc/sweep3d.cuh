@@ -377,6 +377,10 @@ __global__ void __launch_bounds__(32 * (BY + 1), 4)
             char* pb = pa + halfb;
             if (va[j]) *reinterpret_cast<float*>(pa) = o.x;
             if (vb[j]) *reinterpret_cast<float*>(pb) = o.y;
+            if (a.peer_delta) {  // fused P2P ghost exchange (boundary launches)
+                if (va[j]) *reinterpret_cast<float*>(pa + a.peer_delta) = o.x;
+                if (vb[j]) *reinterpret_cast<float*>(pb + a.peer_delta) = o.y;
+            }
             if constexpr (GRAD) {
                 // grad += -(1/dt^2) u_t (v_t - 2 v_{t+1} + v_{t+2}) = nidt2 * u_t * (inc - d)
                 const float2 vtt = fma2(d, mone, inc);
@@ -691,7 +695,10 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
                 const float2 inc = fma2(c1v, d, mul2(c2v, lp));
                 const float2 o = add2(c0, inc);
                 char* pj = cur + jj * rowb;
-                if (vy[jj]) st2(reinterpret_cast<float*>(pj), o);
+                if (vy[jj]) {
+                    st2(reinterpret_cast<float*>(pj), o);
+                    if (a.peer_delta) st2(reinterpret_cast<float*>(pj + a.peer_delta), o);
+                }
                 if constexpr (GRAD) {
                     const float2 vtt = fma2(d, mone, inc);
                     const float2 coef = mul2(nidt2, ld2(UT + ci));

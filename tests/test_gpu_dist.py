@@ -34,7 +34,7 @@ def _problem(so=8):
     return w, model, src, rec, wav
 
 
-def _run_group(kind, w, model, src, rec, wav, world, resid=None):
+def _run_group(kind, w, model, src, rec, wav, world, resid=None, p2p=False):
     import torch
     stream = torch.cuda.Stream()
     comms = [L.Comm.loopback(world, r, 0) for r in range(world)]
@@ -50,9 +50,12 @@ def _run_group(kind, w, model, src, rec, wav, world, resid=None):
         else:
             tr = np.zeros((w.nt, src.npoints))
             argv = [field, model.m, model.damp, src.idx, src.w, tr, rec.idx, rec.w, resid]
-        p.upload(argv)
         plans.append(p)
         outs.append((argv, field, tr))
+    if p2p:  # fused P2P exchange: boundary sweeps store into the neighbours' rows
+        L.peer_group(plans)
+    for p, (argv, _, _) in zip(plans, outs):
+        p.upload(argv)
     L.execute_group(plans)
     field = np.zeros((3, *model.padded))
     trace = 0
@@ -67,11 +70,11 @@ def _run_group(kind, w, model, src, rec, wav, world, resid=None):
     return field, trace
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_emulated_ranks_forward_matches_single_gpu(world):
+@pytest.mark.parametrize("world,p2p", [(2, False), (3, False), (2, True), (3, True)])
+def test_emulated_ranks_forward_matches_single_gpu(world, p2p):
     w, model, src, rec, wav = _problem()
     ref = S.forward(model, src, wav, rec, w.nt, w.dt, False)
-    u, tr = _run_group(L.FORWARD, w, model, src, rec, wav, world)
+    u, tr = _run_group(L.FORWARD, w, model, src, rec, wav, world, p2p=p2p)
     assert O.rel_l2(u, ref.u) <= 1e-6
     assert O.rel_l2(tr, ref.record.data) <= 1e-6
     uo, ro = O.forward(model.padded, w.space_order, w.h, w.dt, w.nt, model.m, model.damp,
@@ -79,12 +82,13 @@ def test_emulated_ranks_forward_matches_single_gpu(world):
     assert O.rel_l2(u, uo) <= 1e-5 and O.rel_l2(tr, ro) <= 1e-5
 
 
-def test_emulated_ranks_adjoint_so16():
+@pytest.mark.parametrize("p2p", [False, True])
+def test_emulated_ranks_adjoint_so16(p2p):
     w, model, src, rec, wav = _problem(so=16)
     rng = np.random.default_rng(2)
     resid = O._f64(rng.standard_normal((w.nt, rec.npoints)).astype(np.float32))
     ref = S.adjoint(model, rec, S.ShotRecord(w.nt, w.dt, rec.npoints, resid), src, w.nt, w.dt)
-    v, tr = _run_group(L.ADJOINT, w, model, src, rec, wav, 3, resid)
+    v, tr = _run_group(L.ADJOINT, w, model, src, rec, wav, 3, resid, p2p=p2p)
     assert O.rel_l2(v, ref.v) <= 1e-6
     assert O.rel_l2(tr, ref.src_samples.data) <= 1e-6
 
@@ -122,3 +126,52 @@ def test_nccl_communicator_single_rank():
         assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
     finally:
         dist.destroy_process_group()
+
+
+def test_p2p_injection_in_sent_planes():
+    """Sources whose corners lie in the planes the boundary sweeps send: the
+    fused P2P exchange must mirror the injected values into the neighbour's
+    ghost copy (launch_mirror); equal to the single-GPU run."""
+    w, model, src, rec, wav = _problem()
+    R = w.space_order // 2
+    pts = []
+    span = (model.interior[0] - 1) * w.h
+    for world in (2, 3):
+        for r in range(1, world):  # the boundary between ranks r-1 and r
+            zb, _ = L.slab(model.padded[0], w.space_order, world, r)
+            # rank r's first R planes (sent down) and rank r-1's last R (sent up)
+            for z in (zb, zb + R - 1, zb - R, zb - 1):
+                zc = (z - model.pad()) * w.h + 2.5
+                if 0.0 <= zc <= span:
+                    pts.append([zc, 100.0, 120.0])
+    src = S.locate_points(model, np.array(pts))
+    wav = O._f64(np.repeat(w.wavelet[:, :1], len(pts), axis=1))
+    ref = S.forward(model, src, wav, rec, w.nt, w.dt, False)
+    for world in (2, 3):
+        u, tr = _run_group(L.FORWARD, w, model, src, rec, wav, world, p2p=True)
+        assert O.rel_l2(u, ref.u) <= 1e-6 and O.rel_l2(tr, ref.record.data) <= 1e-6, world
+
+
+def test_ipc_export_blob():
+    """A dist plan exports its IPC blob (field + step counters); importing a
+    blob that is not the neighbour's is refused (the plan keeps NCCL)."""
+    w, model, src, rec, wav = _problem()
+    comms = [L.Comm.loopback(2, r, 0) for r in range(2)]
+    plans = [L.Plan(L.FORWARD, 3, model.padded, w.space_order, w.nt, w.dt, w.h, src.npoints,
+                    rec.npoints, False, 0, comm=c) for c in comms]
+    try:
+        blobs = [p.ipc_export() for p in plans]
+        assert all(len(b) == L.IPC_BYTES and any(b) for b in blobs)
+        with pytest.raises(L.InvalidArgument):
+            plans[0].ipc_import(None, blobs[0])  # its own blob, not rank 1's
+    finally:
+        for p in plans:
+            p.close()
+        for c in comms:
+            c.close()
+
+
+def test_p2p_step_counters():
+    """cuStreamWriteValue32 / cuStreamWaitValue32 as the P2P exchange uses them
+    (resolved through the driver entry points), on one device."""
+    L.check(L.lib().sfdb200_p2p_selftest(0))
