@@ -382,6 +382,19 @@ def run_ours(args):
                "h2d_bytes_per_step": plan.h2d_bytes, "d2h_bytes_per_step": plan.d2h_bytes,
                "ms_per_step": el / args.steps * 1e3,
                "path": "sfdb200_run(plan, argv): reference argv, pinned fp64 host buffers"}
+        if world == 1:
+            # The same call with pageable host arrays, as the reference's
+            # std::vector buffers are (staged through the plan's pinned chunks).
+            pargv = [np.empty_like(u), np.array(m), np.array(damp), L.i64(src.idx),
+                     L.f64(src.w), np.array(trace), L.i64(rec.idx), L.f64(rec.w),
+                     np.empty_like(rec_data)]
+            plan.run(pargv)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            plan.run(pargv)
+            elp = time.perf_counter() - t0
+            e2e["pageable"] = {"value": pts / elp / 1e9, "ms_per_step": elp * 1e3,
+                               "path": "sfdb200_run with pageable numpy buffers (one run)"}
 
     peak, peak_src = measured_peak()
     per_launch_ms = sweep_ms / max(1, sweep_n)

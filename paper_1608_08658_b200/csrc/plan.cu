@@ -41,6 +41,7 @@ int env_int(const char* name, int dflt) {
 }  // namespace sfdb200
 
 sfdb200_plan::~sfdb200_plan() {
+    release_pinned(*this);
     p2p_release(*this);
     cudaFree(flags);
     cudaFree(field);
@@ -342,7 +343,7 @@ void upload_trace(sfdb200_plan& p, SparseDev& s, const double* data) {
     const long long n = p.d.nt * s.n;
     if (n == 0) return;
     p.ensure_staging(static_cast<size_t>(n));
-    ck(cudaMemcpyAsync(p.staging, data, n * 8, cudaMemcpyHostToDevice, p.stream), "H2D");
+    copy_h2d(p, p.staging, data, static_cast<size_t>(n) * 8);
     ck(launch_dense_to_f32(p.staging, s.trace, n, p.stream), "convert");
     p.h2d += n * 8;
 }
@@ -352,7 +353,7 @@ void download_trace(sfdb200_plan& p, SparseDev& s, double* out) {
     if (n == 0) return;
     p.ensure_staging(static_cast<size_t>(n));
     ck(launch_dense_to_f64(s.trace, p.staging, n, p.stream), "convert");
-    ck(cudaMemcpyAsync(out, p.staging, n * 8, cudaMemcpyDeviceToHost, p.stream), "D2H");
+    copy_d2h(p, out, p.staging, static_cast<size_t>(n) * 8);
     ck(cudaStreamSynchronize(p.stream), "D2H");
     p.d2h += n * 8;
 }
@@ -363,8 +364,7 @@ void upload_rows(sfdb200_plan& p, const double* src, float* dst, long long rows)
     const long long gcells = pc * p.gd.padded[0];
     p.ensure_staging(static_cast<size_t>(cells));
     for (long long r = 0; r < rows; ++r) {
-        ck(cudaMemcpyAsync(p.staging, src + r * gcells + p.zoff * pc, cells * 8,
-                           cudaMemcpyHostToDevice, p.stream), "H2D");
+        copy_h2d(p, p.staging, src + r * gcells + p.zoff * pc, static_cast<size_t>(cells) * 8);
         ck(launch_to_f32(p.g, p.staging, dst + r * p.g.slot, 1, p.stream), "convert");
         p.h2d += cells * 8;
     }
@@ -379,8 +379,8 @@ void download_rows(sfdb200_plan& p, const float* src, double* dst, long long row
     p.ensure_staging(static_cast<size_t>(cells));
     for (long long r = 0; r < rows; ++r) {
         ck(launch_to_f64(p.g, src + r * p.g.slot, p.staging, 1, p.stream), "convert");
-        ck(cudaMemcpyAsync(dst + r * gcells + (p.zoff + lo) * pc, p.staging + lo * pc,
-                           (hi - lo) * pc * 8, cudaMemcpyDeviceToHost, p.stream), "D2H");
+        copy_d2h(p, dst + r * gcells + (p.zoff + lo) * pc, p.staging + lo * pc,
+                 static_cast<size_t>((hi - lo) * pc) * 8);
         ck(cudaStreamSynchronize(p.stream), "D2H");
         p.d2h += (hi - lo) * pc * 8;
     }
@@ -480,9 +480,8 @@ void do_upload(sfdb200_plan& p, void** argv) {
     const long long off = p.zoff * p.plane_cells();
     p.h2d = 0;
     p.ensure_staging(static_cast<size_t>(2 * cells));
-    ck(cudaMemcpyAsync(p.staging, m + off, cells * 8, cudaMemcpyHostToDevice, p.stream), "H2D m");
-    ck(cudaMemcpyAsync(p.staging + cells, damp + off, cells * 8, cudaMemcpyHostToDevice,
-                       p.stream), "H2D damp");
+    copy_h2d(p, p.staging, m + off, static_cast<size_t>(cells) * 8);
+    copy_h2d(p, p.staging + cells, damp + off, static_cast<size_t>(cells) * 8);
     ck(launch_coeffs(p.g, p.staging, p.staging + cells, d.dt, p.c1, p.c2, p.stream), "coeffs");
     // Host work while the model is in flight: the sparse sets' data hashes
     // (the tables are rebuilt only when they change).
@@ -1075,8 +1074,10 @@ void do_execute(sfdb200_plan& p) {
     if (p.ck_interval) prepare_checkpoints(p);
     exec_begin(p);
     p.flushed = 0;
+    // (a pageable record is filled at download through the pinned staging
+    // instead: synchronous pageable copies mid-run would stall the launches)
     const bool stream_out = p.host_rec && p.g.ndim == 3 && p.d.kind == SFDB200_FORWARD &&
-                            p.fused && !p.dist() && p.rec.n;
+                            p.fused && !p.dist() && p.rec.n && host_pinned(p.host_rec);
     if (stream_out && !p.xstream) {
         ck(cudaStreamCreateWithFlags(&p.xstream, cudaStreamNonBlocking), "cudaStreamCreate");
         ck(cudaEventCreateWithFlags(&p.ev_flush, cudaEventDisableTiming), "cudaEventCreate");

@@ -189,6 +189,9 @@ struct sfdb200_plan {
     sfdb200::SparseDev src, rec;
     double* staging = nullptr;
     size_t staging_elems = 0;
+    // hostio.cpp: two pinned chunks staging copies of pageable caller buffers
+    void* pin[2] = {nullptr, nullptr};
+    cudaEvent_t pin_ev[2] = {nullptr, nullptr};
     unsigned long long* counter = nullptr;
     unsigned int* flag = nullptr;
 
@@ -253,6 +256,15 @@ void upload_sparse(sfdb200_plan& p, SparseDev& s, const long* idx, const double*
 // while the model's H2D copy is in flight).
 unsigned long long sparse_data_hash(const sfdb200_plan& p, long n, const long* idx,
                                     const double* w, const double* m_global);
+
+// hostio.cpp: copies of the caller's host buffers (pageable ones staged
+// through pinned chunks filled / drained by host threads).  copy_h2d returns
+// once src may be reused (the DMA may still run); copy_d2h returns with the
+// data in dst when dst is pageable, asynchronously (on p.stream) when pinned.
+bool host_pinned(const void* ptr);
+void copy_h2d(sfdb200_plan& p, void* dst, const void* src, size_t bytes);
+void copy_d2h(sfdb200_plan& p, void* dst, const void* src, size_t bytes);
+void release_pinned(sfdb200_plan& p);
 
 // p2p.cpp: fused P2P ghost exchange.
 // Byte offset from my `row` of plane zl to the neighbour's ghost copy of it.
