@@ -1,7 +1,8 @@
 // Host-side preparation of the sparse operators (source injection, receiver
 // sampling) for one plan: corner offsets in the device layout, ownership by
-// z-slab rank, and the per-(CTA, plane) tables that let the 3-D sweep apply
-// them inside its own launch.
+// z-slab rank, and the per-CTA tables that let the 3-D sweep apply them inside
+// its own launch (injections after the CTA's planes, samples of the previous
+// row at the CTA's start), plus the P2P mirror list.
 //
 // Reference semantics: codegen.cpp:419-462 (corner bit order: bit ndim-1-d of
 // c -> +1 along dim d; inject w * scale * data / m[corner]; sample
