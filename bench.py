@@ -30,11 +30,17 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-# The reference's JIT'd kernels use OpenMP: all host threads, bound close.
+# The reference's JIT'd kernels use OpenMP: all host threads, bound close
+# (set just before the reference first runs, bind_reference_threads(): an
+# OpenMP runtime started earlier with binding would pin this process's main
+# thread, and the helper threads it spawns, to one core).
 os.environ.setdefault("STENCILFD_THREADS", str(os.cpu_count() or 1))
-os.environ.setdefault("OMP_PROC_BIND", "close")
-os.environ.setdefault("OMP_PLACES", "cores")
 os.environ.setdefault("STENCILFD_CACHE_DIR", "/tmp/stencilfd-cache")
+
+
+def bind_reference_threads():
+    os.environ.setdefault("OMP_PROC_BIND", "close")
+    os.environ.setdefault("OMP_PLACES", "cores")
 
 import numpy as np  # noqa: E402
 
@@ -179,6 +185,7 @@ def cpu_baseline(w, steps_hint):
     truncated step count.  Falls back to the C port when _ref was not built."""
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     import oracle_lib as O
+    bind_reference_threads()
     cores = int(os.environ["STENCILFD_THREADS"])
     steps = steps_hint or max(4, min(40, int(2.0e9 / w.points_per_step)))
     nt = steps + 2
@@ -533,6 +540,7 @@ def run_fwi(args):
     if not args.no_cpu:
         sys.path.insert(0, os.path.join(ROOT, "tests"))
         import oracle_lib as O
+        bind_reference_threads()
         if O.have_ref():
             steps = args.cpu_steps or 20
             ntc = steps + 2

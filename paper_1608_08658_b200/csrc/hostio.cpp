@@ -6,7 +6,12 @@
 // on cfg2: 10.7 GB/s up, 21 GB/s down).  Here it is staged through two pinned
 // chunks per plan: a few host threads fill (or drain) one chunk while the DMA
 // of the other runs, so the copy runs near the PCIe rate instead.
+#include <pthread.h>
+#include <sched.h>
+#include <unistd.h>
+
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <thread>
 #include <vector>
@@ -19,9 +24,31 @@ namespace {
 constexpr size_t kChunk = 32u << 20;  // bytes per pinned staging chunk
 
 // memcpy split over a few host threads (one for small copies).
+unsigned copy_threads() {
+    static const unsigned t = [] {
+        if (const char* e = std::getenv("SFDB200_COPY_THREADS")) return std::max(1, std::atoi(e));
+        return static_cast<int>(std::min(8u, std::max(1u, std::thread::hardware_concurrency() / 2)));
+    }();
+    return t;
+}
+
+// Helper threads inherit the caller's CPU binding (an OpenMP runtime started
+// with OMP_PROC_BIND pins the initial thread to one core, e.g. under bench.py
+// or the reference's own OpenMP kernels), which would put every helper on that
+// core; they widen their own mask to every CPU id (the kernel intersects it
+// with the process's cpuset, whose ids need not start at 0).
+void unbind_self() {
+    const long n = std::max<long>(1024, sysconf(_SC_NPROCESSORS_CONF));
+    cpu_set_t* set = CPU_ALLOC(n);
+    const size_t sz = CPU_ALLOC_SIZE(n);
+    CPU_ZERO_S(sz, set);
+    for (long c = 0; c < n; ++c) CPU_SET_S(c, sz, set);
+    pthread_setaffinity_np(pthread_self(), sz, set);
+    CPU_FREE(set);
+}
+
 void par_memcpy(void* dst, const void* src, size_t n) {
-    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-    const size_t t = std::min<size_t>({8, std::max(1u, hw / 2), std::max<size_t>(1, n >> 22)});
+    const size_t t = std::min<size_t>(copy_threads(), std::max<size_t>(1, n >> 22));
     if (t <= 1) {
         std::memcpy(dst, src, n);
         return;
@@ -32,6 +59,7 @@ void par_memcpy(void* dst, const void* src, size_t n) {
         const size_t o = i * per;
         if (o >= n) break;
         th.emplace_back([=] {
+            unbind_self();
             std::memcpy(static_cast<char*>(dst) + o, static_cast<const char*>(src) + o,
                         std::min(per, n - o));
         });

@@ -175,3 +175,42 @@ def test_p2p_step_counters():
     """cuStreamWriteValue32 / cuStreamWaitValue32 as the P2P exchange uses them
     (resolved through the driver entry points), on one device."""
     L.check(L.lib().sfdb200_p2p_selftest(0))
+
+
+@pytest.mark.parametrize("p2p", [False, True])
+def test_emulated_ranks_gradient(p2p):
+    """The fused adjoint + imaging-condition kernel over z slabs (boundary
+    sweeps exchanging v, the gradient local to each rank): assembled gradient
+    equals the single-GPU one."""
+    import torch
+    w, model, src, rec, wav = _problem()
+    u, r = O.forward(model.padded, w.space_order, w.h, w.dt, w.nt, model.m, model.damp,
+                     src.idx, src.w, wav, rec.idx, rec.w, save=True)
+    resid = O._f64(np.random.default_rng(4).standard_normal(r.shape).astype(np.float32))
+    ref = S.gradient(model, rec, S.ShotRecord(w.nt, w.dt, rec.npoints, resid), u, w.nt, w.dt)
+    world = 3
+    stream = torch.cuda.Stream()
+    comms = [L.Comm.loopback(world, k, 0) for k in range(world)]
+    plans, outs = [], []
+    for k in range(world):
+        p = L.Plan(L.GRADIENT, 3, model.padded, w.space_order, w.nt, w.dt, w.h, 0,
+                   rec.npoints, False, 0, comm=comms[k])
+        p.set_stream(stream.cuda_stream)
+        grad = np.zeros(model.padded)
+        argv = [np.zeros((3, *model.padded)), u, model.m, model.damp, grad, rec.idx, rec.w, resid]
+        plans.append(p)
+        outs.append((argv, grad))
+    if p2p:
+        L.peer_group(plans)
+    for p, (argv, _) in zip(plans, outs):
+        p.upload(argv)
+    L.execute_group(plans)
+    total = np.zeros(model.padded)
+    for p, (argv, grad) in zip(plans, outs):
+        p.download(argv)
+        total += grad
+    for p in plans:
+        p.close()
+    for c in comms:
+        c.close()
+    assert O.rel_l2(total, ref.grad) <= 1e-6

@@ -1,6 +1,7 @@
 #!/usr/bin/env python
 """End-to-end cfg2 forward through sfdb200_run with plain (pageable) numpy
-host arrays, as the reference's std::vector buffers would be, vs pinned."""
+host arrays, as the reference's std::vector buffers would be, vs pinned
+(pinned first, as bench.py does)."""
 import os, sys, time
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -18,15 +19,18 @@ def main():
                   rec.npoints, False, 0)
     def pinned(shape):
         return torch.empty(shape, dtype=torch.float64, pin_memory=True).numpy()
-    for kind in ("pageable", "pinned", "pageable", "pinned"):
+    u = pinned((3, *model.padded)); m = pinned(model.m.shape); m[:] = model.m
+    d = pinned(model.damp.shape); d[:] = model.damp; rd = pinned((w.nt, rec.npoints))
+    tr = pinned(w.wavelet.shape); tr[:] = w.wavelet
+    for kind in ("pinned", "pageable", "pageable-touched"):
         if kind == "pinned":
-            u = pinned((3, *model.padded)); m = pinned(model.m.shape); m[:] = model.m
-            d = pinned(model.damp.shape); d[:] = model.damp; rd = pinned((w.nt, rec.npoints))
-            tr = pinned(w.wavelet.shape); tr[:] = w.wavelet
+            argv = [u, m, d, L.i64(src.idx), L.f64(src.w), tr, L.i64(rec.idx), L.f64(rec.w), rd]
         else:
-            u = np.empty((3, *model.padded)); m = model.m.copy(); d = model.damp.copy()
-            rd = np.empty((w.nt, rec.npoints)); tr = w.wavelet.copy()
-        argv = [u, m, d, L.i64(src.idx), L.f64(src.w), tr, L.i64(rec.idx), L.f64(rec.w), rd]
+            pu = np.empty_like(u); prd = np.empty_like(rd)
+            if kind == "pageable-touched":
+                pu[:] = 0; prd[:] = 0
+            argv = [pu, np.array(m), np.array(d), L.i64(src.idx), L.f64(src.w), np.array(tr),
+                    L.i64(rec.idx), L.f64(rec.w), prd]
         plan.run(argv)
         t0 = time.perf_counter()
         plan.run(argv)
