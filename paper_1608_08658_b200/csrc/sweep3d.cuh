@@ -619,7 +619,6 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
         }
         char* cur = reinterpret_cast<char*>(a.out + static_cast<long long>(z0) * pz +
                                             static_cast<long long>(y0 + r0) * py + x);
-        const long long stepb = dz * planeb;
 
         int stage = static_cast<int>(j % S);  // 0 with SST
         uint32_t phase = (j / S) & 1;
@@ -695,10 +694,7 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
                 const float2 inc = fma2(c1v, d, mul2(c2v, lp));
                 const float2 o = add2(c0, inc);
                 char* pj = cur + jj * rowb;
-                if (vy[jj]) {
-                    st2(reinterpret_cast<float*>(pj), o);
-                    if (a.peer_delta) st2(reinterpret_cast<float*>(pj + a.peer_delta), o);
-                }
+                if (vy[jj]) st2(reinterpret_cast<float*>(pj), o);
                 if constexpr (GRAD) {
                     const float2 vtt = fma2(d, mone, inc);
                     const float2 coef = mul2(nidt2, ld2(UT + ci));
@@ -706,7 +702,10 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
                         st2(reinterpret_cast<float*>(pj + gdiff), fma2(coef, vtt, ld2(GR + ci)));
                 }
             }
-            cur += stepb;
+            if (dz > 0)
+                cur += planeb;
+            else
+                cur -= planeb;
 
             __syncwarp();
             if (lx == 0) mbar_arrive(&empty[st]);
@@ -730,6 +729,24 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
             }
         }
         j += static_cast<uint32_t>(n);
+        // Fused P2P ghost exchange (boundary launches only): each thread sends
+        // the values it stored for this item to the neighbour's ghost planes
+        // (re-read from L2; its own stores, so no barrier), out of the plane
+        // loop so the interior launches carry none of it.
+        if (a.peer_delta) {
+            const char* c = reinterpret_cast<const char*>(
+                a.out + static_cast<long long>(z0) * pz + static_cast<long long>(y0 + r0) * py + x);
+            for (int i = 0; i < n; ++i) {
+                const char* cp = c + static_cast<long long>(dz * i) * planeb;
+#pragma unroll
+                for (int jj = 0; jj < NY; ++jj)
+                    if (vy[jj]) {
+                        const char* src = cp + jj * rowb;
+                        st2(reinterpret_cast<float*>(const_cast<char*>(src) + a.peer_delta),
+                            ld2(reinterpret_cast<const float*>(src)));
+                    }
+            }
+        }
         // Fused Inject once every consumer warp has stored this item's planes
         // (named barrier over the consumer warps only).
         if (a.inj_tab && __ldg(a.inj_tab + item + 1) > __ldg(a.inj_tab + item)) {
