@@ -77,8 +77,8 @@ struct SweepArgs {
     const int* inj_pt;
     const unsigned char* inj_gm;  // GRAD: corner inside the updated region
     const float* inj_row;         // trace row of this step
-    // Fused P2P ghost exchange (p2p.cpp): non-zero in the boundary launches,
-    // every stored value is also stored at byte offset peer_delta (the
+    // Fused P2P ghost exchange (p2p.cpp): non-zero in the boundary launches;
+    // every stored value is also written at byte offset peer_delta (the
     // neighbour's ghost copy of the plane, through its IPC mapping).
     long long peer_delta;
 };

@@ -2,10 +2,11 @@
 //
 // The NCCL path (comm.cpp) sweeps the R planes next to each neighbour, then
 // sends them with ncclSend/ncclRecv while the interior runs.  Here the two
-// boundary sweeps store every plane twice: into this rank's row and, through a
-// CUDA IPC mapping of the neighbour's field, straight into the neighbour's
-// ghost planes of the same row (sweep3d.cuh, SweepArgs::peer_delta), so the
-// transfer happens inside the sweep, tile by tile.  Injections that land in
+// boundary sweeps also write their planes, through a CUDA IPC mapping of the
+// neighbour's field, straight into the neighbour's ghost planes of the same
+// row: each thread re-sends its own stores right after its item
+// (sweep3d.cuh, SweepArgs::peer_delta), so the transfer happens inside the
+// sweep launch, tile by tile.  Injections that land in
 // the sent planes are mirrored by a tiny copy after them.  Ordering between
 // the two processes uses one 32-bit step counter per direction in the
 // receiver's memory, written with cuStreamWriteValue32 after the boundary work
