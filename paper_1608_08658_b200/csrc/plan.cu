@@ -1199,9 +1199,17 @@ void do_download(sfdb200_plan& p, void** argv) {
     ck(cudaStreamSynchronize(p.stream), "download");
 }
 
+// sfdb200_call's plans, one per descriptor: the map is guarded by g_cache_mu
+// (lookup / creation only); each plan has its own mutex, so calls on different
+// descriptors (e.g. different GPUs) run concurrently and calls on the same one
+// queue, as the reference's one-host-thread-per-invocation model expects.
+struct CachedPlan {
+    std::unique_ptr<sfdb200_plan> plan;
+    std::mutex mu;
+};
 std::mutex g_cache_mu;
-std::map<std::string, std::unique_ptr<sfdb200_plan>>& plan_cache() {
-    static std::map<std::string, std::unique_ptr<sfdb200_plan>> m;
+std::map<std::string, std::unique_ptr<CachedPlan>>& plan_cache() {
+    static std::map<std::string, std::unique_ptr<CachedPlan>> m;
     return m;
 }
 
@@ -1310,14 +1318,20 @@ int sfdb200_run(sfdb200_plan* p, void** argv) {
 int sfdb200_call(const sfdb200_desc* desc, void** argv) {
     return guarded([&] {
         if (!desc || !argv) fail(SFDB200_EINVAL, "null argument");
-        std::lock_guard<std::mutex> lock(g_cache_mu);
-        auto& slot = plan_cache()[desc_key(*desc)];
-        if (!slot) {
+        CachedPlan* cp = nullptr;
+        {
+            std::lock_guard<std::mutex> lock(g_cache_mu);
+            auto& slot = plan_cache()[desc_key(*desc)];
+            if (!slot) slot = std::make_unique<CachedPlan>();
+            cp = slot.get();
+        }
+        std::lock_guard<std::mutex> run_lock(cp->mu);
+        if (!cp->plan) {
             auto p = std::make_unique<sfdb200_plan>();
             create(*desc, nullptr, *p);
-            slot = std::move(p);
+            cp->plan = std::move(p);
         }
-        sfdb200_plan& p = *slot;
+        sfdb200_plan& p = *cp->plan;
         ck(cudaSetDevice(p.d.device), "cudaSetDevice");
         do_upload(p, argv);
         do_execute(p);

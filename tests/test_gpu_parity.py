@@ -308,3 +308,40 @@ def test_odd_shapes_every_order(so):
     go, _ = O.gradient(model.padded, so, h, dt, nt, model.m, model.damp, us, recp.idx, recp.w,
                        resid)
     assert O.rel_l2(g.grad, go) <= TOL
+
+
+def test_reference_abi_concurrent_calls():
+    """sfdb200_call from several host threads at once: two descriptors run
+    concurrently (per-plan locks), repeated calls on one descriptor queue on its
+    plan; every result matches the oracle."""
+    import threading
+
+    from paper_1608_08658_b200 import _lib as L
+    problems = []
+    for n in (22, 26):
+        w = configs.cfg2(n=n, nt=52, nbpml=6, nrec_side=4)
+        model, src, rec = _setup(w)
+        uo, ro = _oracle_forward(w, model, src, rec)
+        problems.append((w, model, src, rec, uo, ro))
+    errors = []
+
+    def worker(k):
+        w, model, src, rec, uo, ro = problems[k % 2]
+        try:
+            for _ in range(3):
+                u = np.zeros((3, *model.padded))
+                rd = np.zeros((w.nt, rec.npoints))
+                L.call(L.FORWARD, 3, model.padded, w.space_order, w.nt, w.dt, w.h, src.npoints,
+                       rec.npoints, False, [u, model.m, model.damp, src.idx, src.w,
+                                            O._f64(w.wavelet), rec.idx, rec.w, rd])
+                if not (O.rel_l2(u, uo) <= TOL and O.rel_l2(rd, ro) <= TOL):
+                    errors.append(k)
+        except Exception as e:  # noqa: BLE001
+            errors.append(repr(e))
+
+    threads = [threading.Thread(target=worker, args=(k,)) for k in range(4)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
