@@ -37,8 +37,10 @@ struct Blob {  // SFDB200_IPC_BYTES, plain bytes exchanged by the caller
     cudaIpcMemHandle_t field;
     cudaIpcMemHandle_t flags;
     int device;
-    int pz;
-    long long slot;
+    int pz;             // local planes
+    long long slot;     // elements per row
+    long long plane;    // elements per plane (y, x extents and pitch)
+    int radius;
     int rank, world;
 };
 static_assert(sizeof(Blob) <= SFDB200_IPC_BYTES, "IPC blob too large");
@@ -84,6 +86,8 @@ void p2p_export(const sfdb200_plan& p, void* out) {
     b.device = p.d.device;
     b.pz = p.g.Pz;
     b.slot = p.g.slot;
+    b.plane = p.g.pz;
+    b.radius = p.g.R;
     b.rank = p.rank;
     b.world = p.world;
     std::memset(out, 0, SFDB200_IPC_BYTES);
@@ -103,6 +107,8 @@ void p2p_import(sfdb200_plan& p, const void* lower, const void* upper) {
         std::memcpy(&b[side], blobs[side], sizeof(Blob));
         if (b[side].rank != want[side] || b[side].world != p.world)
             fail(SFDB200_EINVAL, "P2P import: blob is not the neighbour's");
+        if (b[side].plane != p.g.pz || b[side].radius != p.g.R)
+            fail(SFDB200_EINVAL, "P2P import: the neighbour's plan is for another problem");
         int can = 0;
         ck(cudaDeviceCanAccessPeer(&can, p.d.device, b[side].device), "cudaDeviceCanAccessPeer");
         if (!can) fail(SFDB200_EINVAL, "P2P import: neighbour device is not peer-accessible");
