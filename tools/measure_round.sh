@@ -21,5 +21,16 @@ SFDB200_TILE=$1 SFDB200_ZCHUNKS=$2 timeout 900 ncu --metrics gpu__time_duration.
 SFDB200_TILE=$1 SFDB200_ZCHUNKS=$2 timeout 600 python tools/sweep_time.py --workload cfg2 --time-steps 4 > $OUT/ncu_full_pre.log 2>&1 && \
 SFDB200_TILE=$1 SFDB200_ZCHUNKS=$2 timeout 900 ncu --set full --import-source on --clock-control none -k regex:sweep3d --launch-skip 6 --launch-count 1 -o $OUT/cfg2_full python tools/sweep_time.py --workload cfg2 --time-steps 4 > $OUT/ncu_full.log 2>&1
 python tools/ncu_summary.py $OUT/cfg2_full.ncu-rep > $OUT/ncu_cfg2_full.json
+# the cfg4 so 8 sweep and the cfg3 gradient sweep, autotuned tilings
+set -- $(python -c "
+import json; d=json.loads(open('$OUT/bench_cfg4-so8.json').read().strip().splitlines()[-1]); c=d['config']['sweep']
+print(c['variant'], c['zchunks'])")
+SFDB200_TILE=$1 SFDB200_ZCHUNKS=$2 timeout 900 ncu --set full --import-source on --clock-control none -k regex:sweep3d --launch-skip 6 --launch-count 1 -o $OUT/cfg4so8_full python tools/sweep_time.py --workload cfg4-so8 --time-steps 4 > $OUT/ncu_cfg4.log 2>&1
+python tools/ncu_summary.py $OUT/cfg4so8_full.ncu-rep > $OUT/ncu_cfg4so8_full.json
+set -- $(python -c "
+import json; d=json.loads(open('$OUT/bench_cfg3.json').read().strip().splitlines()[-1]); c=d['config']['sweep']
+print(c['variant'], c['zchunks'])")
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:sweep3d --launch-skip 4 --launch-count 1 -o $OUT/cfg3_full python tools/tune.py --workload cfg3 --gradient --time-steps 8 --tiles $1 --zchunks $2 --reps 1 > $OUT/ncu_cfg3.log 2>&1
+python tools/ncu_summary.py $OUT/cfg3_full.ncu-rep > $OUT/ncu_cfg3_full.json
 python tools/power_probe.py 4 > $OUT/power.jsonl 2>&1
 echo done
