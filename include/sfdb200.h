@@ -145,12 +145,13 @@ SFDB200_API int sfdb200_execute_group(sfdb200_plan** plans, int n);
 SFDB200_API int sfdb200_plan_create_dist(const sfdb200_desc* global_desc, sfdb200_comm* comm,
                                          sfdb200_plan** out);
 /* Fused P2P ghost exchange over NVLink (the default multi-GPU path when peer
- * access is available): the two boundary sweeps of a step store
- * their planes both locally and straight into the neighbours' ghost planes
- * (peer stores through CUDA IPC mappings of the neighbours' field rows), the
- * injections that land in those planes are mirrored, and a step counter that
- * each rank writes into its neighbours' memory (stream memory operations)
- * orders the steps; no NCCL call remains on the data path.
+ * access is available): a step is one sweep launch whose first
+ * items are the boundary tiles; they write their planes (after their
+ * injections) straight into the neighbours' ghost planes through CUDA IPC
+ * mappings of the neighbours' field rows and publish the step into the
+ * neighbours' step counters, while the interior items keep computing; stream
+ * memory operations wait on the counters.  No NCCL call remains on the data
+ * path.
  * sfdb200_plan_ipc_export fills SFDB200_IPC_BYTES bytes for the caller to pass
  * to the neighbours (e.g. all-gathered through torch.distributed);
  * sfdb200_plan_ipc_import opens the lower / upper neighbour's blob (NULL at a
@@ -161,8 +162,9 @@ SFDB200_API int sfdb200_plan_create_dist(const sfdb200_desc* global_desc, sfdb20
 SFDB200_API int sfdb200_plan_ipc_export(const sfdb200_plan* plan, void* out);
 SFDB200_API int sfdb200_plan_ipc_import(sfdb200_plan* plan, const void* lower, const void* upper);
 /* Loopback harness: the emulated ranks of sfdb200_execute_group use the same
- * fused peer stores into each other's field rows (one device, no IPC; the
- * lockstep phases of execute_group order the steps). */
+ * fused launch and peer stores into each other's field rows (one device, no
+ * IPC; the lockstep phases of execute_group order the steps).  Call before
+ * upload (the sparse tables depend on the boundary items). */
 SFDB200_API int sfdb200_plan_peer_group(sfdb200_plan** plans, int n);
 /* The step-counter primitives of the P2P exchange on one device: a stream
  * writes a counter (cuStreamWriteValue32) and waits for it (GEQ). */

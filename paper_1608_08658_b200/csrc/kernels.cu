@@ -158,15 +158,6 @@ __global__ void inject_kernel(float* __restrict__ field, const long long* __rest
     if (grad && gmask[i]) atomicAdd(grad + o, nidt2 * ut[o] * delta);
 }
 
-__global__ void mirror_kernel(const float* __restrict__ field, const long long* __restrict__ off,
-                              const unsigned char* __restrict__ side, long n, float* lo,
-                              float* hi) {
-    const long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x;
-    if (i >= n) return;
-    const long long o = off[i];
-    (side[i] ? hi : lo)[o] = field[o];
-}
-
 template <int C>
 __global__ void sample_kernel(const float* __restrict__ field, const long long* __restrict__ off,
                               const float* __restrict__ w, const int* __restrict__ pt,
@@ -435,13 +426,6 @@ cudaError_t launch_inject(float* field, const long long* off, const float* coef,
     if (n == 0) return cudaSuccess;
     inject_kernel<<<grid_for(n, 128), 128, 0, s>>>(field, off, coef, pt, row, n, grad, ut, gmask,
                                                    nidt2);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_mirror(const float* field, const long long* off, const unsigned char* side,
-                          long n, float* lo, float* hi, cudaStream_t s) {
-    if (n == 0) return cudaSuccess;
-    mirror_kernel<<<grid_for(n, 128), 128, 0, s>>>(field, off, side, n, lo, hi);
     return cudaGetLastError();
 }
 

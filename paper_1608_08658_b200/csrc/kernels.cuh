@@ -77,10 +77,22 @@ struct SweepArgs {
     const int* inj_pt;
     const unsigned char* inj_gm;  // GRAD: corner inside the updated region
     const float* inj_row;         // trace row of this step
-    // Fused P2P ghost exchange (p2p.cpp): non-zero in the boundary launches;
-    // every stored value is also written at byte offset peer_delta (the
-    // neighbour's ghost copy of the plane, through its IPC mapping).
-    long long peer_delta;
+    // Fused P2P ghost exchange (p2p.cpp), pair kernel: the first nbi items
+    // of the launch are the boundary tiles (R planes next to a neighbour,
+    // group g of `tiles` items on side bside[g]: planes [bz[side], bz[side] + R));
+    // after its planes and injections each boundary item re-sends its values
+    // to byte offset pdelta[side] (the neighbour's ghost copy, through its IPC
+    // mapping).  The last boundary item to finish (done counter reaching
+    // done_target) publishes sig_value to the neighbours' step counters
+    // sig[0], sig[1] (system-scope release).  nbi = 0: no boundary items.
+    int nbi;
+    int bside[2];
+    int bz[2];
+    long long pdelta[2];
+    unsigned int* done;
+    unsigned int done_target;
+    unsigned int* sig[2];
+    unsigned int sig_value;
 };
 
 struct SweepMaps {          // TMA descriptors (3-D only)
@@ -230,10 +242,6 @@ int loop2d_blocks_per_sm(int R, bool grad);
 cudaError_t launch_inject(float* field, const long long* off, const float* coef, const int* pt,
                           const float* row, long n, float* grad, const float* ut,
                           const unsigned char* gmask, float nidt2, cudaStream_t s);
-// P2P mirrors: field[off[i]] copied to (side[i] ? hi : lo)[off[i]] (the
-// neighbours' ghost copies of injected corners in the sent planes).
-cudaError_t launch_mirror(const float* field, const long long* off, const unsigned char* side,
-                          long n, float* lo, float* hi, cudaStream_t s);
 // pt (optional): output index of each sampled point (a subset of the set).
 cudaError_t launch_sample(const float* field, const long long* off, const float* w,
                           const int* pt, float* row, long npoints, int corners, cudaStream_t s);

@@ -1,21 +1,18 @@
 // Fused P2P ghost exchange between z-slab ranks over NVLink.
 //
-// The NCCL path (comm.cpp) sweeps the R planes next to each neighbour, then
-// sends them with ncclSend/ncclRecv while the interior runs.  Here the two
-// boundary sweeps also write their planes, through a CUDA IPC mapping of the
-// neighbour's field, straight into the neighbour's ghost planes of the same
-// row: each thread re-sends its own stores right after its item
-// (sweep3d.cuh, SweepArgs::peer_delta), so the transfer happens inside the
-// sweep launch, tile by tile.  Injections that land in
-// the sent planes are mirrored by a tiny copy after them.  Ordering between
-// the two processes uses one 32-bit step counter per direction in the
-// receiver's memory, written with cuStreamWriteValue32 after the boundary work
-// of a step (the write is fenced behind the earlier peer stores) and waited on
-// with cuStreamWaitValue32 (GEQ) before the receiver's next step:
+// The NCCL path (comm.cpp) sweeps the R planes next to each neighbour in their
+// own launches, then sends them with ncclSend/ncclRecv while the interior
+// runs.  Here a step is ONE sweep launch whose first items are those boundary
+// tiles (sweep3d.cuh, SweepArgs::nbi): each boundary item, after its planes
+// and injections, re-sends its values through a CUDA IPC mapping of the
+// neighbour's field straight into the neighbour's ghost planes of the same
+// row (SweepArgs::pdelta), and the last boundary item publishes the step into
+// the neighbours' counters (st.release.sys) while the interior items of the
+// same launch keep running.  Ordering between the processes:
 //
-//   exec_begin:  zero rows -> signal B (ready) -> wait neighbours >= B
-//   step i:      wait >= B + i -> boundary sweeps (+ peer stores) ->
-//                inject (+ mirrors) -> signal B + i + 1 -> interior sweep
+//   exec_begin:  zero rows -> signal B (cuStreamWriteValue32) -> wait >= B
+//   step i:      wait >= B + i (cuStreamWaitValue32, GEQ) -> fused launch,
+//                whose boundary items publish B + i + 1 to the neighbours
 //   exec_end:    wait >= B + steps        (their last stores into my ghosts)
 //
 // B advances by steps + 1 per execute on every rank, so counters never reset.
@@ -72,10 +69,9 @@ long long p2p_delta(const sfdb200_plan& p, int side, long long row) {
     return static_cast<long long>(theirs - mine);
 }
 
-float* p2p_mirror_base(const sfdb200_plan& p, int side, long long row) {
-    const long long d = p2p_delta(p, side, row);
-    return reinterpret_cast<float*>(reinterpret_cast<std::uintptr_t>(p.field + row * p.g.slot) +
-                                    static_cast<std::uintptr_t>(d));
+int p2p_boundary_items(const sfdb200_plan& p) {
+    if (!p.dist() || !p.p2p || p.g.ndim != 3) return 0;
+    return p.cfg.tiles_x * p.cfg.tiles_y * ((p.rank > 0 ? 1 : 0) + (p.rank < p.world - 1 ? 1 : 0));
 }
 
 void p2p_export(const sfdb200_plan& p, void* out) {

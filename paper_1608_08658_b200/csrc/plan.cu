@@ -423,6 +423,7 @@ void autotune(sfdb200_plan& p) {
     float best = 1e30f;
     SweepConfig pick = start;
     for (const V& v : variants) {
+        if (p.p2p && v.pair != 1) continue;  // the fused P2P launch is a column-pair kernel
         for (int zc = 1; zc <= std::min(8, std::max(1, zupd / (2 * R + 4))); ++zc) {
             SweepConfig c = start;
             c.by = v.by;
@@ -580,6 +581,7 @@ void do_upload(sfdb200_plan& p, void** argv) {
 // phases per rank; execute_group() runs emulated ranks in lockstep on one GPU.
 
 struct StepState {
+    unsigned int flag_base = 0;  // P2P step-counter epoch of this execute
     long prev_srow = -1;
     const float* prev_out = nullptr;
     SweepArgs a{};
@@ -675,21 +677,10 @@ void phase_boundary(sfdb200_plan& p, StepState& st) {
         b.zlo = side == 0 ? R : g.Pz - 2 * R;
         b.zhi = b.zlo + R;
         b.zchunk = R;
-        // P2P: the sweep also stores these planes into the neighbour's ghost planes
-        if (p.p2p) b.peer_delta = p2p_delta(p, side, st.a.row_out);
         ck(launch_sweep3d(g, bcfg, p.maps, b, p.grad_kind(), p.stream), "sweep3d (boundary)");
         ++p.launches;
     }
     launch_rest_inject(p, st);
-    SparseDev& inj = p.injected();
-    if (p.p2p && inj.mir_n) {  // injected corners in the sent planes
-        ck(launch_mirror(st.a.out, inj.mir_off, inj.mir_side, inj.mir_n,
-                         p.peer_field[0] ? p2p_mirror_base(p, 0, st.a.row_out) : nullptr,
-                         p.peer_field[1] ? p2p_mirror_base(p, 1, st.a.row_out) : nullptr,
-                         p.stream),
-           "mirror");
-        ++p.launches;
-    }
 }
 
 void phase_interior(sfdb200_plan& p, long i, StepState& st) {
@@ -700,6 +691,27 @@ void phase_interior(sfdb200_plan& p, long i, StepState& st) {
     c.zlo = p.zint_lo;
     c.zhi = p.zint_hi;
     c.zchunk = p.cfg.zlen;
+    // Fused P2P exchange: the launch starts with the boundary tiles, which also
+    // write their planes into the neighbours' ghost planes (p2p.cpp).
+    if (const int nbi = p2p_boundary_items(p)) {
+        if (p.cfg.pair != 1) fail(SFDB200_EINVAL, "the P2P exchange needs a column-pair tiling");
+        const int R = g.R;
+        c.nbi = nbi;
+        int grp = 0;
+        for (int side = 0; side < 2; ++side) {
+            if (!p.peer_field[side]) continue;
+            c.bside[grp++] = side;
+            c.bz[side] = side == 0 ? R : g.Pz - 2 * R;
+            c.pdelta[side] = p2p_delta(p, side, st.a.row_out);
+        }
+        if (p.p2p_sync) {  // the last boundary item publishes step i to the neighbours
+            c.done = p.flags + 16;
+            c.done_target = static_cast<unsigned int>((i + 1) * nbi);
+            if (p.peer_flags[0]) c.sig[0] = p.peer_flags[0] + 1;  // I am its upper neighbour
+            if (p.peer_flags[1]) c.sig[1] = p.peer_flags[1];      // I am its lower neighbour
+            c.sig_value = st.flag_base + static_cast<unsigned int>(i) + 1;
+        }
+    }
     if (p.fused && inj.f_tab) {
         c.inj_tab = inj.f_tab;
         c.inj_off = inj.f_off;
@@ -721,7 +733,8 @@ void phase_interior(sfdb200_plan& p, long i, StepState& st) {
     if (p.timing) ck(cudaEventRecord(p.events[2 * i + 1], p.stream), "event");
     ++p.timed_launches;
     ++p.launches;
-    if (!p.dist()) launch_rest_inject(p, st);  // unfused, or halo-cell corners
+    // unfused, or halo-cell corners (dist + NCCL: after the boundary launches)
+    if (!p.dist() || p.p2p) launch_rest_inject(p, st);
 }
 
 void phase_samples(sfdb200_plan& p, StepState& st) {
@@ -1089,9 +1102,11 @@ void do_execute(sfdb200_plan& p) {
     StepState st;
     // P2P exchange (p2p.cpp): every rank zeroed its rows before any neighbour
     // stores into them; step i starts once the neighbours' step i-1 planes
-    // are in place.
+    // are in place (their fused launch of step i-1 publishes B + i).
     const unsigned int B = p.flag_base;
+    st.flag_base = B;
     if (p.p2p_sync) {
+        ck(cudaMemsetAsync(p.flags + 16, 0, sizeof(unsigned int), p.stream), "memset");
         p2p_signal(p, B, p.stream);
         p2p_wait(p, B, p.stream);
     }
@@ -1099,8 +1114,6 @@ void do_execute(sfdb200_plan& p) {
         step_setup(p, i, st);
         if (p.dist() && p.p2p) {
             if (p.p2p_sync) p2p_wait(p, B + static_cast<unsigned int>(i), p.stream);
-            phase_boundary(p, st);  // boundary sweeps store into the neighbours too
-            if (p.p2p_sync) p2p_signal(p, B + static_cast<unsigned int>(i) + 1, p.stream);
         } else if (p.dist()) {
             phase_boundary(p, st);
             ck(cudaEventRecord(p.ev_b, p.stream), "event");
@@ -1139,7 +1152,8 @@ void do_execute_group(sfdb200_plan** plans, int n) {
     for (long i = 0; i < steps; ++i) {
         for (int r = 0; r < n; ++r) {
             step_setup(*plans[r], i, st[r]);
-            phase_boundary(*plans[r], st[r]);
+            // P2P peer group: the boundary tiles run inside the interior launch
+            if (!plans[r]->p2p) phase_boundary(*plans[r], st[r]);
         }
         // ghost planes between ranks r and r+1 (P2P peer group: already stored
         // by the boundary sweeps)

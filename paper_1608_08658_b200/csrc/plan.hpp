@@ -69,11 +69,6 @@ struct SparseDev {
     int* f_pt = nullptr;
     unsigned char* f_gm = nullptr;
     InjectList inj_rest;
-    // P2P exchange: rest corners inside the planes sent to a neighbour
-    // (side 0 lower, 1 upper), mirrored after the injection (launch_mirror).
-    long mir_n = 0;
-    long long* mir_off = nullptr;
-    unsigned char* mir_side = nullptr;
     // Sampling: every owned receiver (smp_all).  In the fused 3-D sweep the
     // previous row is sampled at the start of the next interior launch
     // (s_base = corner-0 offsets, weights and columns shared with smp_all);
@@ -108,9 +103,6 @@ struct SparseDev {
         f_tab = nullptr; f_off = nullptr; f_coef = nullptr; f_pt = nullptr; f_gm = nullptr;
         s_base = nullptr;
         inj_rest = InjectList{};
-        mir_n = 0;
-        mir_off = nullptr;
-        mir_side = nullptr;
         smp_all = SampleList{};
         k_n = 0;
         k_max = 0;
@@ -267,10 +259,12 @@ void copy_d2h(sfdb200_plan& p, void* dst, const void* src, size_t bytes);
 void release_pinned(sfdb200_plan& p);
 
 // p2p.cpp: fused P2P ghost exchange.
-// Byte offset from my `row` of plane zl to the neighbour's ghost copy of it.
+// Byte offset from my `row` to the neighbour's ghost copy of the planes I
+// send it on `side` (0 lower, 1 upper).
 long long p2p_delta(const sfdb200_plan& p, int side, long long row);
-// The neighbour's address of my local element offset 0 in `row` (mirrors).
-float* p2p_mirror_base(const sfdb200_plan& p, int side, long long row);
+// Boundary tiles at the front of the fused interior launch (0 unless the plan
+// uses the P2P exchange): tiles x (number of neighbours).
+int p2p_boundary_items(const sfdb200_plan& p);
 void p2p_export(const sfdb200_plan& p, void* out);
 void p2p_import(sfdb200_plan& p, const void* lower, const void* upper);
 void p2p_release(sfdb200_plan& p);

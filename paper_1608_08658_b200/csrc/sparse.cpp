@@ -2,7 +2,7 @@
 // sampling) for one plan: corner offsets in the device layout, ownership by
 // z-slab rank, and the per-CTA tables that let the 3-D sweep apply them inside
 // its own launch (injections after the CTA's planes, samples of the previous
-// row at the CTA's start), plus the P2P mirror list.
+// row at the CTA's start), including the P2P boundary items.
 //
 // Reference semantics: codegen.cpp:419-462 (corner bit order: bit ndim-1-d of
 // c -> +1 along dim d; inject w * scale * data / m[corner]; sample
@@ -20,24 +20,41 @@ struct Owner {
     int cta, plane;
 };
 
-// Sweep CTA of the interior launch (x tiles fastest, then y tiles, then z
-// chunks) and its local plane index for a point of the interior range.
+// Item of the interior launch (x tiles fastest, then y tiles, then z chunks)
+// holding a point, and its local plane index.  With the fused P2P exchange the
+// launch starts with p2p_boundary_items(p) boundary tiles (R planes next to a
+// neighbour, lower side first), which own the points of those planes.
 Owner owner_of(const sfdb200_plan& p, long zl, long y, long x) {
     const SweepConfig& c = p.cfg;
     const int R = p.g.R;
+    const int bx = static_cast<int>(x / 32), by = static_cast<int>((y - R) / c.ty());
+    const int tile = bx + c.tiles_x * by, tiles = c.tiles_x * c.tiles_y;
+    const int nbi = p2p_boundary_items(p);
+    if (nbi) {
+        const bool lo = p.rank > 0 && zl >= R && zl < 2 * R;
+        const bool hi = p.rank < p.world - 1 && zl >= p.g.Pz - 2 * R && zl < p.g.Pz - R;
+        if (lo) return {tile, static_cast<int>(zl - R)};
+        if (hi) return {(p.rank > 0 ? tiles : 0) + tile, static_cast<int>(zl - (p.g.Pz - 2 * R))};
+    }
     const long zr = zl - p.zint_lo;
-    const int bx = static_cast<int>(x / 32), by = static_cast<int>((y - R) / c.ty()),
-              bz = static_cast<int>(zr / c.zlen);
-    return {bx + c.tiles_x * (by + c.tiles_y * bz), static_cast<int>(zr - bz * c.zlen)};
+    const int bz = static_cast<int>(zr / c.zlen);
+    return {nbi + tile + tiles * bz, static_cast<int>(zr - bz * c.zlen)};
 }
 
+// Swept by the interior launch (including its P2P boundary items).
 bool in_interior(const sfdb200_plan& p, long zl, long y, long x) {
     const int R = p.g.R;
-    return zl >= p.zint_lo && zl < p.zint_hi && y >= R && y < p.g.Py - R && x >= R &&
-           x < p.g.Px - R;
+    const bool in_xy = y >= R && y < p.g.Py - R && x >= R && x < p.g.Px - R;
+    if (!in_xy) return false;
+    if (zl >= p.zint_lo && zl < p.zint_hi) return true;
+    if (!p2p_boundary_items(p)) return false;
+    return (p.rank > 0 && zl >= R && zl < 2 * R) ||
+           (p.rank < p.world - 1 && zl >= p.g.Pz - 2 * R && zl < p.g.Pz - R);
 }
 
-int ctas_of(const sfdb200_plan& p) { return p.cfg.tiles_x * p.cfg.tiles_y * p.cfg.zchunks; }
+int ctas_of(const sfdb200_plan& p) {
+    return p.cfg.tiles_x * p.cfg.tiles_y * p.cfg.zchunks + p2p_boundary_items(p);
+}
 
 // 2-D cluster time loop: the CTA whose shared-memory rows hold row z (its
 // band; the global halo rows belong to the first / last CTA) and the first
@@ -91,6 +108,7 @@ unsigned long long fingerprint(const sfdb200_plan& p, unsigned long long data) {
                                            static_cast<unsigned>(p.cfg.zlen));
     h = mix64(h, static_cast<unsigned long long>(p.cfg.zchunks) << 32 ^
                      static_cast<unsigned>(p.cfg.tiles_x));
+    h = mix64(h, static_cast<unsigned long long>(p2p_boundary_items(p)));
     return h | 1ULL;
 }
 
@@ -251,24 +269,6 @@ void upload_sparse(sfdb200_plan& p, SparseDev& s, const long* idx, const double*
             r_pt.push_back(static_cast<int>(i / C));
             r_gm.push_back(k.updated ? 1 : 0);
         }
-        // Corners of the rest list inside the planes the boundary sweeps send to
-        // a neighbour: the P2P exchange mirrors them after the injection.
-        std::vector<long long> m_off;
-        std::vector<unsigned char> m_side;
-        if (p.dist())
-            for (const long long o : r_off) {
-                const long zl = static_cast<long>(o / g.pz);
-                if (p.rank > 0 && zl >= R && zl < 2 * R) {
-                    m_off.push_back(o);
-                    m_side.push_back(0);
-                } else if (p.rank < p.world - 1 && zl >= g.Pz - 2 * R && zl < g.Pz - R) {
-                    m_off.push_back(o);
-                    m_side.push_back(1);
-                }
-            }
-        s.mir_n = static_cast<long>(m_off.size());
-        s.mir_off = s.upload(m_off, st);
-        s.mir_side = s.upload(m_side, st);
         s.inj_rest.n = static_cast<long>(r_off.size());
         s.inj_rest.off = s.upload(r_off, st);
         s.inj_rest.coef = s.upload(r_coef, st);

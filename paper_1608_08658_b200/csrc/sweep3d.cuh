@@ -377,10 +377,6 @@ __global__ void __launch_bounds__(32 * (BY + 1), 4)
             char* pb = pa + halfb;
             if (va[j]) *reinterpret_cast<float*>(pa) = o.x;
             if (vb[j]) *reinterpret_cast<float*>(pb) = o.y;
-            if (a.peer_delta) {  // fused P2P ghost exchange (boundary launches)
-                if (va[j]) *reinterpret_cast<float*>(pa + a.peer_delta) = o.x;
-                if (vb[j]) *reinterpret_cast<float*>(pb + a.peer_delta) = o.y;
-            }
             if constexpr (GRAD) {
                 // grad += -(1/dt^2) u_t (v_t - 2 v_{t+1} + v_{t+2}) = nidt2 * u_t * (inc - d)
                 const float2 vtt = fma2(d, mone, inc);
@@ -479,15 +475,31 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
     const int lx = threadIdx.x;
     const int tid = threadIdx.y * 32 + lx;
     // item -> tile origin (x0, y0), z range [zb, ze) and direction: planes
-    // z0, z0 + dz, ... (dz = -1: the chunk streams downward, a.zdown)
-    auto decode = [&](int item, int& x0, int& y0, int& zb, int& ze, int& z0, int& dz) {
+    // z0, z0 + dz, ... (dz = -1: the chunk streams downward, a.zdown).  The
+    // first a.nbi items are the P2P boundary tiles (SweepArgs::nbi); their side
+    // is returned in bs (-1 for interior items).
+    auto decode = [&](int item, int& x0, int& y0, int& zb, int& ze, int& z0, int& dz, int& bs) {
+        bs = -1;
+        int tz = 0;
+        if (item < a.nbi) {
+            const int tiles = ntx * nty, grp = item / tiles;
+            bs = a.bside[grp];
+            item -= grp * tiles;
+        } else {
+            item -= a.nbi;
+        }
         const int r = item / ntx;
         x0 = (item - r * ntx) * T::TX;
-        const int tz = r / nty;
+        if (bs < 0) tz = r / nty;
         y0 = R + (r - tz * nty) * T::TY;
-        zb = a.zlo + tz * a.zchunk;
-        ze = min(zb + a.zchunk, a.zhi);
-        const bool dn = tz < 64 && ((a.zdown >> tz) & 1ull);
+        if (bs >= 0) {
+            zb = a.bz[bs];
+            ze = zb + R;
+        } else {
+            zb = a.zlo + tz * a.zchunk;
+            ze = min(zb + a.zchunk, a.zhi);
+        }
+        const bool dn = bs < 0 && tz < 64 && ((a.zdown >> tz) & 1ull);
         z0 = dn ? ze - 1 : zb;
         dz = dn ? -1 : 1;
     };
@@ -512,8 +524,8 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
                 return st;
             };
             for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
-                int x0, y0, zb, ze, z0, dz;
-                decode(item, x0, y0, zb, ze, z0, dz);
+                int x0, y0, zb, ze, z0, dz, bs;
+                decode(item, x0, y0, zb, ze, z0, dz, bs);
                 const int n = ze - zb;
                 if (n <= 0) continue;
                 if constexpr (SST) {
@@ -573,8 +585,8 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
     uint32_t j = 0;  // stage sequence number, as the producer's
 
     for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
-        int x0, y0, zb, ze, z0, dz;
-        decode(item, x0, y0, zb, ze, z0, dz);
+        int x0, y0, zb, ze, z0, dz, bs;
+        decode(item, x0, y0, zb, ze, z0, dz, bs);
         const int n = ze - zb;
         if (n <= 0) continue;
         if constexpr (SST) {
@@ -729,29 +741,43 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
             }
         }
         j += static_cast<uint32_t>(n);
-        // Fused P2P ghost exchange (boundary launches only): each thread sends
-        // the values it stored for this item to the neighbour's ghost planes
-        // (re-read from L2; its own stores, so no barrier), out of the plane
-        // loop so the interior launches carry none of it.
-        if (a.peer_delta) {
-            const char* c = reinterpret_cast<const char*>(
-                a.out + static_cast<long long>(z0) * pz + static_cast<long long>(y0 + r0) * py + x);
-            for (int i = 0; i < n; ++i) {
-                const char* cp = c + static_cast<long long>(dz * i) * planeb;
-#pragma unroll
-                for (int jj = 0; jj < NY; ++jj)
-                    if (vy[jj]) {
-                        const char* src = cp + jj * rowb;
-                        st2(reinterpret_cast<float*>(const_cast<char*>(src) + a.peer_delta),
-                            ld2(reinterpret_cast<const float*>(src)));
-                    }
-            }
-        }
         // Fused Inject once every consumer warp has stored this item's planes
         // (named barrier over the consumer warps only).
         if (a.inj_tab && __ldg(a.inj_tab + item + 1) > __ldg(a.inj_tab + item)) {
             named_barrier_sync(1, NT);
             inject_cta<GRAD, NT>(a, item, tid);
+        }
+        // Fused P2P ghost exchange (boundary items only): after the item's
+        // injections, each thread re-sends the values it stored (read back
+        // through L2) to the neighbour's ghost planes; the last boundary item
+        // of the launch then publishes the step to the neighbours' counters.
+        if (bs >= 0) {
+            named_barrier_sync(1, NT);  // the injections (atomics) are done
+            const long long pd = a.pdelta[bs];
+            const char* c = reinterpret_cast<const char*>(
+                a.out + static_cast<long long>(z0) * pz + static_cast<long long>(y0 + r0) * py + x);
+            for (int i = 0; i < n; ++i) {
+                const char* cp = c + static_cast<long long>(i) * planeb;
+#pragma unroll
+                for (int jj = 0; jj < NY; ++jj)
+                    if (vy[jj]) {
+                        const float* src = reinterpret_cast<const float*>(cp + jj * rowb);
+                        const float2 v = __ldcg(reinterpret_cast<const float2*>(src));
+                        st2(reinterpret_cast<float*>(const_cast<char*>(cp + jj * rowb) + pd), v);
+                    }
+            }
+            if (a.done) {
+                __threadfence_system();  // this thread's peer stores, system-wide
+                named_barrier_sync(1, NT);
+                if (tid == 0 && atomicAdd(a.done, 1u) + 1u == a.done_target) {
+                    __threadfence_system();
+                    for (int sd = 0; sd < 2; ++sd)
+                        if (a.sig[sd])
+                            asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(a.sig[sd]),
+                                         "r"(a.sig_value)
+                                         : "memory");
+                }
+            }
         }
     }
 }
@@ -837,7 +863,7 @@ cudaError_t launch3d_pair_t(const FieldGeom& g, const SweepConfig& cfg, const Sw
         resident_smem = smem;
     }
     if (resident < 1) return cudaErrorInvalidConfiguration;
-    const int nitems = cfg.tiles_x * cfg.tiles_y * cfg.zchunks;
+    const int nitems = cfg.tiles_x * cfg.tiles_y * cfg.zchunks + a.nbi;  // + P2P boundary tiles
     // cfg.ctas: 0 = one CTA per item (the hardware hands items to free slots
     // dynamically), > 0 = that many persistent CTAs, < 0 = one per resident slot.
     const int ctas = cfg.ctas > 0   ? std::min(cfg.ctas, nitems)
