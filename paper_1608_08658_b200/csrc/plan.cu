@@ -568,6 +568,7 @@ void do_upload(sfdb200_plan& p, void** argv) {
         tables();
         refine_with_sparse(p, tables);
     }
+    p.tables_nbi = p2p_boundary_items(p);
     ck(cudaStreamSynchronize(p.stream), "upload");
 }
 
@@ -693,6 +694,8 @@ void phase_interior(sfdb200_plan& p, long i, StepState& st) {
     c.zchunk = p.cfg.zlen;
     // Fused P2P exchange: the launch starts with the boundary tiles, which also
     // write their planes into the neighbours' ghost planes (p2p.cpp).
+    if (p2p_boundary_items(p) != p.tables_nbi)
+        fail(SFDB200_EINVAL, "the exchange changed after upload (import peers before uploading)");
     if (const int nbi = p2p_boundary_items(p)) {
         if (p.cfg.pair != 1) fail(SFDB200_EINVAL, "the P2P exchange needs a column-pair tiling");
         const int R = g.R;

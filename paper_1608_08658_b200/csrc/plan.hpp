@@ -157,6 +157,7 @@ struct sfdb200_plan {
     unsigned int* flags = nullptr;      // my inbound step counters [2] (written by the neighbours)
     unsigned int* peer_flags[2] = {nullptr, nullptr};
     unsigned int flag_base = 1;         // epoch base, advanced identically on every rank
+    int tables_nbi = 0;                 // boundary items the sparse tables were built for
 
     float* field = nullptr;  // u (forward) / v (adjoint, gradient), `rows` rows
     float* c1 = nullptr;
