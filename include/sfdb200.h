@@ -149,9 +149,9 @@ SFDB200_API int sfdb200_plan_create_dist(const sfdb200_desc* global_desc, sfdb20
  * items are the boundary tiles; they write their planes (after their
  * injections) straight into the neighbours' ghost planes through CUDA IPC
  * mappings of the neighbours' field rows and publish the step into the
- * neighbours' step counters, while the interior items keep computing; stream
- * memory operations wait on the counters.  No NCCL call remains on the data
- * path.
+ * neighbours' step counters, while the interior items keep computing; a
+ * one-thread poll kernel waits on the counters before the next step.  No NCCL
+ * call remains on the data path.
  * sfdb200_plan_ipc_export fills SFDB200_IPC_BYTES bytes for the caller to pass
  * to the neighbours (e.g. all-gathered through torch.distributed);
  * sfdb200_plan_ipc_import opens the lower / upper neighbour's blob (NULL at a
@@ -167,7 +167,7 @@ SFDB200_API int sfdb200_plan_ipc_import(sfdb200_plan* plan, const void* lower, c
  * upload (the sparse tables depend on the boundary items). */
 SFDB200_API int sfdb200_plan_peer_group(sfdb200_plan** plans, int n);
 /* The step-counter primitives of the P2P exchange on one device: a stream
- * writes a counter (cuStreamWriteValue32) and waits for it (GEQ). */
+ * writes a counter (cuStreamWriteValue32) and waits for it (poll kernel, GEQ). */
 SFDB200_API int sfdb200_p2p_selftest(int device);
 /* Owned updated global planes of `rank`: an even split of [so/2, Pz - so/2). */
 SFDB200_API int sfdb200_slab(long padded_z, int space_order, int world, int rank, long* z_begin,

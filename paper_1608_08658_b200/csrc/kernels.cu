@@ -158,6 +158,28 @@ __global__ void inject_kernel(float* __restrict__ field, const long long* __rest
     if (grad && gmask[i]) atomicAdd(grad + o, nidt2 * ut[o] * delta);
 }
 
+// P2P step counters (p2p.cpp): one thread polls until both counters reach
+// `value` (cyclic compare), sleeping between polls; a counter that never gets
+// there (a neighbour process died) traps after `timeout_ns` instead of hanging
+// the GPU.
+__global__ void wait_flags_kernel(const unsigned int* f0, const unsigned int* f1,
+                                  unsigned int value, unsigned long long timeout_ns) {
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (const unsigned int* f : {f0, f1}) {
+        if (!f) continue;
+        for (;;) {
+            unsigned int v;
+            asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+            if (static_cast<int>(v - value) >= 0) break;
+            __nanosleep(200);
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            if (t - t0 > timeout_ns) __trap();
+        }
+    }
+}
+
 template <int C>
 __global__ void sample_kernel(const float* __restrict__ field, const long long* __restrict__ off,
                               const float* __restrict__ w, const int* __restrict__ pt,
@@ -426,6 +448,12 @@ cudaError_t launch_inject(float* field, const long long* off, const float* coef,
     if (n == 0) return cudaSuccess;
     inject_kernel<<<grid_for(n, 128), 128, 0, s>>>(field, off, coef, pt, row, n, grad, ut, gmask,
                                                    nidt2);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_wait_flags(const unsigned int* f0, const unsigned int* f1, unsigned int value,
+                              unsigned long long timeout_ns, cudaStream_t s) {
+    wait_flags_kernel<<<1, 1, 0, s>>>(f0, f1, value, timeout_ns);
     return cudaGetLastError();
 }
 

@@ -11,7 +11,7 @@
 // same launch keep running.  Ordering between the processes:
 //
 //   exec_begin:  zero rows -> signal B (cuStreamWriteValue32) -> wait >= B
-//   step i:      wait >= B + i (cuStreamWaitValue32, GEQ) -> fused launch,
+//   step i:      wait >= B + i (one-thread poll kernel, GEQ) -> fused launch,
 //                whose boundary items publish B + i + 1 to the neighbours
 //   exec_end:    wait >= B + steps        (their last stores into my ghosts)
 //
@@ -42,7 +42,6 @@ struct Blob {  // SFDB200_IPC_BYTES, plain bytes exchanged by the caller
 };
 static_assert(sizeof(Blob) <= SFDB200_IPC_BYTES, "IPC blob too large");
 
-typedef CUresult (*PFN_wait32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
 typedef CUresult (*PFN_write32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
 
 template <class F>
@@ -156,17 +155,13 @@ void p2p_signal(sfdb200_plan& p, unsigned int value, cudaStream_t s) {
     }
 }
 
+// A one-thread kernel rather than cuStreamWaitValue32: a neighbour that never
+// publishes (its process died) ends in a trap after 60 s instead of a hung GPU.
 void p2p_wait(sfdb200_plan& p, unsigned int value, cudaStream_t s) {
-    static PFN_wait32 wait32 = driver_fn<PFN_wait32>("cuStreamWaitValue32");
-    for (int side = 0; side < 2; ++side) {
-        if (!p.peer_flags[side]) continue;
-        // counter written by the neighbour on `side`
-        const CUresult r = wait32(reinterpret_cast<CUstream>(s),
-                                  reinterpret_cast<CUdeviceptr>(p.flags + side), value,
-                                  CU_STREAM_WAIT_VALUE_GEQ);
-        if (r != CUDA_SUCCESS)
-            fail(SFDB200_ECUDA, "cuStreamWaitValue32 failed (" + std::to_string(r) + ")");
-    }
+    const unsigned int* f0 = p.peer_flags[0] ? p.flags + 0 : nullptr;  // written by side 0
+    const unsigned int* f1 = p.peer_flags[1] ? p.flags + 1 : nullptr;  // written by side 1
+    if (!f0 && !f1) return;
+    ck(launch_wait_flags(f0, f1, value, 60ull * 1000000000ull, s), "P2P wait");
 }
 
 void p2p_selftest(int device) {
