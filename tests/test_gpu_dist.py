@@ -220,3 +220,17 @@ def test_emulated_ranks_gradient(p2p):
     go, _ = O.gradient(model.padded, w.space_order, w.h, w.dt, w.nt, model.m, model.damp, u,
                        rec.idx, rec.w, resid)
     assert O.rel_l2(total, go) <= 1e-5
+
+
+def test_p2p_fused_launch_with_persistent_ctas():
+    """The fused P2P launch (boundary tiles first, then interior items) walked by
+    a few persistent CTAs, each running boundary and interior items in turn."""
+    import os
+    os.environ["SFDB200_CTAS"] = "5"
+    try:
+        w, model, src, rec, wav = _problem()
+        ref = S.forward(model, src, wav, rec, w.nt, w.dt, False)
+        u, tr = _run_group(L.FORWARD, w, model, src, rec, wav, 3, p2p=True)
+        assert O.rel_l2(u, ref.u) <= 1e-6 and O.rel_l2(tr, ref.record.data) <= 1e-6
+    finally:
+        os.environ.pop("SFDB200_CTAS", None)
