@@ -389,6 +389,18 @@ def run_ours(args):
                "h2d_bytes_per_step": plan.h2d_bytes, "d2h_bytes_per_step": plan.d2h_bytes,
                "ms_per_step": el / args.steps * 1e3,
                "path": "sfdb200_run(plan, argv): reference argv, pinned fp64 host buffers"}
+        # Where the e2e time goes: the same run as three synchronised stages
+        # (run() overlaps the receiver rows' D2H with the sweeps; here they all
+        # land in download).
+        stage = {}
+        for name, fn in (("upload", lambda: plan.upload(argv)), ("execute", plan.execute),
+                         ("download", lambda: plan.download(argv))):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            fn()
+            torch.cuda.synchronize()
+            stage[name] = (time.perf_counter() - t0) * 1e3
+        e2e["staged_ms"] = stage
         if world == 1:
             # The same call with pageable host arrays, as the reference's
             # std::vector buffers are (staged through the plan's pinned chunks).
