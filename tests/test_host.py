@@ -172,3 +172,22 @@ def test_cli_config_patch_and_refusal(tmp_path):
     import json as _json
     summ = _json.load(open(tmp_path / "summary.json"))
     assert summ["command"] == "error" and "CFL" in summ["error"]
+
+
+def test_operators_fail_loudly_without_the_cuda_library(monkeypatch, tmp_path):
+    """No CPU fallback: with libsfdb200.so absent the operators raise instead of
+    computing anything, and on a host without a GPU the device plan refuses."""
+    m = S.make_constant_model([17, 17], 15.0, 4, 4, 1500.0)
+    dt = 0.5 * S.critical_dt(m)
+    src = S.locate_points(m, [[120.0, 120.0]])
+    rec = S.locate_points(m, [[60.0, 200.0]])
+    wav = S.ricker(20.0, 0.05, 12, dt)
+    monkeypatch.setattr(L, "LIB_PATH", str(tmp_path / "libsfdb200.so"))
+    monkeypatch.setattr(L, "_lib", None)
+    with pytest.raises(ImportError, match="missing"):
+        S.forward(m, src, wav, rec, 12, dt, False)
+    monkeypatch.undo()
+    import torch
+    if not torch.cuda.is_available():
+        with pytest.raises(L.SfdError):
+            S.forward(m, src, wav, rec, 12, dt, False)
