@@ -259,6 +259,56 @@ def kernel_name(plan):
     return "sweep3d_pair_kernel" if info.get("mapping", "").startswith("column") else "sweep3d_kernel"
 
 
+def check_exchange(L, S, torch, dist, comm, rank, world, local, p2p):
+    """A small forward problem (waves crossing every slab boundary, receivers
+    in every slab) through this job's z-slab exchange, summed over ranks and
+    compared on rank 0 with the same problem on one GPU.  Returns (ok, the
+    larger relative L2 error of the wavefield and the record) on every rank."""
+    nt = 40
+    model = S.make_constant_model([16 * world + 8, 40, 40], 15.0, 8, 8, 1500.0)
+    dt = 0.8 * S.critical_dt(model)
+    ext = (16 * world + 7) * 15.0
+    src = S.locate_points(model, [[0.5 * ext + 4.0, 310.0, 290.0]])
+    rec = S.locate_points(model, [[f * ext, 200.0 + 200.0 * f, 330.0]
+                                  for f in np.linspace(0.02, 0.98, 16)])
+    wav = np.ascontiguousarray(S.ricker(30.0, 0.03, nt, dt).reshape(nt, 1))
+    si, sw = S._sparse_args(src, 3)
+    ri, rw = S._sparse_args(rec, 3)
+    field = np.zeros((3, *model.padded))
+    trace = np.zeros((nt, rec.npoints))
+    ok = 1
+    plan = L.Plan(L.FORWARD, 3, model.padded, 8, nt, dt, model.h, src.npoints, rec.npoints,
+                  False, local, comm=comm)
+    try:
+        if p2p:
+            blobs = [None] * world
+            dist.all_gather_object(blobs, plan.ipc_export())
+            plan.ipc_import(blobs[rank - 1] if rank > 0 else None,
+                            blobs[rank + 1] if rank < world - 1 else None)
+        plan.run([field, L.f64(model.m), L.f64(model.damp), si, sw, wav, ri, rw, trace])
+    except L.SfdError as e:
+        print(f"rank {rank}: exchange check failed: {e}", file=sys.stderr)
+        ok = 0
+    finally:
+        plan.close()
+    flag = torch.tensor([ok], device="cuda")
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    total = torch.from_numpy(np.concatenate([field.ravel(), trace.ravel()])).cuda()
+    dist.reduce(total, 0, op=dist.ReduceOp.SUM)
+    err = torch.tensor([float("inf")], device="cuda", dtype=torch.float64)
+    if rank == 0:
+        ref = S.forward(model, src, wav, rec, nt, dt, False, S.RunConfig(device=local))
+        got = total.cpu().numpy()
+
+        def rel(a, b):
+            return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+        err[0] = max(rel(got[:field.size], np.asarray(ref.u).ravel()),
+                     rel(got[field.size:], ref.record.data.ravel()))
+    dist.broadcast(err, 0)
+    e = float(err.item())
+    return bool(int(flag.item()) == 1 and e <= 1e-5), e
+
+
 def run_ours(args):
     import torch
     from paper_1608_08658_b200 import _lib as L
@@ -321,6 +371,26 @@ def run_ours(args):
                 plan = L.Plan(L.FORWARD, nd, model.padded, w.space_order, w.nt, w.dt, w.h,
                               src.npoints, rec.npoints, False, local, comm=comm)
                 plan.set_stream(stream.cuda_stream)
+
+    exchange_check = None
+    if world > 1:
+        # The exchange has only ever run with emulated ranks on one GPU before
+        # this job: check it on a small problem against one GPU first, and fall
+        # back to NCCL if the fused P2P path fails or disagrees.
+        p2p = exchange.startswith("fused")
+        ok, err = check_exchange(L, S, torch, dist, comm, rank, world, local, p2p)
+        exchange_check = {"exchange": "p2p" if p2p else "nccl", "ok": ok, "max_rel_err": err}
+        if not ok and p2p:
+            if rank == 0:
+                print(f"P2P exchange check failed (rel err {err}); using NCCL", file=sys.stderr)
+            plan.close()
+            plan = L.Plan(L.FORWARD, nd, model.padded, w.space_order, w.nt, w.dt, w.h,
+                          src.npoints, rec.npoints, False, local, comm=comm)
+            plan.set_stream(stream.cuda_stream)
+            exchange = "nccl send/recv on a comm stream, overlapped with the interior sweep"
+            ok2, err2 = check_exchange(L, S, torch, dist, comm, rank, world, local, False)
+            exchange_check = {"exchange": "nccl", "ok": ok2, "max_rel_err": err2,
+                              "p2p_failed": {"ok": ok, "max_rel_err": err}}
 
     # Pinned host buffers in the reference's layout (fp64 grids, long idx).
     def pinned(shape, dtype):
@@ -446,7 +516,8 @@ def run_ours(args):
                 "ms_per_step": ms / args.steps, "higher_is_better": True,
                 "scaling": "strong" if (world > 1 and args.scaling == "strong") else "weak",
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "config": config_of(w, world, {"sweep": plan.info(), "exchange": exchange}),
+                "config": config_of(w, world, {"sweep": plan.info(), "exchange": exchange,
+                                               "exchange_check": exchange_check}),
                 "roofline": roof, "cpu_baseline": cb,
                 "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary}
         print(json.dumps(line))

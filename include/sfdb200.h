@@ -167,8 +167,15 @@ SFDB200_API int sfdb200_plan_ipc_import(sfdb200_plan* plan, const void* lower, c
  * upload (the sparse tables depend on the boundary items). */
 SFDB200_API int sfdb200_plan_peer_group(sfdb200_plan** plans, int n);
 /* The step-counter primitives of the P2P exchange on one device: a stream
- * writes a counter (cuStreamWriteValue32) and waits for it (poll kernel, GEQ). */
+ * writes a counter (cuStreamWriteValue32) and waits for it (poll kernel, GEQ);
+ * a counter that never arrives marks the exchange broken after the timeout. */
 SFDB200_API int sfdb200_p2p_selftest(int device);
+/* Waits for the plan's stream and reports a broken P2P exchange: a neighbour's
+ * step counter that did not arrive within SFDB200_P2P_TIMEOUT_MS (default
+ * 60000) makes the waits give up (no hang, no trap) and this call, like
+ * sfdb200_download, return SFDB200_ECUDA; the plan's results are invalid.
+ * SFDB200_OK otherwise (also for plans without the P2P exchange). */
+SFDB200_API int sfdb200_plan_check(sfdb200_plan* plan);
 /* Owned updated global planes of `rank`: an even split of [so/2, Pz - so/2). */
 SFDB200_API int sfdb200_slab(long padded_z, int space_order, int world, int rank, long* z_begin,
                              long* z_end);

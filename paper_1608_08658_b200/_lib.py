@@ -67,6 +67,7 @@ _SIGS = {
     "sfdb200_plan_ipc_import": (_i, [_P, _P, _P]),
     "sfdb200_plan_peer_group": (_i, [_P, _i]),
     "sfdb200_p2p_selftest": (_i, [_i]),
+    "sfdb200_plan_check": (_i, [_P]),
     "sfdb200_plan_create_dist": (_i, [_P, _P, _P]),
     "sfdb200_slab": (_i, [_L, _i, _i, _i, _lp, _lp]),
     "sfdb200_plan_slab": (_i, [_P, _lp, _lp, _lp]),
@@ -163,6 +164,10 @@ class Plan:
 
     def execute(self):
         check(lib().sfdb200_execute(self.handle))
+
+    def check(self):
+        """Waits for the plan's stream; raises if the P2P exchange timed out."""
+        check(lib().sfdb200_plan_check(self.handle))
 
     def download(self, arrays):
         check(lib().sfdb200_download(self.handle, argv_of(arrays)))

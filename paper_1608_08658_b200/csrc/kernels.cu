@@ -162,8 +162,14 @@ __global__ void inject_kernel(float* __restrict__ field, const long long* __rest
 // `value` (cyclic compare), sleeping between polls; a counter that never gets
 // there (a neighbour process died) traps after `timeout_ns` instead of hanging
 // the GPU.
+// A neighbour that never publishes (its process died, or the mapping is
+// wrong) sets the sticky `broken` flag after timeout_ns instead of trapping:
+// the context stays usable, every later wait returns at once, and the host
+// reports the failed exchange (p2p_check) rather than hanging or aborting.
 __global__ void wait_flags_kernel(const unsigned int* f0, const unsigned int* f1,
-                                  unsigned int value, unsigned long long timeout_ns) {
+                                  unsigned int value, unsigned long long timeout_ns,
+                                  unsigned int* broken) {
+    if (*reinterpret_cast<volatile unsigned int*>(broken)) return;
     unsigned long long t0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     for (const unsigned int* f : {f0, f1}) {
@@ -175,7 +181,10 @@ __global__ void wait_flags_kernel(const unsigned int* f0, const unsigned int* f1
             __nanosleep(200);
             unsigned long long t;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-            if (t - t0 > timeout_ns) __trap();
+            if (t - t0 > timeout_ns) {
+                atomicExch(broken, 1u);
+                return;
+            }
         }
     }
 }
@@ -452,8 +461,9 @@ cudaError_t launch_inject(float* field, const long long* off, const float* coef,
 }
 
 cudaError_t launch_wait_flags(const unsigned int* f0, const unsigned int* f1, unsigned int value,
-                              unsigned long long timeout_ns, cudaStream_t s) {
-    wait_flags_kernel<<<1, 1, 0, s>>>(f0, f1, value, timeout_ns);
+                              unsigned long long timeout_ns, unsigned int* broken,
+                              cudaStream_t s) {
+    wait_flags_kernel<<<1, 1, 0, s>>>(f0, f1, value, timeout_ns, broken);
     return cudaGetLastError();
 }
 

@@ -243,9 +243,11 @@ cudaError_t launch_inject(float* field, const long long* off, const float* coef,
                           const float* row, long n, float* grad, const float* ut,
                           const unsigned char* gmask, float nidt2, cudaStream_t s);
 // Waits (one thread, on the stream) until the P2P step counters f0, f1 (either
-// may be null) reach `value`; traps after timeout_ns.
+// may be null) reach `value`; after timeout_ns it sets *broken (sticky: later
+// waits return at once) and returns.
 cudaError_t launch_wait_flags(const unsigned int* f0, const unsigned int* f1, unsigned int value,
-                              unsigned long long timeout_ns, cudaStream_t s);
+                              unsigned long long timeout_ns, unsigned int* broken,
+                              cudaStream_t s);
 // pt (optional): output index of each sampled point (a subset of the set).
 cudaError_t launch_sample(const float* field, const long long* off, const float* w,
                           const int* pt, float* row, long npoints, int corners, cudaStream_t s);

@@ -156,12 +156,29 @@ void p2p_signal(sfdb200_plan& p, unsigned int value, cudaStream_t s) {
 }
 
 // A one-thread kernel rather than cuStreamWaitValue32: a neighbour that never
-// publishes (its process died) ends in a trap after 60 s instead of a hung GPU.
+// publishes (its process died, its mapping is wrong) marks the plan's exchange
+// broken after SFDB200_P2P_TIMEOUT_MS (default 60 s) instead of hanging the
+// GPU; the run then completes with invalid values and p2p_check reports it.
 void p2p_wait(sfdb200_plan& p, unsigned int value, cudaStream_t s) {
+    static const unsigned long long timeout_ns =
+        1000000ull * static_cast<unsigned long long>(env_int("SFDB200_P2P_TIMEOUT_MS", 60000));
     const unsigned int* f0 = p.peer_flags[0] ? p.flags + 0 : nullptr;  // written by side 0
     const unsigned int* f1 = p.peer_flags[1] ? p.flags + 1 : nullptr;  // written by side 1
     if (!f0 && !f1) return;
-    ck(launch_wait_flags(f0, f1, value, 60ull * 1000000000ull, s), "P2P wait");
+    ck(launch_wait_flags(f0, f1, value, timeout_ns, p.flags + kBrokenFlag, s), "P2P wait");
+}
+
+void p2p_check(sfdb200_plan& p) {
+    if (!p.flags || !p.p2p_sync) return;
+    unsigned int broken = 0;
+    ck(cudaMemcpyAsync(&broken, p.flags + kBrokenFlag, sizeof broken, cudaMemcpyDeviceToHost,
+                       p.stream),
+       "D2H");
+    ck(cudaStreamSynchronize(p.stream), "P2P check");
+    if (broken)
+        fail(SFDB200_ECUDA,
+             "P2P exchange broken: a neighbour's step counter did not arrive in time (peer "
+             "process gone or its plan not imported); this plan's results are invalid");
 }
 
 void p2p_selftest(int device) {
@@ -177,13 +194,19 @@ void p2p_selftest(int device) {
         p2p_signal(p, v, s);
         p2p_wait(p, v, s);
     }
-    unsigned int h[2] = {0, 0};
+    // A counter that never arrives: the wait gives up after 2 ms and marks the
+    // exchange broken; the next wait (60 s budget) returns at once.
+    ck(launch_wait_flags(p.flags, nullptr, 100, 2000000ull, p.flags + kBrokenFlag, s), "wait");
+    ck(launch_wait_flags(p.flags, p.flags + 1, 200, 60000000000ull, p.flags + kBrokenFlag, s),
+       "wait");
+    unsigned int h[kBrokenFlag + 1] = {};
     ck(cudaMemcpyAsync(h, p.flags, sizeof h, cudaMemcpyDeviceToHost, s), "D2H");
     const cudaError_t e = cudaStreamSynchronize(s);
     cudaStreamDestroy(s);
     p.peer_flags[0] = p.peer_flags[1] = nullptr;
     ck(e, "stream counters");
     if (h[0] != 3 || h[1] != 3) fail(SFDB200_ECUDA, "stream counters: unexpected values");
+    if (h[kBrokenFlag] != 1) fail(SFDB200_ECUDA, "timed-out wait did not mark the exchange broken");
 }
 
 }  // namespace sfdb200

@@ -1195,6 +1195,7 @@ void do_download(sfdb200_plan& p, void** argv) {
     const sfdb200_desc& d = p.d;
     p.d2h = 0;
     ck(cudaStreamSynchronize(p.stream), "execute");
+    p2p_check(p);
     check_finite(p, p.field, p.rows * p.g.slot,
                  d.kind == SFDB200_FORWARD ? "the wavefield" : "the adjoint field");
     if (p.grad) check_finite(p, p.grad, p.g.slot, "the gradient");
@@ -1287,6 +1288,15 @@ int sfdb200_execute(sfdb200_plan* p) {
         if (!p) fail(SFDB200_EINVAL, "null plan");
         ck(cudaSetDevice(p->d.device), "cudaSetDevice");
         do_execute(*p);
+    });
+}
+
+int sfdb200_plan_check(sfdb200_plan* p) {
+    return guarded([&] {
+        if (!p) fail(SFDB200_EINVAL, "null plan");
+        ck(cudaSetDevice(p->d.device), "cudaSetDevice");
+        ck(cudaStreamSynchronize(p->stream), "execute");
+        p2p_check(*p);
     });
 }
 

@@ -272,6 +272,8 @@ void p2p_release(sfdb200_plan& p);
 // Stream memory operations on the step counters.
 void p2p_signal(sfdb200_plan& p, unsigned int value, cudaStream_t s);
 void p2p_wait(sfdb200_plan& p, unsigned int value, cudaStream_t s);
+void p2p_check(sfdb200_plan& p);  // syncs; fails if a P2P wait timed out
+constexpr int kBrokenFlag = 24;    // index in flags[] of the sticky timed-out flag
 void p2p_selftest(int device);
 
 // comm.cpp: NCCL (loaded at run time) for the ghost-plane exchange.

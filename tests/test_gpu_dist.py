@@ -122,8 +122,15 @@ def test_nccl_communicator_single_rank():
             p.run([u, model.m, model.damp, src.idx, src.w, wav, rec.idx, rec.w, tr])
             p.close()
             outs.append((u, tr))
-        comm.close()
         assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+        # bench.py's pre-timing check of the exchange (N > 1) runs its whole
+        # path here: the small problem over the communicator, the sum over
+        # ranks, the one-GPU comparison on rank 0.
+        import bench
+        from paper_1608_08658_b200 import seismic as S
+        ok, err = bench.check_exchange(L, S, torch, dist, comm, 0, 1, 0, False)
+        assert ok and err <= 1e-6, err
+        comm.close()
     finally:
         dist.destroy_process_group()
 
