@@ -9,6 +9,7 @@ timeout 900 python -m pytest tests -m gpu -q > $OUT/pytest_gpu.txt 2>&1
 for wl in cfg2 cfg1 cfg3 cfg4-so2 cfg4-so4 cfg4-so8 cfg4-so12 cfg4-so16; do
   timeout 1200 python bench.py --workload $wl > $OUT/bench_$wl.json 2> $OUT/bench_$wl.err
 done
+timeout 1500 python bench.py --workload cfg5 --steps 2 --warmup 3 --no-cpu --no-e2e > $OUT/bench_cfg5.json 2> $OUT/bench_cfg5.err
 timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > $OUT/bench_reference_cfg2.json 2> $OUT/bench_reference_cfg2.err
 # the autotuned cfg2 tiling, fixed below so no tuning launches precede the profiled ones
 set -- $(python -c "
