@@ -11,6 +11,8 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <atomic>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <thread>
@@ -132,6 +134,75 @@ void copy_d2h(sfdb200_plan& p, void* dst, const void* src, size_t bytes) {
         par_memcpy(static_cast<char*>(dst) + o, p.pin[b], n);
         if (k + 2 < chunks) issue(k + 2);
     }
+}
+
+// The reference's damping (build_damping, seismic.cpp:152-173) is
+// max(dz[z], dy[y], dx[x]), zero in the interior.  Candidate profiles are the
+// three lines through the smallest cells found from the grid centre (one
+// argmin per axis); the whole field is then compared with max(A[z], B[y],
+// C[x]) bit for bit, split over host threads, while the DMA of m runs.  When
+// the identity holds the lines ARE the per-axis minima the device check
+// extracts (a line through a cell where all three profiles are minimal is the
+// min profile of a separable field), so only the lines are uploaded.  Any
+// other field -- negative, NaN, perturbed cells, signed zeros on the lines, or
+// separable with its minima away from the centre lines (the argmin search
+// stops at ties) -- returns false and takes the device path.
+bool host_sep_damp(const double* d, long long Pz, long long Py, long long Px,
+                   std::vector<double>& prof) {
+    if (Pz < 1 || Py < 1 || Px < 1) return false;
+    auto at = [&](long long z, long long y, long long x) { return d[(z * Py + y) * Px + x]; };
+    auto argmin = [](long long n, auto&& f) {
+        long long k = 0;
+        for (long long i = 1; i < n; ++i)
+            if (f(i) < f(k)) k = i;
+        return k;
+    };
+    long long yc = Py / 2, xc = Px / 2;
+    const long long zc = argmin(Pz, [&](long long z) { return at(z, yc, xc); });
+    yc = argmin(Py, [&](long long y) { return at(zc, y, xc); });
+    xc = argmin(Px, [&](long long x) { return at(zc, yc, x); });
+    prof.resize(static_cast<size_t>(Pz + Py + Px));
+    double* A = prof.data();
+    double* B = A + Pz;
+    double* C = B + Py;
+    for (long long z = 0; z < Pz; ++z) A[z] = at(z, yc, xc);
+    for (long long y = 0; y < Py; ++y) B[y] = at(zc, y, xc);
+    for (long long x = 0; x < Px; ++x) C[x] = at(zc, yc, x);
+    for (const double v : prof)
+        if (!(v >= 0.0) || std::signbit(v)) return false;
+
+    const unsigned t = static_cast<unsigned>(
+        std::min<long long>(Pz, std::max(1u, std::thread::hardware_concurrency())));
+    std::atomic<bool> bad{false};
+    auto check = [&](long long z0, long long z1) {
+        for (long long z = z0; z < z1 && !bad.load(std::memory_order_relaxed); ++z)
+            for (long long y = 0; y < Py; ++y) {
+                const double rzy = std::max(A[z], B[y]);
+                const double* row = d + (z * Py + y) * Px;
+                bool ok = true;
+                for (long long x = 0; x < Px; ++x) {
+                    const double v = row[x];
+                    ok &= (v == std::max(rzy, C[x])) & (v >= 0.0);
+                }
+                if (!ok) {
+                    bad.store(true, std::memory_order_relaxed);
+                    return;
+                }
+            }
+    };
+    std::vector<std::thread> th;
+    const long long per = (Pz + t - 1) / t;
+    for (unsigned i = 1; i < t; ++i) {
+        const long long z0 = i * per;
+        if (z0 >= Pz) break;
+        th.emplace_back([=, &check] {
+            unbind_self();
+            check(z0, std::min(Pz, z0 + per));
+        });
+    }
+    check(0, std::min(Pz, per));
+    for (auto& x : th) x.join();
+    return !bad.load();
 }
 
 void release_pinned(sfdb200_plan& p) {

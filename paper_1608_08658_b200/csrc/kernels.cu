@@ -232,6 +232,28 @@ __global__ void coeffs_kernel(const double* __restrict__ m, const double* __rest
     c2[r * XP + x] = static_cast<float>(1.0 / (a + b));
 }
 
+// The same coefficients from m and host-checked separable damp profiles
+// (pz, py, px as doubles; hostio.cpp host_sep_damp): the damp value of every
+// cell is max(pz[z], py[y], px[x]), bit for bit the caller's (checked).
+__global__ void coeffs_sep_kernel(const double* __restrict__ m, const double* __restrict__ prof,
+                                  double dt, float* __restrict__ c1, float* __restrict__ c2,
+                                  long long cells, int Px, int XP, int Py, int Pz, int R) {
+    const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (i >= cells) return;
+    const long long r = i / Px, x = i - r * Px;
+    const long long z = r / Py, y = r - z * Py;
+    if (x < R || x >= Px - R || y < R || y >= Py - R) {
+        c1[r * XP + x] = 0.0f;
+        c2[r * XP + x] = 0.0f;
+        return;
+    }
+    const double dmp = fmax(fmax(prof[z], prof[Pz + y]), prof[Pz + Py + x]);
+    const double a = m[i] / (dt * dt);
+    const double b = dmp / (2.0 * dt);
+    c1[r * XP + x] = static_cast<float>((a - b) / (a + b));
+    c2[r * XP + x] = static_cast<float>(1.0 / (a + b));
+}
+
 // ---- separable damping profiles (see SweepArgs::ez) ----------------------
 // Non-negative doubles order like their bit patterns, so the per-axis minima
 // are 64-bit atomicMin on the bits; any other input fails the exact check.
@@ -485,6 +507,19 @@ cudaError_t launch_coeffs(const FieldGeom& g, const double* m, const double* dam
     const long long cells = static_cast<long long>(g.Pz) * g.Py * g.Px;
     coeffs_kernel<<<grid_for(cells, 256), 256, 0, s>>>(m, damp, dt, c1, c2, cells, g.Px, g.XP,
                                                         g.Py, g.ndim == 3 ? g.R : 0);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_coeffs_sep(const FieldGeom& g, const double* m, const double* prof, double dt,
+                              float* c1, float* c2, float* ez, float* ey, float* ex,
+                              cudaStream_t s) {
+    const long long cells = static_cast<long long>(g.Pz) * g.Py * g.Px;
+    coeffs_sep_kernel<<<grid_for(cells, 256), 256, 0, s>>>(m, prof, dt, c1, c2, cells, g.Px, g.XP,
+                                                            g.Py, g.Pz, g.R);
+    const auto* bits = reinterpret_cast<const unsigned long long*>(prof);
+    prof_out_kernel<<<grid_for(g.Pz, 256), 256, 0, s>>>(bits, g.Pz, dt, ez);
+    prof_out_kernel<<<grid_for(g.Py, 256), 256, 0, s>>>(bits + g.Pz, g.Py, dt, ey);
+    prof_out_kernel<<<grid_for(g.Px, 256), 256, 0, s>>>(bits + g.Pz + g.Py, g.Px, dt, ex);
     return cudaGetLastError();
 }
 

@@ -256,6 +256,11 @@ cudaError_t launch_sample(const float* field, const long long* off, const float*
 // fp32 pitched layout.
 cudaError_t launch_coeffs(const FieldGeom& g, const double* m, const double* damp, double dt,
                           float* c1, float* c2, cudaStream_t s);
+// 3-D, separable damping checked on the host: prof = the fp64 per-axis
+// profiles pz[Pz], py[Py], px[Px] (device memory); also writes e* as below.
+cudaError_t launch_coeffs_sep(const FieldGeom& g, const double* m, const double* prof, double dt,
+                              float* c1, float* c2, float* ez, float* ey, float* ex,
+                              cudaStream_t s);
 // Splits a dense fp64 damp field [Pz][Py][Px] into per-axis profiles
 // e*[i] = fp32(min-profile / dt) and sets *mismatch != 0 unless
 // damp == max(dz[z], dy[y], dx[x]) holds bit-exactly for every cell.

@@ -482,8 +482,25 @@ void do_upload(sfdb200_plan& p, void** argv) {
     p.h2d = 0;
     p.ensure_staging(static_cast<size_t>(2 * cells));
     copy_h2d(p, p.staging, m + off, static_cast<size_t>(cells) * 8);
-    copy_h2d(p, p.staging + cells, damp + off, static_cast<size_t>(cells) * 8);
-    ck(launch_coeffs(p.g, p.staging, p.staging + cells, d.dt, p.c1, p.c2, p.stream), "coeffs");
+    // Separable damping (3-D): checked on the host while m is in flight; then
+    // only its three profiles travel (cfg2: 325 MB less H2D per upload).
+    const bool sep_try = p.g.ndim == 3 && env_int("SFDB200_SEPDAMP", 1) != 0;
+    const bool host_sep = sep_try && env_int("SFDB200_SEPDAMP_HOST", 1) != 0 &&
+                          host_sep_damp(damp + off, p.g.Pz, p.g.Py, p.g.Px, p.hprof);
+    if (host_sep) {
+        auto* prof = reinterpret_cast<double*>(p.eprof_scratch);
+        ck(cudaMemcpyAsync(prof, p.hprof.data(), p.hprof.size() * 8, cudaMemcpyHostToDevice,
+                           p.stream),
+           "H2D");
+        float* ez = p.eprof;
+        ck(launch_coeffs_sep(p.g, p.staging, prof, d.dt, p.c1, p.c2, ez, ez + p.g.Pz,
+                             ez + p.g.Pz + p.g.Py, p.stream),
+           "coeffs");
+    } else {
+        copy_h2d(p, p.staging + cells, damp + off, static_cast<size_t>(cells) * 8);
+        ck(launch_coeffs(p.g, p.staging, p.staging + cells, d.dt, p.c1, p.c2, p.stream),
+           "coeffs");
+    }
     // Host work while the model is in flight: the sparse sets' data hashes
     // (the tables are rebuilt only when they change).
     unsigned long long hsrc = 0, hrec = 0;
@@ -499,8 +516,8 @@ void do_upload(sfdb200_plan& p, void** argv) {
             hrec = sparse_data_hash(p, p.rec.n, static_cast<const long*>(argv[6]),
                                     static_cast<const double*>(argv[7]), m);
     }
-    p.sep_damp = false;
-    if (p.g.ndim == 3 && env_int("SFDB200_SEPDAMP", 1)) {
+    p.sep_damp = host_sep;
+    if (sep_try && !host_sep) {
         float* ez = p.eprof;
         float* ey = ez + p.g.Pz;
         float* ex = ey + p.g.Py;
@@ -522,7 +539,7 @@ void do_upload(sfdb200_plan& p, void** argv) {
     p.base.ey = p.sep_damp ? p.eprof + p.g.Pz : nullptr;
     p.base.ex = p.sep_damp ? p.eprof + p.g.Pz + p.g.Py : nullptr;
     ck(cudaStreamSynchronize(p.stream), "coeffs");
-    p.h2d += 2 * cells * 8;
+    p.h2d += host_sep ? cells * 8 + static_cast<long long>(p.hprof.size()) * 8 : 2 * cells * 8;
 
     if (grad && p.ck_fwd) {  // history recomputed per segment from checkpoints
         const long rows = p.ck_fwd->ck_interval + 2;

@@ -164,6 +164,7 @@ struct sfdb200_plan {
     float* c2 = nullptr;
     float* eprof = nullptr;  // 3-D: damp/dt profiles ez[Pz], ey[Py], ex[Px] (SweepArgs::ez)
     unsigned long long* eprof_scratch = nullptr;
+    std::vector<double> hprof;  // host-checked damp profiles (upload source)
     bool sep_damp = false;   // the uploaded damp field is max-separable
     bool sep_layout = true;  // the tiling uses the separable stage layout (cfg.sep)
     // Uniform checkpointing (forward plans, 3-D): every ck_interval steps the
@@ -258,6 +259,10 @@ bool host_pinned(const void* ptr);
 void copy_h2d(sfdb200_plan& p, void* dst, const void* src, size_t bytes);
 void copy_d2h(sfdb200_plan& p, void* dst, const void* src, size_t bytes);
 void release_pinned(sfdb200_plan& p);
+// hostio.cpp: the damp field [Pz][Py][Px] is max(A[z], B[y], C[x]) bit for
+// bit (non-negative); prof = A, B, C (the per-axis minima).
+bool host_sep_damp(const double* damp, long long Pz, long long Py, long long Px,
+                   std::vector<double>& prof);
 
 // p2p.cpp: fused P2P ghost exchange.
 // Byte offset from my `row` to the neighbour's ghost copy of the planes I

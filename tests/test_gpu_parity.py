@@ -237,6 +237,49 @@ def test_damping_profiles_or_streamed_c1(kind):
     assert O.rel_l2(argv[0], uo) <= TOL and O.rel_l2(argv[8], ro) <= TOL
 
 
+@pytest.mark.parametrize("field", ["reference", "shifted"])
+def test_host_checked_damping_profiles_bitwise(field, monkeypatch):
+    """Separable damping checked on the host (only the three profiles are
+    uploaded, hostio.cpp host_sep_damp) gives the same bits as the device
+    check over the uploaded field.  A separable field whose per-axis minima
+    lie off the grid centre is declined by the host check and still found
+    separable by the device check."""
+    from paper_1608_08658_b200 import _lib as L
+    w = configs.cfg2(n=28, nt=122, nbpml=8, nrec_side=6)
+    model, src, rec = _setup(w)
+    damp = model.damp
+    if field == "shifted":
+        rng = np.random.default_rng(3)
+        pz, py, px = (rng.uniform(1e-4, 5e-2, n) for n in model.padded)
+        pz[5], py[-3], px[2] = 0.0, 0.0, 0.0
+        damp = np.maximum(np.maximum(pz[:, None, None], py[None, :, None]), px[None, None, :])
+        damp = np.ascontiguousarray(damp.reshape(-1))
+    outs = []
+    # one tiling for both runs (the fused sparse tables, uploaded too, depend on it)
+    monkeypatch.setenv("SFDB200_TILE", "4,2,4,1,1")
+    monkeypatch.setenv("SFDB200_ZCHUNKS", "2")
+    for host in ("1", "0"):
+        monkeypatch.setenv("SFDB200_SEPDAMP_HOST", host)
+        argv = [np.zeros((3, *model.padded)), model.m, damp, src.idx, src.w,
+                O._f64(w.wavelet), rec.idx, rec.w, np.zeros((w.nt, rec.npoints))]
+        p = L.Plan(L.FORWARD, 3, model.padded, w.space_order, w.nt, w.dt, w.h, src.npoints,
+                   rec.npoints, False, 0)
+        p.run(argv)
+        info, h2d = p.info(), p.h2d_bytes
+        p.close()
+        assert info["separable_damping"]
+        outs.append((argv[0], argv[8], h2d))
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+    cells = int(np.prod(model.padded))
+    # the host check takes the lines through the centre's per-axis minima; a
+    # field whose minima lie elsewhere is left to the device check (full upload)
+    saved = cells * 8 - sum(model.padded) * 8 if field == "reference" else 0
+    assert outs[1][2] - outs[0][2] == saved
+    uo, ro = O.forward(model.padded, w.space_order, w.h, w.dt, w.nt, model.m, damp,
+                       src.idx, src.w, w.wavelet, rec.idx, rec.w)
+    assert O.rel_l2(outs[0][0], uo) <= TOL and O.rel_l2(outs[0][1], ro) <= TOL
+
+
 def test_layout_flip_on_reupload():
     """One plan uploaded with separable, then non-separable, then separable
     damping re-tiles for the matching stage layout each time (sweep3d.cuh
