@@ -203,6 +203,12 @@ SFDB200_API int sfdb200_build_damping(int ndim, const long* padded, long nbpml, 
 SFDB200_API int sfdb200_locate_points(int ndim, const long* interior, double h, long nbpml,
                           int space_order, long npoints, const double* coords, long* idx,
                           double* w);
+/* The upload's host check: 1 when the 3-D damp field [Pz][Py][Px]
+ * equals max(prof[z], prof[Pz + y], prof[Pz + Py + x]) bit for bit with the
+ * profiles (Pz + Py + Px doubles, written) taken through the centre's per-axis
+ * minima, i.e. the reference's build_damping form; 0 otherwise (the device
+ * check over the uploaded field then decides); < 0 on bad arguments. */
+SFDB200_API int sfdb200_damp_separable(const double* damp, long Pz, long Py, long Px, double* prof);
 /* ricker (seismic.cpp:175-185) and critical_dt (seismic.cpp:187-193). */
 SFDB200_API int sfdb200_ricker(double f0, double t0, long nt, double dt, double* out);
 SFDB200_API double sfdb200_critical_dt(int ndim, double h, int space_order, double m_min);

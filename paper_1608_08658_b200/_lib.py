@@ -76,6 +76,7 @@ _SIGS = {
     "sfdb200_make_model": (_i, [_i, _lp, _D, _L, _i, _dp, _lp, _dp, _dp]),
     "sfdb200_build_damping": (_i, [_i, _lp, _L, _L, _D, _dp]),
     "sfdb200_locate_points": (_i, [_i, _lp, _D, _L, _i, _L, _dp, _lp, _dp]),
+    "sfdb200_damp_separable": (_i, [_dp, _L, _L, _L, _dp]),
     "sfdb200_ricker": (_i, [_D, _D, _L, _D, _dp]),
     "sfdb200_critical_dt": (_D, [_i, _D, _i, _D]),
     "sfdb200_last_error": (C.c_char_p, []),

@@ -218,3 +218,11 @@ void release_pinned(sfdb200_plan& p) {
 }
 
 }  // namespace sfdb200
+
+int sfdb200_damp_separable(const double* damp, long Pz, long Py, long Px, double* prof) {
+    if (!damp || !prof || Pz < 1 || Py < 1 || Px < 1) return SFDB200_EINVAL;
+    std::vector<double> p;
+    const bool sep = sfdb200::host_sep_damp(damp, Pz, Py, Px, p);
+    if (sep) std::memcpy(prof, p.data(), p.size() * sizeof(double));
+    return sep ? 1 : 0;
+}

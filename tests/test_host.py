@@ -191,3 +191,39 @@ def test_operators_fail_loudly_without_the_cuda_library(monkeypatch, tmp_path):
     if not torch.cuda.is_available():
         with pytest.raises(L.SfdError):
             S.forward(m, src, wav, rec, 12, dt, False)
+
+
+def test_host_separable_damping_check():
+    """The upload's host check (hostio.cpp host_sep_damp) accepts the
+    reference's build_damping fields (golden fixture) with profiles equal to
+    the per-axis minima, and declines fields the device check must decide."""
+    g = np.load(os.path.join(GOLD, "ref_3d_so8.npz"))
+    mdl = S.make_model(list(g["interior"]), float(g["h"]), int(g["nbpml"]), int(g["so"]),
+                       g["m_interior"])
+    pz, py, px = mdl.padded
+    d = np.ascontiguousarray(g["damp"], dtype=np.float64)
+
+    def check(field):
+        prof = np.full(pz + py + px, np.nan)
+        rc = L.lib().sfdb200_damp_separable(L.dptr(field), pz, py, px, L.dptr(prof))
+        assert rc in (0, 1)
+        return rc == 1, prof
+
+    ok, prof = check(d)
+    assert ok
+    cube = d.reshape(pz, py, px)
+    mins = np.concatenate([cube.min(axis=(1, 2)), cube.min(axis=(0, 2)), cube.min(axis=(0, 1))])
+    assert np.array_equal(prof, mins)
+    rebuilt = np.maximum(np.maximum(prof[:pz, None, None], prof[pz:pz + py][None, :, None]),
+                         prof[pz + py:][None, None, :])
+    assert np.array_equal(rebuilt.reshape(-1), d)
+    for bad in (1e-3, -1e-9, np.nan):  # perturbed, negative, non-finite cell
+        e = d.copy()
+        e[e.size // 2 + 5] = bad
+        assert not check(e)[0]
+    neg0 = d.copy()
+    neg0[(pz // 2 * py + py // 2) * px + px // 2] = -0.0  # equal to 0.0, as on the device
+    ok, prof0 = check(neg0)
+    assert ok and not np.signbit(prof0).any() and np.array_equal(prof0, prof)
+    assert L.lib().sfdb200_damp_separable(L.dptr(d), 0, py, px, L.dptr(prof)) == L.EINVAL
+
