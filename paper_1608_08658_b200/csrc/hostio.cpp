@@ -205,7 +205,42 @@ bool host_sep_damp(const double* d, long long Pz, long long Py, long long Px,
     return !bad.load();
 }
 
+namespace {
+struct HostCopy {
+    void* dst;
+    const void* src;
+    size_t n;
+};
+void CUDART_CB host_copy(void* arg) {  // a stream host function: no CUDA calls
+    auto* j = static_cast<HostCopy*>(arg);
+    par_memcpy(j->dst, j->src, j->n);
+    delete j;
+}
+}  // namespace
+
+void copy_d2h_stream_pageable(sfdb200_plan& p, void* dst, const void* src, size_t bytes,
+                              cudaStream_t s) {
+    for (int b = 0; b < 2; ++b)
+        if (!p.xpin[b]) ck(cudaHostAlloc(&p.xpin[b], kChunk, cudaHostAllocDefault), "cudaHostAlloc");
+    for (size_t o = 0; o < bytes; o += kChunk) {
+        const int b = p.xpin_next;
+        p.xpin_next ^= 1;
+        const size_t n = std::min(kChunk, bytes - o);
+        // chunk b's previous host function precedes this copy in stream order
+        ck(cudaMemcpyAsync(p.xpin[b], static_cast<const char*>(src) + o, n,
+                           cudaMemcpyDeviceToHost, s),
+           "D2H");
+        ck(cudaLaunchHostFunc(s, host_copy, new HostCopy{static_cast<char*>(dst) + o, p.xpin[b], n}),
+           "cudaLaunchHostFunc");
+    }
+}
+
 void release_pinned(sfdb200_plan& p) {
+    if (p.xstream && (p.xpin[0] || p.xpin[1])) cudaStreamSynchronize(p.xstream);
+    for (int b = 0; b < 2; ++b) {
+        if (p.xpin[b]) cudaFreeHost(p.xpin[b]);
+        p.xpin[b] = nullptr;
+    }
     for (int b = 0; b < 2; ++b) {
         if (p.pin_ev[b]) {
             cudaEventSynchronize(p.pin_ev[b]);

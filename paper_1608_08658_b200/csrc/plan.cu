@@ -976,8 +976,12 @@ void flush_rows(sfdb200_plan& p, long upto) {
     ck(cudaStreamWaitEvent(p.xstream, p.ev_flush, 0), "wait");
     const long long off = p.flushed * s.n;
     ck(launch_dense_to_f64(s.trace + off, p.xstaging + off, n, p.xstream), "convert");
-    ck(cudaMemcpyAsync(p.host_rec + off, p.xstaging + off, n * 8, cudaMemcpyDeviceToHost,
-                       p.xstream), "D2H");
+    if (p.host_rec_pinned)
+        ck(cudaMemcpyAsync(p.host_rec + off, p.xstaging + off, n * 8, cudaMemcpyDeviceToHost,
+                           p.xstream), "D2H");
+    else
+        copy_d2h_stream_pageable(p, p.host_rec + off, p.xstaging + off,
+                                 static_cast<size_t>(n) * 8, p.xstream);
     p.d2h += n * 8;
     p.flushed = upto;
 }
@@ -1107,10 +1111,11 @@ void do_execute(sfdb200_plan& p) {
     if (p.ck_interval) prepare_checkpoints(p);
     exec_begin(p);
     p.flushed = 0;
-    // (a pageable record is filled at download through the pinned staging
-    // instead: synchronous pageable copies mid-run would stall the launches)
+    // (a pageable record goes through pinned chunks drained by stream host
+    // functions: a synchronous pageable copy mid-run would stall the launches)
     const bool stream_out = p.host_rec && p.g.ndim == 3 && p.d.kind == SFDB200_FORWARD &&
-                            p.fused && !p.dist() && p.rec.n && host_pinned(p.host_rec);
+                            p.fused && !p.dist() && p.rec.n;
+    p.host_rec_pinned = stream_out && host_pinned(p.host_rec);
     if (stream_out && !p.xstream) {
         ck(cudaStreamCreateWithFlags(&p.xstream, cudaStreamNonBlocking), "cudaStreamCreate");
         ck(cudaEventCreateWithFlags(&p.ev_flush, cudaEventDisableTiming), "cudaEventCreate");

@@ -185,6 +185,9 @@ struct sfdb200_plan {
     size_t staging_elems = 0;
     // hostio.cpp: two pinned chunks staging copies of pageable caller buffers
     void* pin[2] = {nullptr, nullptr};
+    void* xpin[2] = {nullptr, nullptr};  // the same for the record streamed on xstream
+    int xpin_next = 0;
+    bool host_rec_pinned = false;
     cudaEvent_t pin_ev[2] = {nullptr, nullptr};
     unsigned long long* counter = nullptr;
     unsigned int* flag = nullptr;
@@ -259,6 +262,11 @@ bool host_pinned(const void* ptr);
 void copy_h2d(sfdb200_plan& p, void* dst, const void* src, size_t bytes);
 void copy_d2h(sfdb200_plan& p, void* dst, const void* src, size_t bytes);
 void release_pinned(sfdb200_plan& p);
+// Stream-ordered D2H into a pageable destination on stream s (the record
+// streamed during a run): through the plan's two xpin chunks, each drained by
+// a stream host function, so the caller's thread never blocks.
+void copy_d2h_stream_pageable(sfdb200_plan& p, void* dst, const void* src, size_t bytes,
+                              cudaStream_t s);
 // hostio.cpp: the damp field [Pz][Py][Px] is max(A[z], B[y], C[x]) bit for
 // bit (non-negative); prof = A, B, C (the per-axis minima).
 bool host_sep_damp(const double* damp, long long Pz, long long Py, long long Px,

@@ -280,6 +280,41 @@ def test_host_checked_damping_profiles_bitwise(field, monkeypatch):
     assert O.rel_l2(outs[0][0], uo) <= TOL and O.rel_l2(outs[0][1], ro) <= TOL
 
 
+def test_record_streamed_to_pinned_and_pageable_buffers():
+    """sfdb200_run streams finished receiver rows to the caller during the run:
+    straight into pinned buffers, through pinned chunks drained by stream host
+    functions into pageable ones (several chunks per flush here).  Both give
+    the same bits as the staged upload / execute / download path."""
+    import torch
+    from paper_1608_08658_b200 import _lib as L
+    w = configs.cfg2(n=64, nt=202, nbpml=8, nrec_side=256)  # 64 rows x 65,536 rec > 32 MB
+    model, src, rec = _setup(w)
+
+    def argv_for(alloc):
+        u, r = alloc((3, *model.padded)), alloc((w.nt, rec.npoints))
+        u[...] = 1.0  # overwritten (first touch) -- stale values must not leak
+        r[...] = 7.0
+        return [u, model.m, model.damp, src.idx, src.w, O._f64(w.wavelet), rec.idx, rec.w, r]
+
+    def pinned(shape):
+        return torch.empty(shape, dtype=torch.float64, pin_memory=True).numpy()
+
+    p = L.Plan(L.FORWARD, 3, model.padded, w.space_order, w.nt, w.dt, w.h, src.npoints,
+               rec.npoints, False, 0)
+    outs = []
+    for alloc in (np.empty, pinned):
+        a = argv_for(alloc)
+        p.run(a)
+        outs.append((a[0].copy(), a[8].copy()))
+    a = argv_for(np.empty)
+    p.upload(a)
+    p.execute()
+    p.download(a)
+    p.close()
+    for u, r in outs:
+        assert np.array_equal(u, a[0]) and np.array_equal(r, a[8])
+
+
 def test_layout_flip_on_reupload():
     """One plan uploaded with separable, then non-separable, then separable
     damping re-tiles for the matching stage layout each time (sweep3d.cuh
