@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <functional>
+#include <future>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -481,12 +482,22 @@ void do_upload(sfdb200_plan& p, void** argv) {
     const long long off = p.zoff * p.plane_cells();
     p.h2d = 0;
     p.ensure_staging(static_cast<size_t>(2 * cells));
-    copy_h2d(p, p.staging, m + off, static_cast<size_t>(cells) * 8);
-    // Separable damping (3-D): checked on the host while m is in flight; then
-    // only its three profiles travel (cfg2: 325 MB less H2D per upload).
+    // Separable damping (3-D): checked on the host while m is in flight (its
+    // DMA, or for a pageable m its staging by other host threads); then only
+    // its three profiles travel (cfg2: 325 MB less H2D per upload).
     const bool sep_try = p.g.ndim == 3 && env_int("SFDB200_SEPDAMP", 1) != 0;
-    const bool host_sep = sep_try && env_int("SFDB200_SEPDAMP_HOST", 1) != 0 &&
-                          host_sep_damp(damp + off, p.g.Pz, p.g.Py, p.g.Px, p.hprof);
+    std::future<bool> sep_check;
+    if (sep_try && env_int("SFDB200_SEPDAMP_HOST", 1) != 0)
+        sep_check = std::async(std::launch::async, [&] {
+            return host_sep_damp(damp + off, p.g.Pz, p.g.Py, p.g.Px, p.hprof);
+        });
+    try {
+        copy_h2d(p, p.staging, m + off, static_cast<size_t>(cells) * 8);
+    } catch (...) {
+        if (sep_check.valid()) sep_check.wait();
+        throw;
+    }
+    const bool host_sep = sep_check.valid() && sep_check.get();
     if (host_sep) {
         auto* prof = reinterpret_cast<double*>(p.eprof_scratch);
         ck(cudaMemcpyAsync(prof, p.hprof.data(), p.hprof.size() * 8, cudaMemcpyHostToDevice,
