@@ -34,6 +34,30 @@ def _problem(so=8):
     return w, model, src, rec, wav
 
 
+def _collide(pts):
+    """Whether two injection corners of the set share a cell (their fp32 atomics
+    then sum in a decomposition-dependent order)."""
+    nd = pts.idx.shape[1]
+    offs = [np.array([(c >> (nd - 1 - k)) & 1 for k in range(nd)]) for c in range(1 << nd)]
+    cells = [tuple(i + o) for i in pts.idx for o in offs]
+    return len(set(cells)) != len(cells)
+
+
+def _same(a, b, tol, collide):
+    """Bitwise equal to the one-GPU run when no injection corners collide
+    (SURVEY §8(e)), else within tol."""
+    return np.array_equal(a, b) if not collide else O.rel_l2(a, b) <= tol
+
+
+@pytest.fixture
+def one_tiling(monkeypatch):
+    """The one-GPU plan and the slab plans use one compiled sweep variant, so
+    the decomposition is the only difference between the runs."""
+    def pin(so):
+        monkeypatch.setenv("SFDB200_TILE", "4,2,4,1,1" if so <= 8 else "4,2,4,4,1")
+    return pin
+
+
 def _run_group(kind, w, model, src, rec, wav, world, resid=None, p2p=False):
     import torch
     stream = torch.cuda.Stream()
@@ -71,26 +95,28 @@ def _run_group(kind, w, model, src, rec, wav, world, resid=None, p2p=False):
 
 
 @pytest.mark.parametrize("world,p2p", [(2, False), (3, False), (2, True), (3, True)])
-def test_emulated_ranks_forward_matches_single_gpu(world, p2p):
+def test_emulated_ranks_forward_matches_single_gpu(world, p2p, one_tiling):
+    one_tiling(8)
     w, model, src, rec, wav = _problem()
     ref = S.forward(model, src, wav, rec, w.nt, w.dt, False)
     u, tr = _run_group(L.FORWARD, w, model, src, rec, wav, world, p2p=p2p)
-    assert O.rel_l2(u, ref.u) <= 1e-6
-    assert O.rel_l2(tr, ref.record.data) <= 1e-6
+    c = _collide(src)
+    assert _same(u, ref.u, 1e-6, c) and _same(tr, ref.record.data, 1e-6, c)
     uo, ro = O.forward(model.padded, w.space_order, w.h, w.dt, w.nt, model.m, model.damp,
                        src.idx, src.w, wav, rec.idx, rec.w)
     assert O.rel_l2(u, uo) <= 1e-5 and O.rel_l2(tr, ro) <= 1e-5
 
 
 @pytest.mark.parametrize("p2p", [False, True])
-def test_emulated_ranks_adjoint_so16(p2p):
+def test_emulated_ranks_adjoint_so16(p2p, one_tiling):
+    one_tiling(16)
     w, model, src, rec, wav = _problem(so=16)
     rng = np.random.default_rng(2)
     resid = O._f64(rng.standard_normal((w.nt, rec.npoints)).astype(np.float32))
     ref = S.adjoint(model, rec, S.ShotRecord(w.nt, w.dt, rec.npoints, resid), src, w.nt, w.dt)
     v, tr = _run_group(L.ADJOINT, w, model, src, rec, wav, 3, resid, p2p=p2p)
-    assert O.rel_l2(v, ref.v) <= 1e-6
-    assert O.rel_l2(tr, ref.src_samples.data) <= 1e-6
+    c = _collide(rec)  # the adjoint injects at the receivers
+    assert _same(v, ref.v, 1e-6, c) and _same(tr, ref.src_samples.data, 1e-6, c)
 
 
 def test_nccl_communicator_single_rank():
@@ -135,10 +161,11 @@ def test_nccl_communicator_single_rank():
         dist.destroy_process_group()
 
 
-def test_p2p_injection_in_sent_planes():
+def test_p2p_injection_in_sent_planes(one_tiling):
     """Sources whose corners lie in the planes the boundary sweeps send: the
     fused P2P exchange must mirror the injected values into the neighbour's
     ghost copy (launch_mirror); equal to the single-GPU run."""
+    one_tiling(8)
     w, model, src, rec, wav = _problem()
     R = w.space_order // 2
     pts = []
@@ -156,7 +183,8 @@ def test_p2p_injection_in_sent_planes():
     ref = S.forward(model, src, wav, rec, w.nt, w.dt, False)
     for world in (2, 3):
         u, tr = _run_group(L.FORWARD, w, model, src, rec, wav, world, p2p=True)
-        assert O.rel_l2(u, ref.u) <= 1e-6 and O.rel_l2(tr, ref.record.data) <= 1e-6, world
+        c = _collide(src)
+        assert _same(u, ref.u, 1e-6, c) and _same(tr, ref.record.data, 1e-6, c), world
 
 
 def test_ipc_export_blob():

@@ -1,0 +1,238 @@
+"""SURVEY §8(d) parity protocol at FULL step counts on the B200.
+
+Each BASELINE config runs with its full number of time steps on the reduced
+grid the survey fixes for the fp64 oracle:
+
+  cfg1  201^2 + 40, so 4, 1000 steps                (full size)
+  cfg2  128^3 + 40, so 8, 1000 steps, 128^2 carpet
+  cfg3   64^3 + 20, so 8, 800-step forward(save) -> objective -> gradient
+  cfg4  128^3 + 40, 200 steps, so in {2, 4, 8, 12, 16}
+  cfg5  192^3 + 40, so 16, 500 steps, 4 sources, 96^2 carpet; plus the
+        z-slab decomposition over 2 / 4 / 8 emulated ranks, bitwise equal to
+        the one-GPU run (no two injection corners collide in cfg5)
+
+The checker is the UNMODIFIED reference (oracle/_ref/libsfdref.so: its own
+JIT-compiled OpenMP C through sfd::seismic::forward/adjoint/gradient,
+proj/src/seismic.cpp:333-496) when it was built, else the C restatement
+(oracle/libsfdoracle.so, pinned to the reference at <= 1e-12 by
+tests/test_oracle.py).  Gate (BASELINE.json north_star): rel-L2 <= 1e-5 on
+the final three slots, the traces and grad; indices bit-exact.  Every
+achieved error is appended to gpurun_out/parity/protocol.jsonl (copied to
+profiles/ per round).
+"""
+import json
+import os
+import time
+
+import numpy as np
+import pytest
+
+import oracle_lib as O
+from paper_1608_08658_b200 import _lib as L
+from paper_1608_08658_b200 import configs, seismic as S
+
+TOL = 1e-5
+pytestmark = pytest.mark.gpu
+
+LOG = os.path.join(O.ROOT, "gpurun_out", "parity", "protocol.jsonl")
+
+
+def _log(case, **kv):
+    os.makedirs(os.path.dirname(LOG), exist_ok=True)
+    kv = {k: (float(v) if isinstance(v, (np.floating, float)) else v) for k, v in kv.items()}
+    with open(LOG, "a") as fh:
+        fh.write(json.dumps({"case": case, "checker": _checker(), **kv}) + "\n")
+
+
+def _checker():
+    return "reference (oracle/_ref)" if O.have_ref() else "C restatement (oracle/libsfdoracle.so)"
+
+
+def _setup(w):
+    model = S.make_model(w.interior, w.h, w.nbpml, w.space_order, w.m_interior)
+    src = S.locate_points(model, w.src_coords)
+    rec = S.locate_points(model, w.rec_coords)
+    return model, src, rec
+
+
+def _oracle_forward(w, model, src, rec, save=False):
+    """(u, record, checker seconds) from the reference when built, else the port."""
+    t0 = time.perf_counter()
+    if O.have_ref():
+        u, r, _ = O.ref_forward(w.interior, w.h, w.nbpml, w.space_order, w.m_interior,
+                                w.src_coords, w.wavelet, w.rec_coords, w.nt, w.dt, save=save)
+    else:
+        u, r = O.forward(model.padded, w.space_order, w.h, w.dt, w.nt, model.m, model.damp,
+                         src.idx, src.w, w.wavelet, rec.idx, rec.w, save=save)
+    return u, r, time.perf_counter() - t0
+
+
+def _oracle_gradient(w, model, rec, resid, hist):
+    if O.have_ref():
+        g, _ = O.ref_gradient(w.interior, w.h, w.nbpml, w.space_order, w.m_interior,
+                              w.rec_coords, resid, hist, w.nt, w.dt)
+        return g
+    g, _ = O.gradient(model.padded, w.space_order, w.h, w.dt, w.nt, model.m, model.damp, hist,
+                      rec.idx, rec.w, resid)
+    return g
+
+
+def _check_indices(w, model, src, rec):
+    """idx + fp64 weights bit-exact against the reference's locate_points."""
+    if not O.have_ref():
+        return
+    for pts, c in ((src, w.src_coords), (rec, w.rec_coords)):
+        if len(c) == 0:
+            continue
+        idx, wt = O.ref_locate(w.interior, w.h, w.nbpml, w.space_order, w.m_interior, c)
+        assert np.array_equal(pts.idx, idx) and np.array_equal(pts.w, wt)
+
+
+def _last_slots(u, nt):
+    """The three rolling slots in time order t = nt-3, nt-2, nt-1."""
+    return [u[t % 3] for t in (nt - 3, nt - 2, nt - 1)]
+
+
+def _forward_case(name, w):
+    model, src, rec = _setup(w)
+    _check_indices(w, model, src, rec)
+    t0 = time.perf_counter()
+    f = S.forward(model, src, w.wavelet, rec, w.nt, w.dt, False)
+    t_gpu = time.perf_counter() - t0
+    uo, ro, t_ora = _oracle_forward(w, model, src, rec)
+    errs = [O.rel_l2(a, b) for a, b in zip(_last_slots(f.u, w.nt), _last_slots(uo, w.nt))]
+    er = O.rel_l2(f.record.data, ro) if rec.npoints else 0.0
+    _log(name, padded=list(map(int, model.padded)), so=w.space_order, steps=w.nt - 2,
+         nsrc=src.npoints, nrec=rec.npoints, slot_rel_l2=errs, record_rel_l2=er,
+         gpu_call_s=t_gpu, checker_s=t_ora)
+    assert max(errs) <= TOL, (name, errs)
+    assert er <= TOL, (name, er)
+    assert np.all(f.record.data[:2] == 0)
+    return f, model, src, rec
+
+
+def test_protocol_cfg1_full():
+    _forward_case("cfg1 201^2+40 so4 1000 steps", configs.cfg1())
+
+
+def test_protocol_cfg2_128():
+    _forward_case("cfg2 128^3+40 so8 1000 steps",
+                  configs.cfg2(n=128, nt=1002, nbpml=40, nrec_side=128))
+
+
+@pytest.mark.parametrize("so", [2, 4, 8, 12, 16])
+def test_protocol_cfg4_128(so):
+    _forward_case(f"cfg4 128^3+40 so{so} 200 steps", configs.cfg4(so, n=128, nt=202, nbpml=40))
+
+
+def test_protocol_cfg3_64_fwi_gradient():
+    """forward(save) of the true model -> observed; forward(save) of the
+    background -> synthetic + history; objective; gradient.  Gated on the
+    operators with identical inputs (the reference API's contract: the
+    gradient takes the caller's residual and history), and the whole chain
+    kept on the device (fwi_gradient, full history and checkpointed) logged
+    against the checker's chain."""
+    w = configs.cfg3(n=64, nt=802, nbpml=20, nrec_side=64)
+    model_t, src, rec = _setup(w)
+    _check_indices(w, model_t, src, rec)
+    # observed data: the true model through both sides
+    ft = S.forward(model_t, src, w.wavelet, rec, w.nt, w.dt, False)
+    _, obs, _ = _oracle_forward(w, model_t, src, rec)
+    e_obs = O.rel_l2(ft.record.data, obs)
+    # background forward with the saved history
+    wb = configs.Workload(w.name + "-bg", 3, w.interior, w.space_order, w.nt, w.dt,
+                          w.extra["m_background"], w.wavelet, w.src_coords, w.rec_coords, w.h,
+                          w.nbpml, w.f0)
+    model, _, _ = _setup(wb)
+    fb = S.forward(model, src, wb.wavelet, rec, wb.nt, wb.dt, True)
+    hist, syn, _ = _oracle_forward(wb, model, src, rec, save=True)
+    e_syn = O.rel_l2(fb.record.data, syn)
+    e_hist = [O.rel_l2(fb.u[t], hist[t]) for t in (w.nt - 3, w.nt - 2, w.nt - 1)]
+    del fb
+    phi_o, resid_o = S.objective(S.ShotRecord(w.nt, w.dt, rec.npoints, syn),
+                                 S.ShotRecord(w.nt, w.dt, rec.npoints, obs), True)
+    g_o = _oracle_gradient(wb, model, rec, resid_o.data, hist)
+    # the gradient operator on identical inputs
+    t0 = time.perf_counter()
+    g = S.gradient(model, rec, resid_o, hist, w.nt, w.dt)
+    t_g = time.perf_counter() - t0
+    e_grad = O.rel_l2(g.grad, g_o)
+    del hist
+    # the device-resident chain against the checker's chain
+    obs_rec = S.ShotRecord(w.nt, w.dt, rec.npoints, obs)
+    chain = S.fwi_gradient(model, src, wb.wavelet, rec, obs_rec, w.nt, w.dt,
+                           checkpoint_interval=0)
+    ck = S.fwi_gradient(model, src, wb.wavelet, rec, obs_rec, w.nt, w.dt,
+                        checkpoint_interval=28)
+    e_chain = O.rel_l2(chain.grad, g_o)
+    e_chain_phi = abs(chain.phi - phi_o) / phi_o
+    e_ck = O.rel_l2(ck.grad, chain.grad)
+    _log("cfg3 64^3+20 so8 800-step fwd(save)->objective->gradient",
+         padded=list(map(int, model.padded)), steps=w.nt - 2, nrec=rec.npoints,
+         observed_record_rel_l2=e_obs, synthetic_record_rel_l2=e_syn, history_last3_rel_l2=e_hist,
+         gradient_op_rel_l2=e_grad, gradient_op_s=t_g, chain_grad_rel_l2=e_chain,
+         chain_phi_rel=e_chain_phi, checkpointed_vs_full_rel_l2=e_ck,
+         residual_norm_over_record_norm=float(np.linalg.norm(resid_o.data) /
+                                              np.linalg.norm(syn)))
+    assert e_obs <= TOL and e_syn <= TOL and max(e_hist) <= TOL
+    assert e_grad <= TOL
+    assert e_chain_phi <= 1e-4
+    assert e_ck <= 1e-6
+
+
+def _emulated_forward(w, model, src, rec, world):
+    """The z-slab decomposition over `world` emulated ranks on one GPU (the real
+    kernels, tables and fused peer stores; ghost planes delivered into each
+    other's rows), assembled on the host."""
+    import torch
+    stream = torch.cuda.Stream()
+    comms = [L.Comm.loopback(world, r, 0) for r in range(world)]
+    plans, outs = [], []
+    wav = O._f64(w.wavelet)
+    try:
+        for r in range(world):
+            p = L.Plan(L.FORWARD, 3, model.padded, w.space_order, w.nt, w.dt, w.h, src.npoints,
+                       rec.npoints, False, 0, comm=comms[r])
+            p.set_stream(stream.cuda_stream)
+            field = np.zeros((3, *model.padded))
+            tr = np.zeros((w.nt, rec.npoints))
+            plans.append(p)
+            outs.append(([field, model.m, model.damp, src.idx, src.w, wav, rec.idx, rec.w, tr],
+                         field, tr))
+        L.peer_group(plans)
+        for p, (argv, _, _) in zip(plans, outs):
+            p.upload(argv)
+        L.execute_group(plans)
+        field = np.zeros((3, *model.padded))
+        trace = np.zeros((w.nt, rec.npoints))
+        for p, (argv, f, tr) in zip(plans, outs):
+            p.download(argv)
+            field += f     # every plane / receiver has exactly one owner
+            trace += tr
+        return field, trace
+    finally:
+        for p in plans:
+            p.close()
+        for c in comms:
+            c.close()
+
+
+def test_protocol_cfg5_192_and_slabs(monkeypatch):
+    """cfg5 at 192^3 so 16 (500 steps, 4 sources) against the checker, then the
+    same problem z-slab-decomposed over 2 / 4 / 8 emulated ranks: bitwise equal
+    to the one-GPU run.  One tiling for every plan, so the only
+    difference between the runs is the decomposition."""
+    monkeypatch.setenv("SFDB200_TILE", "4,2,4,4,1")  # by,ny,stages,rot,pair
+    w = configs.cfg5(n=192, nt=502, nbpml=40, nrec_side=96)
+    f, model, src, rec = _forward_case("cfg5 192^3+40 so16 500 steps 4 src", w)
+    # no two injection corners share a cell (the bitwise precondition)
+    cells = [tuple(i + np.array([(c >> 2) & 1, (c >> 1) & 1, c & 1]))
+             for i in src.idx for c in range(8)]
+    assert len(set(cells)) == len(cells)
+    diffs = {}
+    for world in (2, 4, 8):
+        u, tr = _emulated_forward(w, model, src, rec, world)
+        diffs[world] = (float(np.abs(u - f.u).max()), float(np.abs(tr - f.record.data).max()))
+    _log("cfg5 192^3 so16 z slabs vs 1 GPU (emulated ranks)", max_abs_diff=diffs)
+    for world, (du, dt_) in diffs.items():
+        assert du == 0.0 and dt_ == 0.0, (world, du, dt_)
