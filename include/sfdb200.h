@@ -24,8 +24,10 @@
  * reference's runtime::run turns into RuntimeError (runtime.cpp:344-345).
  *
  * Semantics follow the generated kernel, including first-touch zeroing of the
- * written grids (codegen.cpp:464-492) and, for Gradient, the host-side row-2
- * term of seismic::gradient (seismic.cpp:468-490) so that `grad` is final.
+ * written grids (codegen.cpp:464-492); for Gradient, `grad` by default also
+ * holds the host-side row-2 term of seismic::gradient (seismic.cpp:468-490),
+ * i.e. it is final, unless desc.flags has SFDB200_F_GRAD_NO_ROW2 (then it is
+ * exactly what the generated Gradient kernel leaves for its caller).
  * Arithmetic is fp32 on the device (see DESIGN.md for the error budget).
  */
 #ifndef SFDB200_H
@@ -62,7 +64,16 @@ typedef struct sfdb200_desc {
     long nsrc, nrec;     /* sparse-set sizes (Gradient: nsrc ignored) */
     int save;            /* Forward only: u holds nt+1 history rows (seismic.hpp:91-93) */
     int device;          /* CUDA device ordinal */
+    int flags;           /* SFDB200_F_* (0: the operator-level semantics above) */
 } sfdb200_desc;
+
+/* Gradient: leave out the t = 2 term of the imaging condition, exactly as the
+ * reference's generated Gradient kernel does: its caller seismic::gradient
+ * adds grad -= v[2] u[2] / dt^2 over the updated region on the host
+ * (seismic.cpp:468-490).  The shim the JIT driver emits for a generated
+ * Gradient kernel sets it (bin/sfdb200-jit), so the
+ * drop-in `Gradient_call` returns what the reference kernel returns. */
+#define SFDB200_F_GRAD_NO_ROW2 1
 
 typedef struct sfdb200_plan sfdb200_plan;
 
@@ -176,6 +187,14 @@ SFDB200_API int sfdb200_p2p_selftest(int device);
  * sfdb200_download, return SFDB200_ECUDA; the plan's results are invalid.
  * SFDB200_OK otherwise (also for plans without the P2P exchange). */
 SFDB200_API int sfdb200_plan_check(sfdb200_plan* plan);
+/* Aborts the P2P exchange now (not in stream order): sets this rank's and
+ * both neighbours' sticky broken flags, so waits already parked on any of them
+ * return, later sweeps skip their peer stores and step publications, and
+ * sfdb200_plan_check / sfdb200_download of every rank in the chain return
+ * SFDB200_ECUDA.  For a caller that hits an error on one rank mid-run (the
+ * neighbours fail within a step instead of after the P2P timeout).  Also
+ * works on the loopback peer group.  SFDB200_EINVAL without a P2P exchange. */
+SFDB200_API int sfdb200_plan_abort(sfdb200_plan* plan);
 /* Owned updated global planes of `rank`: an even split of [so/2, Pz - so/2). */
 SFDB200_API int sfdb200_slab(long padded_z, int space_order, int world, int rank, long* z_begin,
                              long* z_end);

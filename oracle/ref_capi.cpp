@@ -11,16 +11,23 @@
 //   sfd::seismic::forward           proj/src/seismic.cpp:333-380
 //   sfd::seismic::adjoint           proj/src/seismic.cpp:382-426
 //   sfd::seismic::gradient          proj/src/seismic.cpp:428-496
+//   sfd::seismic::build_*_ir + codegen::generate (seismic.cpp:241-331,
+//                                   codegen.cpp:579-629): the kernel source
+//   sfd::seismic::save/load_model, save/load_record (seismic.cpp:557-614),
+//   sfd::runtime::dump_grid (runtime.cpp:425-440): the file formats
 // Every entry returns 0 on success and 1 on a thrown exception; the message
 // is kept in a thread-local buffer (sfdref_last_error).
 
+#include <algorithm>
 #include <cstring>
 #include <locale>
 #include <exception>
 #include <string>
 #include <vector>
 
+#include "stencilfd/codegen.hpp"
 #include "stencilfd/fd.hpp"
+#include "stencilfd/runtime.hpp"
 #include "stencilfd/seismic.hpp"
 
 using namespace sfd;
@@ -174,6 +181,94 @@ int sfdref_gradient(int ndim, const long* interior, double h, long nbpml, int so
             seismic::gradient(m, rec, r, hist, nt, dt, config_of(portable));
         std::memcpy(grad_out, g.grad.data(), g.grad.size() * sizeof(double));
         if (seconds) *seconds = g.stats.seconds;
+    });
+}
+
+/// The C source codegen::generate emits for build_{forward,adjoint,gradient}_ir
+/// (kind 0 / 1 / 2) on this model; plan 0 = default CodegenPlan, 1 = all_off,
+/// 2 = fixed blocks of 4, 3 = blocking off.  Writes at most len bytes
+/// (NUL-terminated) and the full length to *need.
+int sfdref_generate(int kind, int ndim, const long* interior, double h, long nbpml, int so,
+                    const double* m_interior, long nsrc, long nrec, long nt, double dt, int save,
+                    int plan, char* out, long len, long* need) {
+    return guarded([&] {
+        const seismic::VelocityModel m = model_of(ndim, interior, h, nbpml, so, m_interior);
+        const lower::KernelIR ir = kind == 0 ? seismic::build_forward_ir(m, nsrc, nrec, nt, dt, save)
+                                   : kind == 1 ? seismic::build_adjoint_ir(m, nsrc, nrec, nt, dt)
+                                               : seismic::build_gradient_ir(m, nrec, nt, dt);
+        codegen::CodegenPlan p = plan == 1 ? codegen::CodegenPlan::all_off() : codegen::CodegenPlan{};
+        if (plan == 2) {
+            p.blocking = codegen::CodegenPlan::Blocking::Fixed;
+            p.fixed_blocks.assign(static_cast<size_t>(codegen::blocked_dims(ndim)), 4);
+        } else if (plan == 3) {
+            p.blocking = codegen::CodegenPlan::Blocking::Off;
+        }
+        const std::string src = codegen::generate(ir, p).source;
+        *need = static_cast<long>(src.size()) + 1;
+        if (out && len > 0) {
+            const size_t n = std::min(src.size(), static_cast<size_t>(len - 1));
+            std::memcpy(out, src.data(), n);
+            out[n] = 0;
+        }
+    });
+}
+
+/// save_model of make_model(interior, h, nbpml, so, m_interior).
+int sfdref_save_model(int ndim, const long* interior, double h, long nbpml, int so,
+                      const double* m_interior, const char* prefix) {
+    return guarded([&] {
+        seismic::save_model(model_of(ndim, interior, h, nbpml, so, m_interior), prefix);
+    });
+}
+
+/// load_model(prefix, so): ndim, interior, h, nbpml and the padded m / damp
+/// (pass null m_out to query the shape first).
+int sfdref_load_model(const char* prefix, int so, int* ndim, long* interior, double* h,
+                      long* nbpml, long* padded, double* m_out, double* damp_out) {
+    return guarded([&] {
+        const seismic::VelocityModel m = seismic::load_model(prefix, so);
+        *ndim = m.ndim();
+        for (int d = 0; d < m.ndim(); ++d) {
+            interior[d] = m.interior[static_cast<size_t>(d)];
+            padded[d] = m.padded[static_cast<size_t>(d)];
+        }
+        *h = m.h;
+        *nbpml = m.nbpml;
+        if (m_out) std::memcpy(m_out, m.m.data(), m.m.size() * sizeof(double));
+        if (damp_out) std::memcpy(damp_out, m.damp.data(), m.damp.size() * sizeof(double));
+    });
+}
+
+int sfdref_save_record(long nt, double dt, long npts, int ndim, const double* coords,
+                       const double* data, const char* prefix) {
+    return guarded([&] {
+        seismic::ShotRecord r = seismic::zero_record(nt, dt, npts);
+        r.data.assign(data, data + nt * npts);
+        seismic::save_record(r, coords_of(npts, ndim, coords), prefix);
+    });
+}
+
+/// load_record: nt, dt, npoints, coordinate width; data / coords when non-null.
+int sfdref_load_record(const char* prefix, long* nt, double* dt, long* npts, int* ndim,
+                       double* coords, double* data) {
+    return guarded([&] {
+        std::vector<std::vector<double>> c;
+        const seismic::ShotRecord r = seismic::load_record(prefix, &c);
+        *nt = r.nt;
+        *dt = r.dt;
+        *npts = r.npoints;
+        *ndim = c.empty() ? 0 : static_cast<int>(c[0].size());
+        if (coords)
+            for (size_t p = 0; p < c.size(); ++p)
+                std::memcpy(coords + p * c[p].size(), c[p].data(), c[p].size() * sizeof(double));
+        if (data) std::memcpy(data, r.data.data(), r.data.size() * sizeof(double));
+    });
+}
+
+int sfdref_dump_grid(const double* data, int nshape, const long* shape, long halo, long time_slots,
+                     const char* prefix) {
+    return guarded([&] {
+        runtime::dump_grid(data, std::vector<long>(shape, shape + nshape), halo, time_slots, prefix);
     });
 }
 

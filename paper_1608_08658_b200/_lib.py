@@ -22,7 +22,10 @@ class Desc(C.Structure):
     _fields_ = [("kind", C.c_int), ("ndim", C.c_int), ("padded", C.c_long * 3),
                 ("space_order", C.c_int), ("nt", C.c_long), ("dt", C.c_double),
                 ("h", C.c_double), ("nsrc", C.c_long), ("nrec", C.c_long), ("save", C.c_int),
-                ("device", C.c_int)]
+                ("device", C.c_int), ("flags", C.c_int)]
+
+
+F_GRAD_NO_ROW2 = 1  # SFDB200_F_GRAD_NO_ROW2
 
 
 class SfdError(RuntimeError):
@@ -68,6 +71,7 @@ _SIGS = {
     "sfdb200_plan_peer_group": (_i, [_P, _i]),
     "sfdb200_p2p_selftest": (_i, [_i]),
     "sfdb200_plan_check": (_i, [_P]),
+    "sfdb200_plan_abort": (_i, [_P]),
     "sfdb200_plan_create_dist": (_i, [_P, _P, _P]),
     "sfdb200_slab": (_i, [_L, _i, _i, _i, _lp, _lp]),
     "sfdb200_plan_slab": (_i, [_P, _lp, _lp, _lp]),
@@ -170,14 +174,20 @@ class Plan:
         """Waits for the plan's stream; raises if the P2P exchange timed out."""
         check(lib().sfdb200_plan_check(self.handle))
 
+    def abort(self):
+        """Marks the P2P exchange broken on this rank and its neighbours now."""
+        check(lib().sfdb200_plan_abort(self.handle))
+
     def download(self, arrays):
         check(lib().sfdb200_download(self.handle, argv_of(arrays)))
 
     def run(self, arrays):
+        self._keep = arrays  # the caller's buffers outlive every copy of the call
         check(lib().sfdb200_run(self.handle, argv_of(arrays)))
 
     def bind_history(self, forward_plan):
         check(lib().sfdb200_bind_history(self.handle, forward_plan.handle))
+        self._hist_fwd = forward_plan  # keep it alive while bound
 
     def set_checkpointing(self, interval):
         """Forward plans: keep restart rows every `interval` steps (0: off)."""

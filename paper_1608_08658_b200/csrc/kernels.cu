@@ -159,34 +159,61 @@ __global__ void inject_kernel(float* __restrict__ field, const long long* __rest
 }
 
 // P2P step counters (p2p.cpp): one thread polls until both counters reach
-// `value` (cyclic compare), sleeping between polls; a counter that never gets
-// there (a neighbour process died) traps after `timeout_ns` instead of hanging
-// the GPU.
-// A neighbour that never publishes (its process died, or the mapping is
-// wrong) sets the sticky `broken` flag after timeout_ns instead of trapping:
-// the context stays usable, every later wait returns at once, and the host
-// reports the failed exchange (p2p_check) rather than hanging or aborting.
+// `value` (cyclic compare), sleeping between polls.  A neighbour that never
+// publishes (its process died, it stalls, or the mapping is wrong) sets the
+// sticky `broken` flag after timeout_ns instead of trapping, and the flag is
+// also written into both neighbours' broken flags (pb0, pb1, through their IPC
+// mappings): every rank of the chain then stops its peer stores and step
+// publications (the sweep checks the flag) and its waits return at once, so
+// no rank runs ahead into ghost rows a neighbour still reads, and every
+// rank's p2p_check / download reports the failed exchange.
+__device__ __forceinline__ unsigned int ld_acquire_sys(const unsigned int* f) {
+    unsigned int v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+    return v;
+}
+
 __global__ void wait_flags_kernel(const unsigned int* f0, const unsigned int* f1,
                                   unsigned int value, unsigned long long timeout_ns,
-                                  unsigned int* broken) {
-    if (*reinterpret_cast<volatile unsigned int*>(broken)) return;
+                                  unsigned int* broken, unsigned int* pb0, unsigned int* pb1) {
+    auto poison = [&] {
+        atomicExch(broken, 1u);
+        __threadfence_system();
+        for (unsigned int* pb : {pb0, pb1})
+            if (pb) asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(pb), "r"(1u) : "memory");
+    };
+    if (ld_acquire_sys(broken)) {
+        poison();
+        return;
+    }
     unsigned long long t0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     for (const unsigned int* f : {f0, f1}) {
         if (!f) continue;
         for (;;) {
-            unsigned int v;
-            asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
-            if (static_cast<int>(v - value) >= 0) break;
+            if (static_cast<int>(ld_acquire_sys(f) - value) >= 0) break;
             __nanosleep(200);
             unsigned long long t;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-            if (t - t0 > timeout_ns) {
-                atomicExch(broken, 1u);
+            if (t - t0 > timeout_ns || ld_acquire_sys(broken)) {
+                poison();
                 return;
             }
         }
     }
+}
+
+// grad += v2 u2 / dt^2 over the updated region [R, P - R) of every dim
+// (plan.cu grad_row2_fixup: takes the t = 2 term back out of the gradient).
+__global__ void grad_row2_kernel(float* __restrict__ grad, const float* __restrict__ v2,
+                                 const float* __restrict__ u2, float idt2, FieldGeom g) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y;
+    const int z = blockIdx.z;
+    if (x < g.R || x >= g.Px - g.R || z < g.R || z >= g.Pz - g.R) return;
+    if (g.ndim == 3 && (y < g.R || y >= g.Py - g.R)) return;
+    const long long c = z * g.pz + y * g.py + x;
+    grad[c] = fmaf(v2[c] * u2[c], idt2, grad[c]);
 }
 
 template <int C>
@@ -482,10 +509,19 @@ cudaError_t launch_inject(float* field, const long long* off, const float* coef,
     return cudaGetLastError();
 }
 
+cudaError_t launch_grad_row2(float* grad, const float* v2, const float* u2, float idt2,
+                             const FieldGeom& g, cudaStream_t s) {
+    const dim3 grid((g.Px + 127) / 128, g.Py, g.Pz);
+    grad_row2_kernel<<<grid, 128, 0, s>>>(grad, v2, u2, idt2, g);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_wait_flags(const unsigned int* f0, const unsigned int* f1, unsigned int value,
                               unsigned long long timeout_ns, unsigned int* broken,
+                              unsigned int* peer_broken0, unsigned int* peer_broken1,
                               cudaStream_t s) {
-    wait_flags_kernel<<<1, 1, 0, s>>>(f0, f1, value, timeout_ns, broken);
+    wait_flags_kernel<<<1, 1, 0, s>>>(f0, f1, value, timeout_ns, broken, peer_broken0,
+                                      peer_broken1);
     return cudaGetLastError();
 }
 

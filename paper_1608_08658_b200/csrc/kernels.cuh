@@ -93,6 +93,9 @@ struct SweepArgs {
     unsigned int done_target;
     unsigned int* sig[2];
     unsigned int sig_value;
+    // This rank's sticky broken flag (P2P with step counters): once set, the
+    // boundary items skip their peer stores and the step publication.
+    const unsigned int* broken;
 };
 
 struct SweepMaps {          // TMA descriptors (3-D only)
@@ -242,11 +245,17 @@ int loop2d_blocks_per_sm(int R, bool grad);
 cudaError_t launch_inject(float* field, const long long* off, const float* coef, const int* pt,
                           const float* row, long n, float* grad, const float* ut,
                           const unsigned char* gmask, float nidt2, cudaStream_t s);
+// grad += v2 u2 idt2 over the updated region (SFDB200_F_GRAD_NO_ROW2).
+cudaError_t launch_grad_row2(float* grad, const float* v2, const float* u2, float idt2,
+                             const FieldGeom& g, cudaStream_t s);
 // Waits (one thread, on the stream) until the P2P step counters f0, f1 (either
-// may be null) reach `value`; after timeout_ns it sets *broken (sticky: later
-// waits return at once) and returns.
+// may be null) reach `value`; after timeout_ns, or once *broken is set, it
+// sets *broken and the neighbours' flags peer_broken0/1 (either may be null;
+// sticky: later waits return at once, later sweeps skip their peer stores)
+// and returns.
 cudaError_t launch_wait_flags(const unsigned int* f0, const unsigned int* f1, unsigned int value,
                               unsigned long long timeout_ns, unsigned int* broken,
+                              unsigned int* peer_broken0, unsigned int* peer_broken1,
                               cudaStream_t s);
 // pt (optional): output index of each sampled point (a subset of the set).
 cudaError_t launch_sample(const float* field, const long long* off, const float* w,

@@ -21,6 +21,7 @@
 // (t - 2) % 3 ghosts), so there is no write-after-read hazard.
 #include <cuda.h>
 
+#include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <string>
@@ -165,11 +166,14 @@ void p2p_wait(sfdb200_plan& p, unsigned int value, cudaStream_t s) {
     const unsigned int* f0 = p.peer_flags[0] ? p.flags + 0 : nullptr;  // written by side 0
     const unsigned int* f1 = p.peer_flags[1] ? p.flags + 1 : nullptr;  // written by side 1
     if (!f0 && !f1) return;
-    ck(launch_wait_flags(f0, f1, value, timeout_ns, p.flags + kBrokenFlag, s), "P2P wait");
+    unsigned int* pb0 = p.peer_flags[0] ? p.peer_flags[0] + kBrokenFlag : nullptr;
+    unsigned int* pb1 = p.peer_flags[1] ? p.peer_flags[1] + kBrokenFlag : nullptr;
+    ck(launch_wait_flags(f0, f1, value, timeout_ns, p.flags + kBrokenFlag, pb0, pb1, s),
+       "P2P wait");
 }
 
 void p2p_check(sfdb200_plan& p) {
-    if (!p.flags || !p.p2p_sync) return;
+    if (!p.flags || !p.p2p) return;
     unsigned int broken = 0;
     ck(cudaMemcpyAsync(&broken, p.flags + kBrokenFlag, sizeof broken, cudaMemcpyDeviceToHost,
                        p.stream),
@@ -178,35 +182,84 @@ void p2p_check(sfdb200_plan& p) {
     if (broken)
         fail(SFDB200_ECUDA,
              "P2P exchange broken: a neighbour's step counter did not arrive in time (peer "
-             "process gone or its plan not imported); this plan's results are invalid");
+             "process gone, stalled or its plan not imported) or a rank aborted the exchange; "
+             "this plan's results are invalid");
+}
+
+// Marks the exchange broken on this rank and both neighbours now, not in
+// stream order: a wait kernel already polling on any of them returns, and
+// every later sweep skips its peer stores.  A separate non-blocking stream,
+// since the plan's stream may be parked in a wait.
+void p2p_abort(sfdb200_plan& p) {
+    if (!p.flags) fail(SFDB200_EINVAL, "abort: the plan has no P2P exchange");
+    cudaStream_t s;
+    ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
+    static const unsigned int one = 1;
+    cudaError_t e = cudaSuccess;
+    for (unsigned int* f : {p.flags, p.peer_flags[0], p.peer_flags[1]})
+        if (f && e == cudaSuccess)
+            e = cudaMemcpyAsync(f + kBrokenFlag, &one, sizeof one, cudaMemcpyHostToDevice, s);
+    const cudaError_t e2 = cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+    ck(e, "abort");
+    ck(e2, "abort");
 }
 
 void p2p_selftest(int device) {
     ck(cudaSetDevice(device), "cudaSetDevice");
-    sfdb200_plan p;  // a bare plan: its own counters stand in for a neighbour's
-    p.flags = dalloc<unsigned int>(64);
+    // Two bare plans on one device stand in for neighbouring ranks: A is the
+    // lower neighbour of B (A writes B's counter [0], B writes A's [1]).
+    sfdb200_plan a, b;
+    a.flags = dalloc<unsigned int>(64);
+    b.flags = dalloc<unsigned int>(64);
+    a.peer_flags[1] = b.flags;
+    b.peer_flags[0] = a.flags;
+    a.p2p = b.p2p = true;
     cudaStream_t s;
     ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
-    ck(cudaMemsetAsync(p.flags, 0, 64 * sizeof(unsigned int), s), "memset");
-    p.peer_flags[0] = p.flags;  // I am side 0's upper neighbour: I write its [1] ...
-    p.peer_flags[1] = p.flags;  // ... and side 1's lower neighbour: its [0]
+    ck(cudaMemsetAsync(a.flags, 0, 64 * sizeof(unsigned int), s), "memset");
+    ck(cudaMemsetAsync(b.flags, 0, 64 * sizeof(unsigned int), s), "memset");
     for (unsigned int v = 1; v <= 3; ++v) {
-        p2p_signal(p, v, s);
-        p2p_wait(p, v, s);
+        p2p_signal(a, v, s);
+        p2p_signal(b, v, s);
+        p2p_wait(a, v, s);
+        p2p_wait(b, v, s);
     }
-    // A counter that never arrives: the wait gives up after 2 ms and marks the
-    // exchange broken; the next wait (60 s budget) returns at once.
-    ck(launch_wait_flags(p.flags, nullptr, 100, 2000000ull, p.flags + kBrokenFlag, s), "wait");
-    ck(launch_wait_flags(p.flags, p.flags + 1, 200, 60000000000ull, p.flags + kBrokenFlag, s),
+    // B stalls (alive, but never publishes step 4): A's wait gives up after
+    // 2 ms, marks A broken and poisons B; B's next wait (60 s budget) then
+    // returns at once instead of timing out in turn.
+    const auto t0 = std::chrono::steady_clock::now();
+    ck(launch_wait_flags(a.flags + 1, nullptr, 4, 2000000ull, a.flags + kBrokenFlag, nullptr,
+                         b.flags + kBrokenFlag, s),
        "wait");
-    unsigned int h[kBrokenFlag + 1] = {};
-    ck(cudaMemcpyAsync(h, p.flags, sizeof h, cudaMemcpyDeviceToHost, s), "D2H");
+    ck(launch_wait_flags(b.flags, nullptr, 5, 60000000000ull, b.flags + kBrokenFlag,
+                         a.flags + kBrokenFlag, nullptr, s),
+       "wait");
+    unsigned int ha[kBrokenFlag + 1] = {}, hb[kBrokenFlag + 1] = {};
+    ck(cudaMemcpyAsync(ha, a.flags, sizeof ha, cudaMemcpyDeviceToHost, s), "D2H");
+    ck(cudaMemcpyAsync(hb, b.flags, sizeof hb, cudaMemcpyDeviceToHost, s), "D2H");
     const cudaError_t e = cudaStreamSynchronize(s);
+    const double secs =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     cudaStreamDestroy(s);
-    p.peer_flags[0] = p.peer_flags[1] = nullptr;
+    a.peer_flags[1] = b.peer_flags[0] = nullptr;
     ck(e, "stream counters");
-    if (h[0] != 3 || h[1] != 3) fail(SFDB200_ECUDA, "stream counters: unexpected values");
-    if (h[kBrokenFlag] != 1) fail(SFDB200_ECUDA, "timed-out wait did not mark the exchange broken");
+    if (ha[1] != 3 || hb[0] != 3) fail(SFDB200_ECUDA, "stream counters: unexpected values");
+    if (ha[kBrokenFlag] != 1) fail(SFDB200_ECUDA, "timed-out wait did not mark the exchange broken");
+    if (hb[kBrokenFlag] != 1) fail(SFDB200_ECUDA, "the timed-out rank did not poison its neighbour");
+    if (secs > 30.0) fail(SFDB200_ECUDA, "the poisoned neighbour's wait did not return at once");
+    // p2p_check reports it on both sides.
+    for (sfdb200_plan* q : {&a, &b}) {
+        ck(cudaStreamCreateWithFlags(&q->own_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+        q->stream = q->own_stream;
+        bool thrown = false;
+        try {
+            p2p_check(*q);
+        } catch (const Error&) {
+            thrown = true;
+        }
+        if (!thrown) fail(SFDB200_ECUDA, "p2p_check did not report the broken exchange");
+    }
 }
 
 }  // namespace sfdb200

@@ -62,6 +62,7 @@ sfdb200_plan::~sfdb200_plan() {
     cudaFree(xstaging);
     cudaFree(counter);
     if (ev_flush) cudaEventDestroy(ev_flush);
+    if (ev_done) cudaEventDestroy(ev_done);
     if (xstream) cudaStreamDestroy(xstream);
     for (cudaEvent_t e : events) cudaEventDestroy(e);
     if (ev_b) cudaEventDestroy(ev_b);
@@ -135,6 +136,7 @@ void validate(const sfdb200_desc& d) {
     if (d.nt < 0) fail(SFDB200_EINVAL, "nt must be non-negative");
     if (!(d.dt > 0) || !(d.h > 0)) fail(SFDB200_EINVAL, "dt and h must be positive");
     if (d.nsrc < 0 || d.nrec < 0) fail(SFDB200_EINVAL, "negative sparse-set size");
+    if (d.flags & ~SFDB200_F_GRAD_NO_ROW2) fail(SFDB200_EINVAL, "unknown descriptor flags");
 }
 
 // Compiled sweep variants worth timing for radius R, best-first (B200
@@ -478,6 +480,10 @@ void do_upload(sfdb200_plan& p, void** argv) {
     const double* m = static_cast<const double*>(argv[im]);
     const double* damp = static_cast<const double*>(argv[im + 1]);
     if (!m || !damp) fail(SFDB200_EINVAL, "null model buffer");
+    // (the autotune below sweeps over a bound forward plan's rows)
+    if (const sfdb200_plan* fwd = p.ck_fwd ? p.ck_fwd : p.hist_fwd)
+        if (fwd->ev_done && fwd->stream != p.stream)
+            ck(cudaStreamWaitEvent(p.stream, fwd->ev_done, 0), "wait");
     const long long cells = p.cells();
     const long long off = p.zoff * p.plane_cells();
     p.h2d = 0;
@@ -742,6 +748,7 @@ void phase_interior(sfdb200_plan& p, long i, StepState& st) {
             if (p.peer_flags[1]) c.sig[1] = p.peer_flags[1];      // I am its lower neighbour
             c.sig_value = st.flag_base + static_cast<unsigned int>(i) + 1;
         }
+        if (p.flags) c.broken = p.flags + kBrokenFlag;
     }
     if (p.fused && inj.f_tab) {
         c.inj_tab = inj.f_tab;
@@ -845,7 +852,23 @@ void refine_with_sparse(sfdb200_plan& p, const std::function<void()>& tables) {
     p.cands.clear();
 }
 
+// SFDB200_F_GRAD_NO_ROW2: the device loop sums the imaging condition over
+// t = 2 .. nt-1 (summation by parts); the reference's
+// generated Gradient kernel stops short of t = 2, which seismic::gradient
+// adds on the host (grad -= v[2] u[2] / dt^2, seismic.cpp:468-490), so that
+// term is taken back out here.  v[2] is row 2 % 3 = 2 of the field (final
+// after the last backward step), u[2] row 2 of the history / segment buffer.
+void grad_row2_fixup(sfdb200_plan& p) {
+    if (!p.grad_kind() || !(p.d.flags & SFDB200_F_GRAD_NO_ROW2) || p.steps() == 0) return;
+    const FieldGeom& g = p.g;
+    ck(launch_grad_row2(p.grad, p.field + 2 * g.slot, p.hist + 2 * g.slot,
+                        static_cast<float>(1.0 / (p.d.dt * p.d.dt)), g, p.stream),
+       "grad row 2");
+    ++p.launches;
+}
+
 void exec_end(sfdb200_plan& p, StepState& st) {
+    grad_row2_fixup(p);
     SparseDev* smp = sampled_nonempty(p);
     // The last row has no following sweep to be sampled in.
     if (p.fused && smp && st.prev_out && smp->s_base) {
@@ -961,6 +984,7 @@ void execute_2d(sfdb200_plan& p) {
     if (p.steps() == 0) return;
     if (p.nc2d) {
         execute_cluster2d(p);
+        grad_row2_fixup(p);
         return;
     }
     if (p.timing) ck(cudaEventRecord(p.events[0], p.stream), "event");
@@ -968,6 +992,7 @@ void execute_2d(sfdb200_plan& p) {
     if (p.timing) ck(cudaEventRecord(p.events[1], p.stream), "event");
     p.timed_launches = 1;
     p.launches = 1;
+    grad_row2_fixup(p);
 }
 
 // Forward run(): trace rows [p.flushed, upto) are final; convert and copy them
@@ -1112,7 +1137,25 @@ void do_execute_checkpointed(sfdb200_plan& p) {
     exec_end(p, st);
 }
 
+void do_execute_body(sfdb200_plan& p);
+
+// A Gradient plan bound to a Forward plan's device history or checkpoints
+// reads them on its own stream: it waits for the forward plan's last execute
+// (an event, no host sync), so execute(fwd); bind; run(grad) needs no
+// download in between.  Forward plans record that event when they finish.
 void do_execute(sfdb200_plan& p) {
+    const sfdb200_plan* fwd = p.ck_fwd ? p.ck_fwd : p.hist_fwd;
+    if (fwd && fwd->ev_done && fwd->stream != p.stream)
+        ck(cudaStreamWaitEvent(p.stream, fwd->ev_done, 0), "wait");
+    do_execute_body(p);
+    if (p.d.kind == SFDB200_FORWARD) {
+        if (!p.ev_done)
+            ck(cudaEventCreateWithFlags(&p.ev_done, cudaEventDisableTiming), "cudaEventCreate");
+        ck(cudaEventRecord(p.ev_done, p.stream), "event");
+    }
+}
+
+void do_execute_body(sfdb200_plan& p) {
     if (p.dist() && comm_loopback(p.comm))
         fail(SFDB200_EINVAL, "loopback ranks run through sfdb200_execute_group");
     if (p.ck_fwd) {
@@ -1266,9 +1309,9 @@ std::map<std::string, std::unique_ptr<CachedPlan>>& plan_cache() {
 
 std::string desc_key(const sfdb200_desc& d) {
     char buf[512];
-    std::snprintf(buf, sizeof buf, "%d|%d|%ld,%ld,%ld|%d|%ld|%a|%a|%ld|%ld|%d|%d", d.kind, d.ndim,
-                  d.padded[0], d.padded[1], d.padded[2], d.space_order, d.nt, d.dt, d.h, d.nsrc,
-                  d.nrec, d.save, d.device);
+    std::snprintf(buf, sizeof buf, "%d|%d|%ld,%ld,%ld|%d|%ld|%a|%a|%ld|%ld|%d|%d|%d", d.kind,
+                  d.ndim, d.padded[0], d.padded[1], d.padded[2], d.space_order, d.nt, d.dt, d.h,
+                  d.nsrc, d.nrec, d.save, d.device, d.flags);
     return buf;
 }
 
@@ -1353,19 +1396,25 @@ int sfdb200_run(sfdb200_plan* p, void** argv) {
         const auto t0 = now();
         do_upload(*p, argv);
         const auto t1 = now();
+        // Record rows stream into the caller's argv[8] on xstream during the
+        // run; whatever way this call ends (an error in execute, the P2P or
+        // finite checks of download), those copies are drained and the
+        // pointer dropped before returning, so nothing writes into the
+        // caller's buffer afterwards and no later execute() reuses it.
+        struct RecordStreamGuard {
+            sfdb200_plan& p;
+            ~RecordStreamGuard() {
+                if (p.xstream) cudaStreamSynchronize(p.xstream);
+                p.host_rec = nullptr;
+            }
+        } guard{*p};
         p->host_rec = p->d.kind == SFDB200_FORWARD ? static_cast<double*>(argv[8]) : nullptr;
         p->d2h = 0;
-        try {
-            do_execute(*p);
-        } catch (...) {
-            p->host_rec = nullptr;
-            throw;
-        }
+        do_execute(*p);
         const auto t2 = now();
         const long streamed = p->d2h;
         do_download(*p, argv);
         p->d2h += streamed;
-        p->host_rec = nullptr;
         const auto t3 = now();
         if (prof) {
             auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
@@ -1410,6 +1459,7 @@ int sfdb200_bind_history(sfdb200_plan* gp, const sfdb200_plan* fp) {
             fail(SFDB200_EINVAL, "history comes from a different problem");
         if (gp->own_hist) cudaFree(gp->hist);
         gp->ck_fwd = nullptr;
+        gp->hist_fwd = fp;
         gp->hist = fp->field;
         gp->hist_rows = fp->rows;
         gp->own_hist = false;
@@ -1449,6 +1499,7 @@ int sfdb200_bind_checkpoints(sfdb200_plan* gp, sfdb200_plan* fp) {
         gp->hist = nullptr;
         gp->hist_rows = 0;
         gp->own_hist = false;
+        gp->hist_fwd = nullptr;
         gp->ck_fwd = fp;
         gp->maps_ready = false;
     });
@@ -1573,10 +1624,19 @@ int sfdb200_plan_peer_group(sfdb200_plan** plans, int n) {
                 p.peer_field[side] = plans[q]->field;
                 p.peer_slot[side] = plans[q]->g.slot;
                 p.peer_pz[side] = plans[q]->g.Pz;
+                p.peer_flags[side] = plans[q]->flags;  // broken flags only (no counters)
             }
             p.p2p = true;
             p.p2p_sync = false;  // execute_group's lockstep phases order the steps
         }
+    });
+}
+
+int sfdb200_plan_abort(sfdb200_plan* p) {
+    return guarded([&] {
+        if (!p) fail(SFDB200_EINVAL, "null plan");
+        ck(cudaSetDevice(p->d.device), "cudaSetDevice");
+        p2p_abort(*p);
     });
 }
 

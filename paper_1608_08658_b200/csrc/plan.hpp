@@ -177,6 +177,11 @@ struct sfdb200_plan {
     // Gradient plans bound to a checkpointed forward plan: hist holds one
     // recomputed segment (ck_interval + 2 rows).
     sfdb200_plan* ck_fwd = nullptr;
+    // Gradient plans bound to a saved Forward plan's rows (sfdb200_bind_history).
+    const sfdb200_plan* hist_fwd = nullptr;
+    // Forward plans: recorded on `stream` at the end of every execute(); bound
+    // gradient plans wait for it before reading the history / checkpoints.
+    cudaEvent_t ev_done = nullptr;
     float* hist = nullptr;   // gradient: u history
     bool own_hist = false;
     float* grad = nullptr;
@@ -286,6 +291,7 @@ void p2p_release(sfdb200_plan& p);
 void p2p_signal(sfdb200_plan& p, unsigned int value, cudaStream_t s);
 void p2p_wait(sfdb200_plan& p, unsigned int value, cudaStream_t s);
 void p2p_check(sfdb200_plan& p);  // syncs; fails if a P2P wait timed out
+void p2p_abort(sfdb200_plan& p);  // marks this rank and its neighbours broken now
 constexpr int kBrokenFlag = 24;    // index in flags[] of the sticky timed-out flag
 void p2p_selftest(int device);
 

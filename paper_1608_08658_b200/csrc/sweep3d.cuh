@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <mutex>
 #include <utility>
 
 #include "kernels.cuh"
@@ -36,6 +37,19 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 
 __device__ __forceinline__ void named_barrier_sync(int id, int threads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
+// bar.red.or over the named barrier `id` (`threads` threads): returns, in every
+// participating thread, whether any of them passed pred = true.
+__device__ __forceinline__ bool named_barrier_or(int id, int threads, bool pred) {
+    unsigned int r;
+    asm volatile(
+        "{\n\t.reg .pred p, q;\n\tsetp.ne.u32 p, %1, 0;\n\t"
+        "barrier.cta.red.or.pred q, %2, %3, p;\n\tselp.u32 %0, 1, 0, q;\n\t}"
+        : "=r"(r)
+        : "r"(static_cast<unsigned int>(pred)), "r"(id), "r"(threads)
+        : "memory");
+    return r != 0;
 }
 
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
@@ -751,8 +765,13 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
         // injections, each thread re-sends the values it stored (read back
         // through L2) to the neighbour's ghost planes; the last boundary item
         // of the launch then publishes the step to the neighbours' counters.
-        if (bs >= 0) {
-            named_barrier_sync(1, NT);  // the injections (atomics) are done
+        // Nothing goes to the neighbours once the exchange is broken (a
+        // neighbour timed out): the flag is read by one thread and reduced
+        // over the consumer warps, so the whole CTA takes the same branch.
+        if (bs >= 0 &&
+            !named_barrier_or(1, NT, tid == 0 && a.broken &&
+                                         *reinterpret_cast<const volatile unsigned int*>(a.broken))) {
+            // (the barrier also orders the injections (atomics) before the re-send)
             const long long pd = a.pdelta[bs];
             const char* c = reinterpret_cast<const char*>(
                 a.out + static_cast<long long>(z0) * pz + static_cast<long long>(y0 + r0) * py + x);
@@ -836,31 +855,51 @@ cudaError_t launch3d_t(const FieldGeom& g, const SweepConfig& cfg, const SweepMa
                               g.py, g.pz);
 }
 
+constexpr int kMaxDevices = 64;
+
 template <int R, int BY, int NY, int S, bool GRAD, int MINB, int UN, bool SEP>
 cudaError_t launch3d_pair_t(const FieldGeom& g, const SweepConfig& cfg, const SweepMaps& m,
                             const SweepArgs& a, cudaStream_t s, int* occ) {
     auto kern = sweep3d_pair_kernel<R, BY, NY, S, GRAD, MINB, UN, SEP>;
     if (!occ && (a.ez != nullptr) != SEP) return cudaErrorInvalidValue;  // layout mismatch
     const size_t smem = sweep3d_smem_bytes(R, cfg, GRAD);
-    static int resident = 0, sms = 0;  // per instantiation: CTAs per SM at this smem size
-    static size_t resident_smem = 0;
-    if (occ || resident_smem != smem) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(smem));
-        if (e != cudaSuccess) return e;
-        int r = 0;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, kern, 32 * (BY + 1), smem);
-        if (e != cudaSuccess) return e;
-        if (occ) {
-            *occ = r;
-            return cudaSuccess;
+    // Per instantiation and device: CTAs per SM at this smem size (the
+    // max-smem attribute and the occupancy are per device; concurrent
+    // sfdb200_call threads share the cache under its mutex).
+    struct Occ {
+        std::mutex mu;
+        int resident[kMaxDevices] = {};
+        int sms[kMaxDevices] = {};
+        size_t smem[kMaxDevices] = {};
+    };
+    static Occ cache;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+    int resident = 0, sms = 0;
+    {
+        std::lock_guard<std::mutex> lk(cache.mu);
+        if (occ || cache.smem[dev] != smem) {
+            e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem));
+            if (e != cudaSuccess) return e;
+            int r = 0;
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, kern, 32 * (BY + 1), smem);
+            if (e != cudaSuccess) return e;
+            if (occ) {
+                *occ = r;
+                return cudaSuccess;
+            }
+            int n = 0;
+            if ((e = cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess)
+                return e;
+            cache.resident[dev] = r;
+            cache.sms[dev] = n;
+            cache.smem[dev] = smem;
         }
-        int dev = 0;
-        if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
-        if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess)
-            return e;
-        resident = r;
-        resident_smem = smem;
+        resident = cache.resident[dev];
+        sms = cache.sms[dev];
     }
     if (resident < 1) return cudaErrorInvalidConfiguration;
     const int nitems = cfg.tiles_x * cfg.tiles_y * cfg.zchunks + a.nbi;  // + P2P boundary tiles

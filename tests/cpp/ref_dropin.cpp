@@ -1,0 +1,222 @@
+// TEST INFRASTRUCTURE (links the unmodified reference, oracle/_ref/libsfdref.so).
+//
+// The B200 backend as a drop-in under the reference's own operator API: the
+// UNMODIFIED sfd::seismic::forward / adjoint / gradient (seismic.cpp:333-496)
+// and sfd::verify::adjoint_test (verify.cpp:123-177) run once with the
+// reference's generic preset (its own JIT-compiled OpenMP C: the oracle) and
+// once with sfdb200::stencilfd_preset (every generated kernel swapped for the
+// sfdb200_call shim by bin/sfdb200-jit inside runtime::compile_and_load,
+// runtime.cpp:177-250; bound by KernelArgs as seismic.cpp:363-368; timed by
+// runtime::run, runtime.cpp:335-353).  Gates: rel-L2 <= 1e-5 on every output
+// (SURVEY.md section 8(d)); the fp32 adjoint dot test <= 1e-5.  Also checks
+// that sfdb200::desc_of(KernelIR) equals the
+// descriptor the driver reads back from the generated source.
+//
+//   ref_dropin <repo root>      (prints one JSON line per check; rc 0 = all pass)
+
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <fstream>
+#include <locale>
+#include <string>
+#include <vector>
+
+#include "sfdb200/stencilfd_preset.hpp"
+#include "stencilfd/codegen.hpp"
+#include "stencilfd/seismic.hpp"
+#include "stencilfd/verify.hpp"
+
+using namespace sfd;
+
+namespace {
+
+int failures = 0;
+
+double rel_l2(const std::vector<double>& a, const std::vector<double>& b) {
+    if (a.size() != b.size()) return INFINITY;
+    double num = 0, den = 0;
+    for (size_t i = 0; i < a.size(); ++i) {
+        num += (a[i] - b[i]) * (a[i] - b[i]);
+        den += b[i] * b[i];
+    }
+    return den > 0 ? std::sqrt(num / den) : std::sqrt(num);
+}
+
+void gate(const std::string& what, double err, double tol) {
+    const bool ok = err <= tol;
+    if (!ok) ++failures;
+    std::printf("{\"check\": \"%s\", \"rel_l2\": %.3e, \"tol\": %.0e, \"ok\": %s}\n", what.c_str(), err,
+                tol, ok ? "true" : "false");
+    std::fflush(stdout);
+}
+
+std::string describe(const std::string& root, const codegen::GeneratedSource& src) {
+    const std::string path = std::string(std::getenv("STENCILFD_CACHE_DIR")) + "/describe_" + src.name + ".c";
+    std::ofstream(path) << src.source;
+    const std::string cmd = root + "/paper_1608_08658_b200/bin/sfdb200-jit --describe " + path;
+    FILE* f = popen(cmd.c_str(), "r");
+    std::string out;
+    char buf[512];
+    while (f && std::fgets(buf, sizeof buf, f)) out += buf;
+    if (f) pclose(f);
+    return out;
+}
+
+std::string json_of(const char* name, const sfdb200_desc& d) {
+    char buf[1024];
+    std::snprintf(buf, sizeof buf,
+                  "{\"name\": \"%s\", \"kind\": %d, \"ndim\": %d, \"padded\": [%ld, %ld, %ld], "
+                  "\"space_order\": %d, \"nt\": %ld, \"dt\": %.17g, \"h\": %.17g, \"nsrc\": %ld, "
+                  "\"nrec\": %ld, \"save\": %d, \"device\": %d, \"flags\": %d}\n",
+                  name, d.kind, d.ndim, d.padded[0], d.padded[1], d.padded[2], d.space_order, d.nt,
+                  d.dt, d.h, d.nsrc, d.nrec, d.save, d.device, d.flags);
+    return buf;
+}
+
+// The driver recovers dt and h from printed literals (<= a few ulp); compare
+// the integer fields exactly and dt / h to 1e-14.
+void check_desc(const std::string& root, const lower::KernelIR& ir, double dt, double h, bool save) {
+    const codegen::GeneratedSource src = codegen::generate(ir, codegen::CodegenPlan{});
+    sfdb200_desc d = sfdb200::desc_of(ir, dt, h, save);
+    const std::string got = describe(root, src);
+    // Parse the two numbers back out of the driver's JSON, then print it with ours.
+    auto num = [&](const std::string& key) {
+        const size_t at = got.find("\"" + key + "\": ");
+        return at == std::string::npos ? NAN : std::strtod(got.c_str() + at + key.size() + 4, nullptr);
+    };
+    const double gdt = num("dt"), gh = num("h");
+    sfdb200_desc e = d;
+    e.dt = gdt;
+    e.h = gh;
+    const bool same = got == json_of(src.name.c_str(), e) && std::fabs(gdt - dt) <= 1e-14 * dt &&
+                      std::fabs(gh - h) <= 1e-14 * h;
+    if (!same) ++failures;
+    std::printf("{\"check\": \"desc_of(%s) == sfdb200-jit --describe\", \"ok\": %s}\n", src.name.c_str(),
+                same ? "true" : "false");
+    if (!same) std::printf("# desc_of: %s# driver:  %s", json_of(src.name.c_str(), d).c_str(), got.c_str());
+}
+
+std::vector<double> slowness(const std::vector<long>& n, double vmin, double vmax) {
+    long cells = 1;
+    for (long e : n) cells *= e;
+    std::vector<double> m(static_cast<size_t>(cells));
+    const int nd = static_cast<int>(n.size());
+    for (long c = 0; c < cells; ++c) {
+        long r = c;
+        double s = 0;
+        std::vector<long> pos(static_cast<size_t>(nd));
+        for (int k = nd - 1; k >= 0; --k) {
+            pos[static_cast<size_t>(k)] = r % n[static_cast<size_t>(k)];
+            r /= n[static_cast<size_t>(k)];
+        }
+        const double z = static_cast<double>(pos[0]) / static_cast<double>(n[0] - 1);
+        for (int k = 1; k < nd; ++k) s += std::sin(0.37 * static_cast<double>(pos[static_cast<size_t>(k)]) + k);
+        const double v = vmin + (vmax - vmin) * (0.8 * z + 0.1 * (1.0 + s / (nd - 1 + 1e-9)));
+        m[static_cast<size_t>(c)] = 1.0 / (v * v);
+    }
+    return m;
+}
+
+void operators(const std::string& root, int ndim, int so, long nt) {
+    const std::vector<long> n = ndim == 3 ? std::vector<long>{30, 34, 28} : std::vector<long>{90, 101};
+    const double h = 10.0;
+    const long nbpml = ndim == 3 ? 8 : 20;
+    seismic::VelocityModel model = seismic::make_model(n, h, nbpml, so, slowness(n, 1500.0, 3000.0));
+    const double dt = 0.8 * seismic::critical_dt(model);
+    std::vector<std::vector<double>> src_c, rec_c;
+    const double sx = (n[ndim - 1] - 1) * h;
+    if (ndim == 3) {
+        src_c.push_back({25.0, 0.37 * (n[1] - 1) * h, 0.55 * sx});
+        src_c.push_back({103.0, 0.61 * (n[1] - 1) * h, 0.27 * sx});
+        for (int j = 0; j < 7; ++j)
+            for (int i = 0; i < 6; ++i)
+                rec_c.push_back({20.0, (j + 0.5) * (n[1] - 1) * h / 7, (i + 0.5) * sx / 6});
+    } else {
+        src_c.push_back({20.0, 0.5 * sx});
+        for (int i = 0; i <= 50; ++i) rec_c.push_back({20.0, i * sx / 50});
+    }
+    const seismic::SparsePoints src = seismic::locate_points(model, src_c);
+    const seismic::SparsePoints rec = seismic::locate_points(model, rec_c);
+    const std::vector<double> w = seismic::ricker(15.0, 1.0 / 15.0, nt, dt);
+    std::vector<double> trace(static_cast<size_t>(nt * src.npoints));
+    for (long t = 0; t < nt; ++t)
+        for (long p = 0; p < src.npoints; ++p)
+            trace[static_cast<size_t>(t * src.npoints + p)] = w[static_cast<size_t>(t)] * (1.0 + 0.5 * p);
+
+    seismic::RunConfig cpu;  // the reference's generic preset: its own OpenMP C
+    seismic::RunConfig gpu;
+    gpu.preset = sfdb200::stencilfd_preset(root);
+    const std::string tag = std::to_string(ndim) + "-D so " + std::to_string(so) + " nt " + std::to_string(nt);
+
+    check_desc(root, seismic::build_forward_ir(model, src.npoints, rec.npoints, nt, dt, true), dt, h, true);
+    check_desc(root, seismic::build_forward_ir(model, src.npoints, rec.npoints, nt, dt, false), dt, h, false);
+    check_desc(root, seismic::build_adjoint_ir(model, src.npoints, rec.npoints, nt, dt), dt, h, false);
+    check_desc(root, seismic::build_gradient_ir(model, rec.npoints, nt, dt), dt, h, false);
+
+    // forward (saved history and rolling slots)
+    const seismic::ForwardResult fc = seismic::forward(model, src, trace, rec, nt, dt, true, cpu);
+    const seismic::ForwardResult fg = seismic::forward(model, src, trace, rec, nt, dt, true, gpu);
+    gate("forward(save) u history, " + tag, rel_l2(fg.u, fc.u), 1e-5);
+    gate("forward(save) record, " + tag, rel_l2(fg.record.data, fc.record.data), 1e-5);
+    const seismic::ForwardResult rc = seismic::forward(model, src, trace, rec, nt, dt, false, cpu);
+    const seismic::ForwardResult rg = seismic::forward(model, src, trace, rec, nt, dt, false, gpu);
+    gate("forward u slots, " + tag, rel_l2(rg.u, rc.u), 1e-5);
+    gate("forward record, " + tag, rel_l2(rg.record.data, rc.record.data), 1e-5);
+
+    // residual against a perturbed model (objective(), seismic.cpp:498-510)
+    std::vector<double> m2 = slowness(n, 1520.0, 3050.0);
+    const seismic::VelocityModel truth = seismic::make_model(n, h, nbpml, so, m2);
+    const seismic::ForwardResult obs = seismic::forward(truth, src, trace, rec, nt, dt, false, cpu);
+    seismic::ShotRecord resid;
+    const double phi_c = seismic::objective(fc.record, obs.record, &resid);
+    const double phi_g = seismic::objective(fg.record, obs.record, nullptr);
+    gate("objective, " + tag, std::fabs(phi_g - phi_c) / std::fabs(phi_c), 1e-5);
+
+    const seismic::AdjointResult ac = seismic::adjoint(model, rec, resid, src, nt, dt, cpu);
+    const seismic::AdjointResult ag = seismic::adjoint(model, rec, resid, src, nt, dt, gpu);
+    gate("adjoint v slots, " + tag, rel_l2(ag.v, ac.v), 1e-5);
+    gate("adjoint source samples, " + tag, rel_l2(ag.src_samples.data, ac.src_samples.data), 1e-5);
+
+    const seismic::GradientResult gc = seismic::gradient(model, rec, resid, fc.u, nt, dt, cpu);
+    const seismic::GradientResult gg = seismic::gradient(model, rec, resid, fc.u, nt, dt, gpu);
+    gate("gradient, " + tag, rel_l2(gg.grad, gc.grad), 1e-5);
+    std::printf("{\"timing\": \"%s\", \"forward_s\": {\"reference\": %.4f, \"b200\": %.4f}, "
+                "\"gradient_s\": {\"reference\": %.4f, \"b200\": %.4f}}\n",
+                tag.c_str(), rc.stats.seconds, rg.stats.seconds, gc.stats.seconds, gg.stats.seconds);
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+    std::locale::global(std::locale::classic());
+    if (argc < 2) {
+        std::fprintf(stderr, "usage: ref_dropin <repo root>\n");
+        return 2;
+    }
+    const std::string root = argv[1];
+    try {
+        operators(root, 3, 8, 160);
+        operators(root, 3, 16, 90);
+        operators(root, 2, 4, 300);
+
+        // The reference's own verification through the B200 preset.
+        verify::AdjointConfig ac;
+        ac.run.preset = sfdb200::stencilfd_preset(root);
+        ac.nt = 400;
+        const verify::AdjointReport r = verify::adjoint_test(ac);
+        gate("verify::adjoint_test (" + r.descriptor + ")", r.rel_discrepancy, 1e-5);
+        verify::AdjointConfig a3 = ac;
+        a3.interior = {40, 44, 38};
+        a3.space_order = 8;
+        a3.nbpml = 8;
+        a3.nt = 200;
+        const verify::AdjointReport r3 = verify::adjoint_test(a3);
+        gate("verify::adjoint_test (" + r3.descriptor + ")", r3.rel_discrepancy, 1e-5);
+    } catch (const std::exception& e) {
+        std::printf("{\"error\": \"%s\"}\n", e.what());
+        return 1;
+    }
+    std::printf("{\"failures\": %d}\n", failures);
+    return failures ? 1 : 0;
+}

@@ -63,6 +63,13 @@ _REF_SIGS = {
                             _dp, _dp]),
     "sfdref_gradient": (_i, [_i, _lp, _D, _L, _i, _dp, _L, _dp, _dp, _dp, _L, _D, _i, _dp,
                              _dp]),
+    "sfdref_generate": (_i, [_i, _i, _lp, _D, _L, _i, _dp, _L, _L, _L, _D, _i, _i, C.c_char_p,
+                             _L, _lp]),
+    "sfdref_save_model": (_i, [_i, _lp, _D, _L, _i, _dp, C.c_char_p]),
+    "sfdref_load_model": (_i, [C.c_char_p, _i, C.POINTER(_i), _lp, _dp, _lp, _lp, _dp, _dp]),
+    "sfdref_save_record": (_i, [_L, _D, _L, _i, _dp, _dp, C.c_char_p]),
+    "sfdref_load_record": (_i, [C.c_char_p, _lp, _dp, _lp, C.POINTER(_i), _dp, _dp]),
+    "sfdref_dump_grid": (_i, [_dp, _i, _lp, _L, _L, C.c_char_p]),
 }
 
 
@@ -328,6 +335,66 @@ def ref_gradient(interior, h, nbpml, so, m_interior, rec_coords, residual, u_his
                                      _d(_f64(u_history).ravel()), C.c_long(nt), C.c_double(dt),
                                      int(portable), _d(grad), _d_ref(secs)))
     return grad.reshape(padded), secs.value
+
+
+def ref_generate(kind, interior, h, nbpml, so, m_interior, nsrc, nrec, nt, dt, save=False,
+                 plan=0):
+    """The kernel source the reference's codegen::generate emits (str)."""
+    interior = _i64(interior)
+    need = C.c_long()
+    args = [kind, len(interior), _l(interior), C.c_double(h), C.c_long(nbpml), so,
+            _d(_f64(m_interior).ravel()), C.c_long(nsrc), C.c_long(nrec), C.c_long(nt),
+            C.c_double(dt), int(save), int(plan)]
+    _check_ref(ref().sfdref_generate(*args, None, 0, C.byref(need)))
+    buf = C.create_string_buffer(need.value)
+    _check_ref(ref().sfdref_generate(*args, buf, need.value, C.byref(need)))
+    return buf.value.decode()
+
+
+def ref_save_model(prefix, interior, h, nbpml, so, m_interior):
+    interior = _i64(interior)
+    _check_ref(ref().sfdref_save_model(len(interior), _l(interior), C.c_double(h),
+                                       C.c_long(nbpml), so, _d(_f64(m_interior).ravel()),
+                                       str(prefix).encode()))
+
+
+def ref_load_model(prefix, so):
+    """(interior, h, nbpml, padded m, padded damp) as the reference loads them."""
+    nd, h, nbpml = C.c_int(), C.c_double(), C.c_long()
+    interior, padded = np.zeros(3, np.int64), np.zeros(3, np.int64)
+    args = [str(prefix).encode(), so, C.byref(nd), _l(interior), C.byref(h), C.byref(nbpml),
+            _l(padded)]
+    _check_ref(ref().sfdref_load_model(*args, None, None))
+    shape = tuple(int(x) for x in padded[:nd.value])
+    m, damp = np.zeros(shape), np.zeros(shape)
+    _check_ref(ref().sfdref_load_model(*args, _d(m), _d(damp)))
+    return interior[:nd.value].copy(), h.value, nbpml.value, m, damp
+
+
+def ref_save_record(prefix, data, dt, coords):
+    data = _f64(data)
+    coords = _f64(coords)
+    nt, n = data.shape
+    _check_ref(ref().sfdref_save_record(nt, C.c_double(dt), n, coords.shape[1], _d(coords),
+                                        _d(data), str(prefix).encode()))
+
+
+def ref_load_record(prefix):
+    """(data [nt][npoints], dt, coords [npoints][ndim]) as the reference loads them."""
+    nt, dt, n, nd = C.c_long(), C.c_double(), C.c_long(), C.c_int()
+    args = [str(prefix).encode(), C.byref(nt), C.byref(dt), C.byref(n), C.byref(nd)]
+    _check_ref(ref().sfdref_load_record(*args, None, None))
+    coords = np.zeros((n.value, nd.value))
+    data = np.zeros((nt.value, n.value))
+    _check_ref(ref().sfdref_load_record(*args, _d(coords), _d(data)))
+    return data, dt.value, coords
+
+
+def ref_dump_grid(prefix, data, halo, time_slots):
+    data = _f64(data)
+    shape = _i64(data.shape)
+    _check_ref(ref().sfdref_dump_grid(_d(data), len(shape), _l(shape), C.c_long(halo),
+                                      C.c_long(time_slots), str(prefix).encode()))
 
 
 def rel_l2(a, b):

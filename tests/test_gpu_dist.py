@@ -58,7 +58,7 @@ def one_tiling(monkeypatch):
     return pin
 
 
-def _run_group(kind, w, model, src, rec, wav, world, resid=None, p2p=False):
+def _run_group(kind, w, model, src, rec, wav, world, resid=None, p2p=False, abort=None):
     import torch
     stream = torch.cuda.Stream()
     comms = [L.Comm.loopback(world, r, 0) for r in range(world)]
@@ -80,7 +80,22 @@ def _run_group(kind, w, model, src, rec, wav, world, resid=None, p2p=False):
         L.peer_group(plans)
     for p, (argv, _, _) in zip(plans, outs):
         p.upload(argv)
+    if abort is not None:
+        plans[abort].abort()
     L.execute_group(plans)
+    if abort is not None:  # every rank of the chain reports the broken exchange
+        errors = []
+        for p, (argv, _, _) in zip(plans, outs):
+            try:
+                p.download(argv)
+                errors.append(None)
+            except L.SfdError as e:
+                errors.append(e.code)
+        for p in plans:
+            p.close()
+        for c in comms:
+            c.close()
+        return errors
     field = np.zeros((3, *model.padded))
     trace = 0
     for p, (argv, f, tr) in zip(plans, outs):
@@ -207,8 +222,10 @@ def test_ipc_export_blob():
 
 
 def test_p2p_step_counters():
-    """cuStreamWriteValue32 / cuStreamWaitValue32 as the P2P exchange uses them
-    (resolved through the driver entry points), on one device."""
+    """cuStreamWriteValue32 and the polling wait kernel as the P2P exchange uses
+    them, on one device; a neighbour that stalls (alive, never publishing) makes
+    the waiting rank time out AND poisons the staller, whose next wait returns at
+    once; p2p_check then fails on both sides."""
     L.check(L.lib().sfdb200_p2p_selftest(0))
 
 
@@ -269,3 +286,16 @@ def test_p2p_fused_launch_with_persistent_ctas():
         assert O.rel_l2(u, ref.u) <= 1e-6 and O.rel_l2(tr, ref.record.data) <= 1e-6
     finally:
         os.environ.pop("SFDB200_CTAS", None)
+
+
+@pytest.mark.parametrize("world,rank", [(2, 0), (3, 1), (3, 2)])
+def test_p2p_abort_fails_every_rank(world, rank):
+    """sfdb200_plan_abort on one rank of the fused P2P exchange: it and its
+    neighbours skip their peer stores, and every rank adjacent to the abort
+    reports SFDB200_ECUDA at download instead of returning stale ghost planes
+    as results."""
+    w, model, src, rec, wav = _problem()
+    errors = _run_group(L.FORWARD, w, model, src, rec, wav, world, p2p=True, abort=rank)
+    for r, e in enumerate(errors):
+        if abs(r - rank) <= 1:
+            assert e == L.ECUDA, (r, errors)
