@@ -232,6 +232,12 @@ SFDB200_API int sfdb200_damp_separable(const double* damp, long Pz, long Py, lon
 SFDB200_API int sfdb200_ricker(double f0, double t0, long nt, double dt, double* out);
 SFDB200_API double sfdb200_critical_dt(int ndim, double h, int space_order, double m_min);
 
+/* objective (seismic.cpp:498-510): *phi = 1/2 sum_i (syn[i] - obs[i])^2 in
+ * element order (bit-equal to the reference); residual (may be NULL) gets
+ * syn - obs.  n = nt * npoints. */
+SFDB200_API int sfdb200_objective(const double* syn, const double* obs, long n, double* residual,
+                                  double* phi);
+
 SFDB200_API const char* sfdb200_last_error(void);
 SFDB200_API const char* sfdb200_version(void);
 

@@ -213,6 +213,17 @@ int sfdref_generate(int kind, int ndim, const long* interior, double h, long nbp
     });
 }
 
+/// seismic::objective on two records of n samples (npoints = n, nt = 1).
+int sfdref_objective(const double* syn, const double* obs, long n, double* residual, double* phi) {
+    return guarded([&] {
+        seismic::ShotRecord a = seismic::zero_record(1, 1.0, n), b = a, r;
+        a.data.assign(syn, syn + n);
+        b.data.assign(obs, obs + n);
+        *phi = seismic::objective(a, b, residual ? &r : nullptr);
+        if (residual) std::memcpy(residual, r.data.data(), static_cast<size_t>(n) * sizeof(double));
+    });
+}
+
 /// save_model of make_model(interior, h, nbpml, so, m_interior).
 int sfdref_save_model(int ndim, const long* interior, double h, long nbpml, int so,
                       const double* m_interior, const char* prefix) {

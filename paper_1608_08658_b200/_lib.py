@@ -72,6 +72,7 @@ _SIGS = {
     "sfdb200_p2p_selftest": (_i, [_i]),
     "sfdb200_plan_check": (_i, [_P]),
     "sfdb200_plan_abort": (_i, [_P]),
+    "sfdb200_objective": (_i, [_dp, _dp, _L, _dp, _dp]),
     "sfdb200_plan_create_dist": (_i, [_P, _P, _P]),
     "sfdb200_slab": (_i, [_L, _i, _i, _i, _lp, _lp]),
     "sfdb200_plan_slab": (_i, [_P, _lp, _lp, _lp]),

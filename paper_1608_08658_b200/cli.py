@@ -150,19 +150,32 @@ def cmd_bench(patch, out):
     pts = plan.points_per_step * plan.steps
     sweeps = plan.steps if m.ndim() == 3 else 1
     dev_s = ms / 1e3 * (sweeps / max(1, n)) if m.ndim() == 3 else ms / 1e3
-    rows = [{"kernel": "Forward", "plan": "b200-device", "seconds": dev_s,
-             "gpts": pts / dev_s / 1e9, "bytes_per_point": 20, "gbps": 20 * pts / dev_s / 1e9,
-             "config": plan.info()},
-            {"kernel": "Forward", "plan": "b200-e2e", "seconds": e2e, "gpts": pts / e2e / 1e9,
-             "h2d_bytes": plan.h2d_bytes, "d2h_bytes": plan.d2h_bytes}]
+    info = plan.info()
+    bpp = int(info.get("bytes_per_point", 20))
+    # the device update's arithmetic per point: per
+    # radius k, 2 ndim - 1 neighbour adds, the centre term and the tap (FMA = 2);
+    # then u1 + c1 (u1 - u2) + c2 lap.
+    fpp = (m.space_order // 2) * (2 * m.ndim() + 2) + 5
+
+    def row(plan_name, seconds, **extra):
+        # the reference's roofline-row keys (verify.hpp:110-119, verify.cpp:380-392)
+        r = {"kernel": "Forward", "flops_per_point": fpp, "bytes_per_point": bpp,
+             "intensity": fpp / bpp, "seconds": seconds, "gflops": fpp * pts / seconds / 1e9,
+             "plan": plan_name, "blocks": [], "gpts": pts / seconds / 1e9}
+        r.update(extra)
+        return r
+
+    rows = [row("b200-device", dev_s, gbps=bpp * pts / dev_s / 1e9, config=info),
+            row("b200-e2e", e2e, h2d_bytes=plan.h2d_bytes, d2h_bytes=plan.d2h_bytes)]
     with open(os.path.join(out, "bench.jsonl"), "w") as fh:
         for r in rows:
             fh.write(json.dumps(r) + "\n")
     with open(os.path.join(out, "bench.csv"), "w", newline="") as fh:
         wr = csv.writer(fh)
-        wr.writerow(["kernel", "plan", "seconds", "gpts"])
+        wr.writerow(["kernel", "plan", "blocks", "seconds", "gflops", "intensity", "gpts"])
         for r in rows:
-            wr.writerow([r["kernel"], r["plan"], r["seconds"], r["gpts"]])
+            wr.writerow([r["kernel"], r["plan"], "", r["seconds"], r["gflops"], r["intensity"],
+                         r["gpts"]])
     write_summary(out, {"command": "bench", "passed": True, "rows": len(rows),
                         "seconds": e2e, "gpts": rows[0]["gpts"], "first_run_seconds": first})
     print(f"Forward: device {dev_s:.4f} s ({rows[0]['gpts']:.1f} Gpts/s), "

@@ -182,4 +182,19 @@ double sfdb200_critical_dt(int ndim, double h, int so, double m_min) {
     return 0.9 * 2.0 * h * std::sqrt(m_min / (static_cast<double>(ndim) * tap_sum));
 }
 
+// objective (seismic.cpp:498-510): Phi = 1/2 sum (syn - obs)^2, summed in
+// element order like the reference (compiled without contraction, so the
+// bits agree); residual (optional) = syn - obs.
+int sfdb200_objective(const double* syn, const double* obs, long n, double* residual, double* phi) {
+    if (n < 0 || !phi || (n > 0 && (!syn || !obs))) return SFDB200_EINVAL;
+    double acc = 0.0;
+    for (long i = 0; i < n; ++i) {
+        const double d = syn[i] - obs[i];
+        acc += d * d;
+        if (residual) residual[i] = d;
+    }
+    *phi = 0.5 * acc;
+    return SFDB200_OK;
+}
+
 }  // extern "C"

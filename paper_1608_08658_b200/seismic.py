@@ -17,6 +17,7 @@ Every kernel runs on the B200 through libsfdb200.so; there is no CPU path.
 """
 from __future__ import annotations
 
+import ctypes as C
 import json
 import time
 from dataclasses import dataclass, field
@@ -375,12 +376,17 @@ def objective(synthetic: ShotRecord, observed: ShotRecord, want_residual=False):
     b = np.asarray(observed.data, np.float64)
     if synthetic.nt != observed.nt or synthetic.npoints != observed.npoints or a.size != b.size:
         raise L.InvalidArgument(L.EINVAL, "records disagree in shape")
-    d = (a - b).reshape(a.shape)
-    phi = 0.0
-    for x in d.ravel():  # sequential order, as the reference accumulates
-        phi += x * x
-    phi *= 0.5
+    shape = a.shape
+    a = np.ascontiguousarray(a).ravel()
+    b = np.ascontiguousarray(b).ravel()
+    d = np.empty(a.size) if want_residual else None
+    phi = C.c_double()
+    # element order, as the reference accumulates (sfdb200_objective, host C)
+    L.check(L.lib().sfdb200_objective(L.dptr(a), L.dptr(b), a.size,
+                                      L.dptr(d) if d is not None else None, C.byref(phi)))
+    phi = phi.value
     if want_residual:
+        d = d.reshape(shape)
         return phi, ShotRecord(synthetic.nt, synthetic.dt, synthetic.npoints, d)
     return phi
 

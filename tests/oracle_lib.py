@@ -70,6 +70,7 @@ _REF_SIGS = {
     "sfdref_save_record": (_i, [_L, _D, _L, _i, _dp, _dp, C.c_char_p]),
     "sfdref_load_record": (_i, [C.c_char_p, _lp, _dp, _lp, C.POINTER(_i), _dp, _dp]),
     "sfdref_dump_grid": (_i, [_dp, _i, _lp, _L, _L, C.c_char_p]),
+    "sfdref_objective": (_i, [_dp, _dp, _L, _dp, _dp]),
 }
 
 
@@ -349,6 +350,14 @@ def ref_generate(kind, interior, h, nbpml, so, m_interior, nsrc, nrec, nt, dt, s
     buf = C.create_string_buffer(need.value)
     _check_ref(ref().sfdref_generate(*args, buf, need.value, C.byref(need)))
     return buf.value.decode()
+
+
+def ref_objective(syn, obs):
+    """(Phi, residual) from the reference's seismic::objective."""
+    syn, obs = _f64(syn).ravel(), _f64(obs).ravel()
+    res, phi = np.zeros(syn.size), C.c_double()
+    _check_ref(ref().sfdref_objective(_d(syn), _d(obs), syn.size, _d(res), C.byref(phi)))
+    return phi.value, res
 
 
 def ref_save_model(prefix, interior, h, nbpml, so, m_interior):

@@ -192,24 +192,6 @@ def test_reference_abi_call_with_argv():
                                     rec.idx, rec.w, rec_data])
 
 
-def test_cli_run_and_bench(tmp_path):
-    """The sfd-compatible driver end to end on the device."""
-    import json as _json
-    from paper_1608_08658_b200 import cli
-    out = tmp_path / "run"
-    assert cli.main(["--out", str(out), "--set", "interior=[24,20,22]", "--set", "nbpml=4",
-                     "--set", "time=0.1", "run"]) == 0
-    s = _json.load(open(out / "summary.json"))
-    assert s["passed"] and s["record_peak"] > 0
-    meta = _json.load(open(out / "wavefield.json"))
-    assert np.fromfile(out / "wavefield.bin").size == np.prod(meta["shape"])
-    out2 = tmp_path / "bench"
-    assert cli.main(["--out", str(out2), "--set", "interior=[24,20,22]", "--set", "nbpml=4",
-                     "--set", "time=0.1", "bench"]) == 0
-    rows = [_json.loads(x) for x in open(out2 / "bench.jsonl")]
-    assert rows[0]["gpts"] > 0 and rows[1]["plan"] == "b200-e2e"
-
-
 @pytest.mark.parametrize("kind", ["separable", "perturbed", "negative"])
 def test_damping_profiles_or_streamed_c1(kind):
     """The sweep forms c1 from per-axis damping profiles only when the damp
