@@ -1,17 +1,25 @@
 #!/usr/bin/env python
 """Benchmark of the damped acoustic stencil hot path (BASELINE.json metric:
-"Gpts/s (grid-point updates/sec) 3D acoustic so-8; % of HBM roofline").
+"Gpts/s (grid-point updates/sec) 3D acoustic so-8; % of HBM roofline; 1/2/4/8 GPU").
 
 One bench step = one full operator run (all nt-2 time steps) over one
 synthetic problem.  At N=1 the workload is BASELINE configs[1] (cfg2: 3-D
 forward, 256^3 + 40-point damping layer, so 8, 1000 steps, 65,536 receivers).
+At N>1 it is BASELINE configs[4] (cfg5: 1024^3 + 40-point layer, so 16, 500
+steps, 4 sources, 512^2 receivers) strong-scaled over z slabs, the north
+star's parallel-efficiency configuration; each rank generates and uploads
+only its slab.  `python bench.py --gpus N` launches the N ranks itself
+(torch.distributed.run) when it is not already running under one.
 
   value    Gpts/s with inputs resident in HBM (plan.execute() only), device-timed
            with CUDA events on the plan's stream, max over ranks
-  e2e      the same metric through the C ABI with pinned HOST fp64 buffers
-           (sfdb200_run: H2D + fp64->fp32, the run, fp32->fp64 + D2H)
-  roofline dominant kernel (the 3-D sweep): algorithmic bytes per launch
-           (20 B/pt forward, 32 B/pt gradient) / mean launch time
+  e2e      the same metric through the C ABI (sfdb200_run) with PAGEABLE host
+           fp64 buffers -- the reference hands its kernel std::vectors
+           (seismic.cpp:354-361) -- H2D + fp64->fp32, the run, fp32->fp64 + D2H;
+           e2e.pinned: the same with pinned buffers (N=1)
+  roofline dominant kernel (the 3-D sweep): algorithmic bytes per launch /
+           mean launch time; frac at the bytes the kernel needs (16 B/pt with
+           separable damping), frac_alg at SURVEY 8(d)'s 20 B/pt (32 gradient)
   cpu_baseline  the unmodified reference (oracle/_ref) on this host's cores,
            full grid, truncated step count
 
@@ -53,11 +61,15 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="cfg2",
-                    help="cfg1 | cfg2 | cfg3 (FWI gradient) | cfg4-so{2,4,8,12,16} | cfg5")
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
-                    help="N>1 with cfg2: weak = one cfg2 slab per GPU (default), "
+    ap.add_argument("--workload", default=None,
+                    help="cfg1 | cfg2 | cfg3 (FWI gradient) | cfg4-so{2,4,8,12,16} | cfg5 "
+                         "(default: cfg2 at N=1, cfg5 at N>1)")
+    ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
+                    help="N>1 with cfg2: weak = one cfg2 slab per GPU, "
                          "strong = the cfg2 grid split over the GPUs")
+    ap.add_argument("--measure-1gpu", action="store_true",
+                    help="N>1: rank 0 also times the same workload on one GPU "
+                         "(config.one_gpu) for the parallel efficiency")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--checkpoint", type=int, default=0,
                     help="cfg3: checkpoint interval k (0 = whole history in HBM)")
@@ -65,7 +77,12 @@ def parse():
     ap.add_argument("--cpu-steps", type=int, default=0, help="reference sample steps (0: auto)")
     ap.add_argument("--time-steps", type=int, default=0,
                     help="override the workload's time steps (profiling runs only)")
-    return ap.parse_args()
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "0"))
+    n = world or args.gpus
+    if args.workload is None:
+        args.workload = "cfg5" if n > 1 else "cfg2"
+    return args
 
 
 def make_workload(name, time_steps=0):
@@ -169,15 +186,22 @@ def measured_peak():
         return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
 
 
-def ncu_traffic(workload):
-    """dram bytes per sweep launch from the committed ncu --set full summary."""
+def ncu_traffic(workload, info, ndim):
+    """DRAM bytes per sweep launch from the committed ncu --set full capture of
+    THIS instantiation (template arguments + z chunks + grid) on this workload:
+    profiles/ncu_summary.json is keyed "<workload>|<instantiation>|z<zchunks>"
+    (tools/ncu_traffic.py writes it from the capture).  (None, why) when the
+    tiling the bench autotuned to has no capture."""
+    if ndim != 3:
+        return None, "2-D: L2 / shared-memory resident, no DRAM roofline"
+    key = f"{workload}|{info.get('instantiation')}|z{info.get('zchunks')}"
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(p) as fh:
-            d = json.load(fh)
-        return d.get(workload, {}).get("dram_bytes_per_launch")
+            e = json.load(fh)["captures"][key]
+        return e["dram_bytes_per_launch"], e["source"]
     except Exception:
-        return None
+        return None, f"no committed ncu capture of {key}"
 
 
 def cpu_baseline(w, steps_hint):
@@ -234,11 +258,15 @@ def run_reference(args):
     v = float(np.median(vals))
     cb["value"] = v
     line = {"metric": "Gpts/s (grid-point updates/sec) 3D acoustic so-8", "value": v,
-            "unit": "Gpts/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": cb["seconds"] * 1e3, "higher_is_better": True, "scaling": "weak",
+            "unit": "Gpts/s", "n_gpus": world, "gpus_used": 0,
+            "ranks_working": 1, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": cb["seconds"] * 1e3, "higher_is_better": True,
+            "scaling": "strong" if world > 1 and args.workload != "cfg2" else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
             "config": config_of(w, world, {"sample": cb["sample"],
-                                           "parallelism": f"reference CPU path, {cb['cores']} host threads"}),
+                                           "parallelism": f"reference CPU path on rank 0 of "
+                                                          f"{world}, {cb['cores']} host threads; "
+                                                          "no GPU"}),
             "cpu_baseline": cb,
             "e2e": {"value": v, "unit": "Gpts/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
@@ -309,6 +337,54 @@ def check_exchange(L, S, torch, dist, comm, rank, world, local, p2p):
     return bool(int(flag.item()) == 1 and e <= 1e-5), e
 
 
+def _pinned(torch, shape, fill=None):
+    t = torch.empty(shape, dtype=torch.float64, pin_memory=True).numpy()
+    if fill is not None:
+        t[...] = fill
+    return t
+
+
+def slab_problem(L, S, args, world, rank):
+    """cfg5 at N > 1: this rank's slab only.  The interior rows its planes
+    need are generated here (configs.cfg5_rows; the rescale range is
+    all-reduced), and the model arrays are GLOBAL-shaped but untouched outside
+    the rank's planes (np.zeros: pages that are never written are never
+    backed), so sfdb200_upload reads exactly its slab from them as it does
+    from a full model."""
+    import torch
+    import torch.distributed as dist
+    from paper_1608_08658_b200 import configs
+    n, nbpml, so = 1024, 40, 16
+    R, pad = so // 2, nbpml + so // 2
+    P = n + 2 * pad
+    zb, ze = L.slab(P, so, world, rank)
+    zoff, pz = zb - R, (ze - zb) + 2 * R  # local planes [zoff, zoff + pz) of the global grid
+    z0, z1 = max(0, zoff - pad), min(n, zoff + pz - pad)
+
+    def minmax(a, b):
+        t = torch.tensor([-a, b], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return -float(t[0]), float(t[1])
+
+    steps = args.time_steps
+    w = configs.cfg5_rows(z0, z1, minmax, n=n, nbpml=nbpml,
+                          nt=(steps + 2) if steps else 502)
+    w.wavelet = np.ascontiguousarray(w.wavelet.reshape(w.nt, -1))
+    mi = w.m_interior.reshape(z1 - z0, n, n)
+    dprof = S.build_damping([P], nbpml, R, w.h)  # the per-axis taper (seismic.cpp:152-173)
+    m = np.zeros(P * P * P)
+    damp = np.zeros(P * P * P)
+    mv, dv = m.reshape(P, P, P), damp.reshape(P, P, P)
+    yx = np.maximum(dprof[:, None], dprof[None, :])
+    for zg in range(zoff, zoff + pz):  # make_model's edge replication (seismic.cpp:100-142)
+        iz = min(max(zg - pad, 0), n - 1) - z0
+        mv[zg] = np.pad(mi[iz], pad, mode="edge")
+        dv[zg] = np.maximum(dprof[zg], yx)
+    model = S.VelocityModel([n, n, n], w.h, nbpml, so, [P, P, P], m, damp)
+    w.m_interior = None
+    return w, model
+
+
 def run_ours(args):
     import torch
     from paper_1608_08658_b200 import _lib as L
@@ -330,22 +406,35 @@ def run_ours(args):
         dist.broadcast_object_list(uid, src=0)
         comm = L.Comm(uid[0], world, rank, local)
 
-    if world > 1 and args.workload == "cfg2" and args.scaling == "weak":
+    slab = world > 1 and args.workload == "cfg5"
+    if slab:
+        w, model = slab_problem(L, S, args, world, rank)
+    elif world > 1 and args.workload == "cfg2" and args.scaling == "weak":
         # weak scaling: one cfg2-sized slab per GPU (the cfg2 model stacked along z)
         from paper_1608_08658_b200 import configs
         w = configs.cfg2_stacked(world)
         if args.time_steps:
             w.nt = args.time_steps + 2
         w.wavelet = np.ascontiguousarray(w.wavelet[:w.nt].reshape(w.nt, -1))
+        model = None
     else:
         w = make_workload(args.workload, args.time_steps)
-    model, src, rec = problem(w)
-    S.check_dt(model, w.dt)
+        model = None
+    if model is None:
+        model = S.make_model(w.interior, w.h, w.nbpml, w.space_order, w.m_interior)
+        S.check_dt(model, w.dt)
+    src = S.locate_points(model, w.src_coords)
+    rec = S.locate_points(model, w.rec_coords)
     nd = model.ndim()
-    plan = L.Plan(L.FORWARD, nd, model.padded, w.space_order, w.nt, w.dt, w.h, src.npoints,
-                  rec.npoints, False, local, comm=comm)
+
+    def new_plan():
+        p = L.Plan(L.FORWARD, nd, model.padded, w.space_order, w.nt, w.dt, w.h, src.npoints,
+                   rec.npoints, False, local, comm=comm)
+        p.set_stream(stream.cuda_stream)
+        return p
+
     stream = torch.cuda.Stream()
-    plan.set_stream(stream.cuda_stream)
+    plan = new_plan()
     exchange = None
     if world > 1:
         # Fused P2P ghost exchange (default): the boundary sweeps store into the
@@ -368,14 +457,11 @@ def run_ours(args):
                             "(CUDA IPC over NVLink), step counters via stream memory ops")
             else:  # every rank must use the same exchange
                 plan.close()
-                plan = L.Plan(L.FORWARD, nd, model.padded, w.space_order, w.nt, w.dt, w.h,
-                              src.npoints, rec.npoints, False, local, comm=comm)
-                plan.set_stream(stream.cuda_stream)
+                plan = new_plan()
 
     exchange_check = None
     if world > 1:
-        # The exchange has only ever run with emulated ranks on one GPU before
-        # this job: check it on a small problem against one GPU first, and fall
+        # Check the exchange on a small problem against one GPU first, and fall
         # back to NCCL if the fused P2P path fails or disagrees.
         p2p = exchange.startswith("fused")
         ok, err = check_exchange(L, S, torch, dist, comm, rank, world, local, p2p)
@@ -384,25 +470,20 @@ def run_ours(args):
             if rank == 0:
                 print(f"P2P exchange check failed (rel err {err}); using NCCL", file=sys.stderr)
             plan.close()
-            plan = L.Plan(L.FORWARD, nd, model.padded, w.space_order, w.nt, w.dt, w.h,
-                          src.npoints, rec.npoints, False, local, comm=comm)
-            plan.set_stream(stream.cuda_stream)
+            plan = new_plan()
             exchange = "nccl send/recv on a comm stream, overlapped with the interior sweep"
             ok2, err2 = check_exchange(L, S, torch, dist, comm, rank, world, local, False)
             exchange_check = {"exchange": "nccl", "ok": ok2, "max_rel_err": err2,
                               "p2p_failed": {"ok": ok, "max_rel_err": err}}
 
-    # Pinned host buffers in the reference's layout (fp64 grids, long idx).
-    def pinned(shape, dtype):
-        return torch.empty(shape, dtype=dtype, pin_memory=True).numpy()
-
-    u = pinned((3, *model.padded), torch.float64)
-    m = pinned(model.m.shape, torch.float64); m[:] = model.m
-    damp = pinned(model.damp.shape, torch.float64); damp[:] = model.damp
-    rec_data = pinned((w.nt, rec.npoints), torch.float64)
-    trace = pinned(w.wavelet.shape, torch.float64); trace[:] = w.wavelet
-    argv = [u, m, damp, L.i64(src.idx), L.f64(src.w), trace, L.i64(rec.idx), L.f64(rec.w),
-            rec_data]
+    # Pageable host buffers in the reference's layout (fp64 grids, long idx),
+    # as seismic::forward binds them (seismic.cpp:354-368).  The output grid
+    # is global-shaped; a rank writes only its owned planes.
+    u = np.zeros((3, *model.padded))
+    rec_data = np.zeros((w.nt, rec.npoints))
+    trace = np.ascontiguousarray(w.wavelet)
+    argv = [u, model.m, model.damp, L.i64(src.idx), L.f64(src.w), trace, L.i64(rec.idx),
+            L.f64(rec.w), rec_data]
 
     # ---- device-resident timing (value)
     plan.upload(argv)
@@ -421,6 +502,7 @@ def run_ours(args):
         torch.cuda.synchronize()
     if dist:
         dist.barrier()
+    plan.check()  # a broken P2P exchange fails the run instead of reporting a number
     ms = ev0.elapsed_time(ev1)
     # Kernel timing for the roofline: CUDA events around every sweep launch of
     # one more execute() right after the timed region.  (Events between the
@@ -441,25 +523,30 @@ def run_ours(args):
     launches = plan.launches_per_execute * args.steps
 
     # ---- end to end through the C ABI with host buffers (e2e)
-    e2e = None
-    if not args.no_e2e:
-        plan.run(argv)  # warm
+    def timed_runs(av, reps):
+        plan.run(av)  # warm (and sizes the staging chunks)
         torch.cuda.synchronize()
         if dist:
             dist.barrier()
         t0 = time.perf_counter()
-        for _ in range(args.steps):
-            plan.run(argv)
+        for _ in range(reps):
+            plan.run(av)
         el = time.perf_counter() - t0
         if dist:
             t = torch.tensor([el], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             el = float(t.item())
-        e2e = {"value": pts * args.steps / el / 1e9, "unit": "Gpts/s",
+        return el / reps
+
+    e2e = None
+    if not args.no_e2e:
+        per = timed_runs(argv, args.steps)
+        e2e = {"value": pts / per / 1e9, "unit": "Gpts/s",
                "h2d_bytes_per_step": plan.h2d_bytes, "d2h_bytes_per_step": plan.d2h_bytes,
-               "ms_per_step": el / args.steps * 1e3,
-               "path": "sfdb200_run(plan, argv): reference argv, pinned fp64 host buffers"}
-        # Where the e2e time goes: the same run as three synchronised stages
+               "ms_per_step": per * 1e3, "runs": args.steps,
+               "path": "sfdb200_run(plan, argv): reference argv, pageable fp64 host buffers "
+                       "(the reference's std::vector case, seismic.cpp:354-368)"}
+        # Where the time goes: the same run as three synchronised stages
         # (run() overlaps the receiver rows' D2H with the sweeps; here they all
         # land in download).
         stage = {}
@@ -472,35 +559,41 @@ def run_ours(args):
             stage[name] = (time.perf_counter() - t0) * 1e3
         e2e["staged_ms"] = stage
         if world == 1:
-            # The same call with pageable host arrays, as the reference's
-            # std::vector buffers are (staged through the plan's pinned chunks).
-            pargv = [np.empty_like(u), np.array(m), np.array(damp), L.i64(src.idx),
-                     L.f64(src.w), np.array(trace), L.i64(rec.idx), L.f64(rec.w),
-                     np.empty_like(rec_data)]
-            plan.run(pargv)
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            plan.run(pargv)
-            elp = time.perf_counter() - t0
-            e2e["pageable"] = {"value": pts / elp / 1e9, "ms_per_step": elp * 1e3,
-                               "path": "sfdb200_run with pageable numpy buffers (one run)"}
+            # The same call with pinned host buffers (a caller that owns pinned
+            # memory; not the reference's case).
+            pargv = [_pinned(torch, u.shape), _pinned(torch, model.m.shape, model.m),
+                     _pinned(torch, model.damp.shape, model.damp), L.i64(src.idx), L.f64(src.w),
+                     _pinned(torch, trace.shape, trace), L.i64(rec.idx), L.f64(rec.w),
+                     _pinned(torch, rec_data.shape)]
+            perp = timed_runs(pargv, args.steps)
+            e2e["pinned"] = {"value": pts / perp / 1e9, "ms_per_step": perp * 1e3,
+                             "runs": args.steps,
+                             "path": "sfdb200_run with pinned fp64 host buffers"}
 
     peak, peak_src = measured_peak()
     per_launch_ms = sweep_ms / max(1, sweep_n)
-    # the timed launch is the (interior) sweep over this rank's slab
-    zb, ze, _ = plan.slab()
+    # the timed launch: with the fused P2P exchange one launch per step sweeps
+    # every owned plane (boundary items first); with NCCL the interior launch
+    # leaves out the R planes next to each neighbour
     interior = plan.points_per_step
-    if world > 1:
+    if world > 1 and not exchange.startswith("fused"):
+        zb, ze, _ = plan.slab()
         R = w.space_order // 2
         interior = plan.points_per_step // (ze - zb) * ((ze - zb) - R * ((rank > 0) + (rank < world - 1)))
     # 2-D runs the whole time loop in one cooperative launch
     sweeps_per_launch = plan.steps if nd == 2 else 1
+    info = plan.info()
     bpp = bytes_per_point(plan, "forward")
     alg = bpp * interior * sweeps_per_launch
     achieved = alg / (per_launch_ms / 1e3) / 1e9
+    alg20 = BYTES_PER_POINT["forward"] * interior * sweeps_per_launch
+    traffic, traffic_src = ncu_traffic(w.name, info, nd)
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak, "traffic": ncu_traffic(w.name),
+            "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+            "frac_alg": alg20 / (per_launch_ms / 1e3) / 1e9 / peak,
+            "alg_bytes_per_point_survey": BYTES_PER_POINT["forward"],
             "kernel": kernel_name(plan) if nd == 3 else "loop2d_kernel (all steps, cooperative)",
+            "instantiation": info.get("instantiation"),
             "alg_bytes_per_launch": alg, "bytes_per_point": bpp, "mean_launch_ms": per_launch_ms,
             "kernel_timing": "CUDA events around each launch of one execute() after the timed region",
             "kernel_share_of_step": sweep_ms / (ms / args.steps), "peak_source": peak_src}
@@ -510,14 +603,28 @@ def run_ours(args):
         cb = cpu_baseline(w, args.cpu_steps or 0)
         cb.pop("seconds", None)
 
+    one_gpu = None
+    if world > 1 and args.measure_1gpu:
+        one_gpu = measure_one_gpu(args, rank, dist, torch)
+
     if rank == 0:
+        scaling = "weak" if (world > 1 and args.workload == "cfg2" and args.scaling == "weak") \
+            else "strong"
+        extra = {"sweep": info, "exchange": exchange, "exchange_check": exchange_check}
+        if slab:
+            extra["inputs"] = ("each rank generated only the interior rows its slab needs "
+                               "(configs.cfg5_rows, PCG64 advanced to the rows, rescale range "
+                               "all-reduced) and filled only its planes of the global-shaped "
+                               "model arrays")
+        if one_gpu:
+            extra["one_gpu"] = one_gpu
+            extra["parallel_efficiency"] = value / (world * one_gpu["value"])
         line = {"metric": "Gpts/s (grid-point updates/sec) 3D acoustic so-8", "value": value,
                 "unit": "Gpts/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": ms / args.steps, "higher_is_better": True,
-                "scaling": "strong" if (world > 1 and args.scaling == "strong") else "weak",
+                "scaling": scaling if world > 1 else "weak",
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "config": config_of(w, world, {"sweep": plan.info(), "exchange": exchange,
-                                               "exchange_check": exchange_check}),
+                "config": config_of(w, world, extra),
                 "roofline": roof, "cpu_baseline": cb,
                 "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary}
         print(json.dumps(line))
@@ -526,6 +633,35 @@ def run_ours(args):
         comm.close()
     if dist:
         dist.destroy_process_group()
+
+
+def measure_one_gpu(args, rank, dist, torch):
+    """Rank 0 times the same workload on its GPU alone (the other ranks wait):
+    the denominator of the strong-scaling efficiency."""
+    res = None
+    if rank == 0:
+        from paper_1608_08658_b200 import _lib as L
+        from paper_1608_08658_b200 import seismic as S
+        w = make_workload(args.workload, args.time_steps)
+        model = S.make_model(w.interior, w.h, w.nbpml, w.space_order, w.m_interior)
+        src = S.locate_points(model, w.src_coords)
+        rec = S.locate_points(model, w.rec_coords)
+        p = L.Plan(L.FORWARD, 3, model.padded, w.space_order, w.nt, w.dt, w.h, src.npoints,
+                   rec.npoints, False, int(os.environ.get("LOCAL_RANK", "0")))
+        p.upload([None, model.m, model.damp, src.idx, src.w, w.wavelet, rec.idx, rec.w,
+                  np.zeros((w.nt, rec.npoints))])
+        p.execute()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        p.execute()
+        p.check()
+        el = time.perf_counter() - t0
+        res = {"workload": w.name, "value": w.points_per_step * p.steps / el / 1e9,
+               "timing": "one execute() on rank 0's GPU, host clock around a synchronised run"}
+        p.close()
+        del model
+    dist.barrier()
+    return res
 
 
 def run_fwi(args):
@@ -573,13 +709,10 @@ def run_fwi(args):
         g.bind_checkpoints(fwd)  # history recomputed per segment (one extra forward sweep/step)
     else:
         g.bind_history(fwd)
-    # pinned host buffers for everything the e2e leg moves (model, residual, gradient)
-    def pinned_copy(a):
-        t = torch.empty(a.shape, dtype=torch.float64, pin_memory=True).numpy()
-        t[...] = a
-        return t
-    gargv = [None, None, pinned_copy(bg.m), pinned_copy(bg.damp), pinned_copy(grad),
-             L.i64(rec.idx), L.f64(rec.w), pinned_copy(resid)]
+    # pageable host buffers (the reference's std::vectors, seismic.cpp:446-462)
+    # for everything the e2e leg moves (model, residual, gradient)
+    gargv = [None, None, np.array(bg.m), np.array(bg.damp), grad, L.i64(rec.idx), L.f64(rec.w),
+             np.ascontiguousarray(resid)]
     g.upload(gargv)
     for _ in range(args.warmup):
         g.execute()
@@ -601,21 +734,28 @@ def run_fwi(args):
     value = pts * args.steps / (ms / 1e3) / 1e9
     # e2e: the gradient through the C ABI with host buffers (residual in, grad out;
     # the history stays device-resident from the saved forward, as the design intends)
+    g.run(gargv)  # warm (staging chunks)
     t0 = time.perf_counter()
     for _ in range(args.steps):
         g.run(gargv)
     el = time.perf_counter() - t0
     e2e = {"value": pts * args.steps / el / 1e9, "unit": "Gpts/s",
            "h2d_bytes_per_step": g.h2d_bytes, "d2h_bytes_per_step": g.d2h_bytes,
-           "ms_per_step": el / args.steps * 1e3,
-           "path": "sfdb200_run(gradient plan bound to the saved forward's device history)"}
+           "ms_per_step": el / args.steps * 1e3, "runs": args.steps,
+           "path": "sfdb200_run(gradient plan bound to the saved forward's device history), "
+                   "pageable fp64 host buffers"}
     peak, peak_src = measured_peak()
     per_launch_ms = sweep_ms / max(1, sweep_n)
     bpp = bytes_per_point(g, "gradient")
     alg = bpp * w.points_per_step
     achieved = alg / (per_launch_ms / 1e3) / 1e9
+    traffic, traffic_src = ncu_traffic(w.name, g.info(), 3)
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak, "traffic": ncu_traffic(w.name),
+            "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+            "frac_alg": BYTES_PER_POINT["gradient"] * w.points_per_step / (per_launch_ms / 1e3)
+                        / 1e9 / peak,
+            "alg_bytes_per_point_survey": BYTES_PER_POINT["gradient"],
+            "instantiation": g.info().get("instantiation"),
             "kernel": kernel_name(g) + "<GRAD>", "alg_bytes_per_launch": alg, "bytes_per_point": bpp,
             "mean_launch_ms": per_launch_ms, "kernel_share_of_step": sweep_ms / (ms / args.steps),
             "peak_source": peak_src}
@@ -653,8 +793,27 @@ def run_fwi(args):
         p.close()
 
 
+def relaunch(n):
+    """`python bench.py --gpus N` outside a launcher: run the same command as N
+    ranks under torch.distributed.run (one process per GPU, 127.0.0.1)."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.run(cmd).returncode)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch(args.gpus)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; timing {world} ranks",
+              file=sys.stderr)
     if args.impl == "reference":
         run_reference(args)
     elif args.workload == "cfg3":

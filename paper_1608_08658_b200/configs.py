@@ -83,6 +83,37 @@ def smooth_random_velocity(shape, seed, sigma):
     return 1500.0 + 3000.0 * (v - lo) / (hi - lo)
 
 
+def smooth_random_velocity_rows(shape, seed, sigma, z0, z1, minmax=None):
+    """Rows [z0, z1) (axis 0) of smooth_random_velocity(shape, seed, sigma)
+    without the rest of the grid: the draws of rows [z0 - r, z1 + r) (r = the
+    4-sigma filter radius) come straight from the PCG64 stream advanced to
+    their offset (one 64-bit draw per value, row-major), the block is smoothed
+    like the whole grid (clamp-to-edge only where it touches the grid's ends,
+    so rows [z0, z1) see exactly their full filter windows), then cropped.
+    minmax(lo, hi) -> (global lo, global hi) supplies the rescale range over
+    all rows (e.g. an all-reduce over the ranks that together cover [0, n));
+    None: these rows' own range (only right when [z0, z1) is the whole grid)."""
+    n0 = shape[0]
+    plane = int(np.prod(shape[1:]))
+    r = int(4.0 * sigma + 0.5)
+    lo, hi = max(0, z0 - r), min(n0, z1 + r)
+    bg = np.random.PCG64(seed)
+    bg.advance(lo * plane)
+    v = 1500.0 + 3000.0 * np.random.Generator(bg).random((hi - lo) * plane, dtype=np.float64)
+    v = v.reshape((hi - lo, *shape[1:]))
+    if v.size > (1 << 26) and _cuda_available():
+        v = _smooth_on_gpu(v, sigma)
+    else:
+        from scipy.ndimage import gaussian_filter1d
+        for ax in range(len(shape)):
+            v = gaussian_filter1d(v, sigma, axis=ax, mode="nearest", truncate=4.0)
+    v = np.ascontiguousarray(v[z0 - lo:z1 - lo])
+    a, b = float(v.min()), float(v.max())
+    if minmax is not None:
+        a, b = minmax(a, b)
+    return 1500.0 + 3000.0 * (v - a) / (b - a)
+
+
 def _cuda_available():
     try:
         import torch
@@ -207,3 +238,22 @@ def cfg5(n=1024, nt=502, nbpml=40, nrec_side=512):
     src = np.array([[10.0, a, b] for a in q for b in q])
     return Workload("cfg5-3d-so16", 3, [n, n, n], 16, nt, dt, m, _ricker(10.0, nt, dt, 4), src,
                     _carpet(nrec_side, span, 20.0), h, nbpml, 10.0)
+
+
+def cfg5_rows(z0, z1, minmax, n=1024, nt=502, nbpml=40, nrec_side=512):
+    """cfg5 restricted to the interior rows [z0, z1) a z-slab rank needs
+    (bench.py --gpus N): m_interior holds those rows only (extra["rows"]), the
+    rescale range and dt come from the whole grid through minmax (see
+    smooth_random_velocity_rows).  Sources and receivers are the full sets."""
+    h = 10.0
+    v = smooth_random_velocity_rows((n, n, n), 1, 16.0, z0, z1, minmax)
+    m = _round32(1.0 / v ** 2).ravel()
+    m_min = _round32(np.array([1.0 / 4500.0 ** 2]))[0]  # v reaches 4500 exactly at the global max
+    dt = _crit(m_min, 3, 16, h)
+    span = (n - 1) * h
+    q = [span / 4, 3 * span / 4]
+    src = np.array([[10.0, a, b] for a in q for b in q])
+    w = Workload("cfg5-3d-so16", 3, [n, n, n], 16, nt, dt, m, _ricker(10.0, nt, dt, 4), src,
+                 _carpet(nrec_side, span, 20.0), h, nbpml, 10.0)
+    w.extra["rows"] = (z0, z1)
+    return w

@@ -413,6 +413,16 @@ cudaError_t launch_sweep3d(const FieldGeom& g, const SweepConfig& cfg, const Swe
     return dispatch3d(g, cfg, m, a, grad, s, nullptr);
 }
 
+std::string sweep3d_instantiation(const FieldGeom& g, const SweepConfig& cfg, bool grad) {
+    std::string name;
+    SweepMaps m{};
+    SweepArgs a{};
+    detail::g_describe = &name;
+    const cudaError_t e = dispatch3d(g, cfg, m, a, grad, nullptr, nullptr);
+    detail::g_describe = nullptr;
+    return e == cudaSuccess ? name : std::string();
+}
+
 cudaError_t sweep3d_occupancy(const FieldGeom& g, const SweepConfig& cfg, bool grad,
                               int* blocks_per_sm) {
     SweepMaps m{};

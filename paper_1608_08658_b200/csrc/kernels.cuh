@@ -1,6 +1,7 @@
 // Internal interface between the plan/runtime layer (plan.cu) and the sm_100a
 // kernels (kernels.cu).  No torch, no reference types: plain pointers.
 #pragma once
+#include <string>
 
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -147,6 +148,14 @@ SFDB_DECL_R(7)
 SFDB_DECL_R(8)
 #undef SFDB_DECL_R
 
+namespace detail {
+// sweep3d_instantiation(): when set, a launcher writes the kernel template it
+// would launch (ncu's naming) here and returns without launching.
+inline thread_local std::string* g_describe = nullptr;
+}  // namespace detail
+// The kernel template (with arguments) the variant cfg launches, e.g.
+// "sweep3d_pair_kernel<4, 4, 2, 4, 0, 4, 9, 1>"; empty if cfg has none.
+std::string sweep3d_instantiation(const FieldGeom& g, const SweepConfig& cfg, bool grad);
 // Resident CTAs per SM of the variant cfg selects (registers + shared memory).
 cudaError_t sweep3d_occupancy(const FieldGeom& g, const SweepConfig& cfg, bool grad,
                               int* blocks_per_sm);

@@ -1691,7 +1691,8 @@ int sfdb200_plan_info(const sfdb200_plan* p, char* buf, long len) {
                       "\"stages\": %d, \"tiles\": [%d, %d], \"zchunks\": %d, \"zlen\": %d, "
                       "\"smem_bytes\": %zu, \"fused_sparse\": %s, \"slab\": [%ld, %ld], "
                       "\"x_pitch\": %d, \"mapping\": \"%s\", \"pdl\": %s, "
-                      "\"separable_damping\": %s, \"bytes_per_point\": %d, \"cluster2d_ctas\": %d, \"z_unroll\": %d, \"variant\": \"%d,%d,%d,%d,%d\"}",
+                      "\"separable_damping\": %s, \"bytes_per_point\": %d, \"cluster2d_ctas\": %d, \"z_unroll\": %d, \"variant\": \"%d,%d,%d,%d,%d\", "
+                      "\"instantiation\": \"%s\"}",
                       c.ty(), c.by + 1, 2 * c.ny, c.stages, c.tiles_x, c.tiles_y, c.zchunks,
                       c.zlen, c.smem_bytes, p->fused ? "true" : "false", p->zoff + p->g.R,
                       p->zoff + p->g.Pz - p->g.R, p->g.XP,
@@ -1702,7 +1703,9 @@ int sfdb200_plan_info(const sfdb200_plan* p, char* buf, long len) {
                       c.pdl ? "true" : "false", p->sep_damp ? "true" : "false",
                       (p->grad_kind() ? 32 : 20) - (p->sep_damp ? 4 : 0), p->nc2d,
                       c.rot == 1 ? 2 * p->g.R + 1 : (c.rot == 0 ? 1 : c.rot), c.by, c.ny,
-                      c.stages, c.rot, c.pair);
+                      c.stages, c.rot, c.pair,
+                      p->g.ndim == 3 ? sweep3d_instantiation(p->g, c, p->grad_kind()).c_str()
+                                     : (p->nc2d ? "cluster2d_kernel" : "loop2d_kernel"));
     });
 }
 

@@ -5,7 +5,9 @@
 
 #include <algorithm>
 #include <cmath>
+#include <initializer_list>
 #include <mutex>
+#include <string>
 #include <utility>
 
 #include "kernels.cuh"
@@ -831,11 +833,23 @@ inline unsigned long long zdown_mask(int tiles, int zchunks, long long slots) {
     return pick;
 }
 
+// The kernel template as ncu names it (detail::g_describe).
+inline std::string kernel_name(const char* base, std::initializer_list<int> args) {
+    std::string s = std::string(base) + "<";
+    int k = 0;
+    for (int a : args) s += (k++ ? ", " : "") + std::to_string(a);
+    return s + ">";
+}
+
 // occ != nullptr: report resident CTAs per SM instead of launching.
 template <int R, int BY, int NY, int S, bool GRAD>
 cudaError_t launch3d_t(const FieldGeom& g, const SweepConfig& cfg, const SweepMaps& m,
                        const SweepArgs& a, cudaStream_t s, int* occ) {
     auto kern = sweep3d_kernel<R, BY, NY, S, GRAD, true>;
+    if (g_describe) {
+        *g_describe = kernel_name("sweep3d_kernel", {R, BY, NY, S, GRAD, 1});
+        return cudaSuccess;
+    }
     const size_t smem = sweep3d_smem_bytes(R, cfg, GRAD);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
@@ -857,10 +871,15 @@ cudaError_t launch3d_t(const FieldGeom& g, const SweepConfig& cfg, const SweepMa
 
 constexpr int kMaxDevices = 64;
 
+
 template <int R, int BY, int NY, int S, bool GRAD, int MINB, int UN, bool SEP>
 cudaError_t launch3d_pair_t(const FieldGeom& g, const SweepConfig& cfg, const SweepMaps& m,
                             const SweepArgs& a, cudaStream_t s, int* occ) {
     auto kern = sweep3d_pair_kernel<R, BY, NY, S, GRAD, MINB, UN, SEP>;
+    if (g_describe) {
+        *g_describe = kernel_name("sweep3d_pair_kernel", {R, BY, NY, S, GRAD, MINB, UN, SEP});
+        return cudaSuccess;
+    }
     if (!occ && (a.ez != nullptr) != SEP) return cudaErrorInvalidValue;  // layout mismatch
     const size_t smem = sweep3d_smem_bytes(R, cfg, GRAD);
     // Per instantiation and device: CTAs per SM at this smem size (the
