@@ -344,27 +344,29 @@ def _pinned(torch, shape, fill=None):
     return t
 
 
-def slab_problem(L, S, args, world, rank):
+def slab_problem(L, S, args, world, rank, n=1024, minmax=None):
     """cfg5 at N > 1: this rank's slab only.  The interior rows its planes
     need are generated here (configs.cfg5_rows; the rescale range is
     all-reduced), and the model arrays are GLOBAL-shaped but untouched outside
     the rank's planes (np.zeros: pages that are never written are never
     backed), so sfdb200_upload reads exactly its slab from them as it does
     from a full model."""
-    import torch
-    import torch.distributed as dist
     from paper_1608_08658_b200 import configs
-    n, nbpml, so = 1024, 40, 16
+    nbpml, so = 40, 16
     R, pad = so // 2, nbpml + so // 2
     P = n + 2 * pad
     zb, ze = L.slab(P, so, world, rank)
     zoff, pz = zb - R, (ze - zb) + 2 * R  # local planes [zoff, zoff + pz) of the global grid
     z0, z1 = max(0, zoff - pad), min(n, zoff + pz - pad)
 
-    def minmax(a, b):
-        t = torch.tensor([-a, b], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return -float(t[0]), float(t[1])
+    if minmax is None:  # the rescale range over all ranks' rows
+        import torch
+        import torch.distributed as dist
+
+        def minmax(a, b):
+            t = torch.tensor([-a, b], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            return -float(t[0]), float(t[1])
 
     steps = args.time_steps
     w = configs.cfg5_rows(z0, z1, minmax, n=n, nbpml=nbpml,
