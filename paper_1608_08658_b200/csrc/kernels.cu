@@ -241,7 +241,8 @@ __global__ void sample_kernel(const float* __restrict__ field, const long long* 
 // 3-D (R > 0): the coefficients of the x/y halo cells (never updated) are
 // zero, so the sweep may store its result there unconditionally: with
 // u1 = u2 = 0 on the halo the update yields exactly 0 (sweep3d.cuh).
-__global__ void coeffs_kernel(const double* __restrict__ m, const double* __restrict__ damp,
+template <class M>
+__global__ void coeffs_kernel(const M* __restrict__ m, const double* __restrict__ damp,
                               double dt, float* __restrict__ c1, float* __restrict__ c2,
                               long long cells, int Px, int XP, int Py, int R) {
     const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
@@ -253,7 +254,7 @@ __global__ void coeffs_kernel(const double* __restrict__ m, const double* __rest
         c2[r * XP + x] = 0.0f;
         return;
     }
-    const double a = m[i] / (dt * dt);
+    const double a = static_cast<double>(m[i]) / (dt * dt);
     const double b = damp[i] / (2.0 * dt);
     c1[r * XP + x] = static_cast<float>((a - b) / (a + b));
     c2[r * XP + x] = static_cast<float>(1.0 / (a + b));
@@ -262,7 +263,12 @@ __global__ void coeffs_kernel(const double* __restrict__ m, const double* __rest
 // The same coefficients from m and host-checked separable damp profiles
 // (pz, py, px as doubles; hostio.cpp host_sep_damp): the damp value of every
 // cell is max(pz[z], py[y], px[x]), bit for bit the caller's (checked).
-__global__ void coeffs_sep_kernel(const double* __restrict__ m, const double* __restrict__ prof,
+// M = float: m arrived narrowed on the host, which happens only when every
+// value is exactly representable (hostio.cpp copy_h2d_narrow), so
+// static_cast<double>(m[i]) is the caller's fp64 value and the coefficients
+// are bit for bit the ones from the fp64 upload.
+template <class M>
+__global__ void coeffs_sep_kernel(const M* __restrict__ m, const double* __restrict__ prof,
                                   double dt, float* __restrict__ c1, float* __restrict__ c2,
                                   long long cells, int Px, int XP, int Py, int Pz, int R) {
     const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
@@ -275,7 +281,7 @@ __global__ void coeffs_sep_kernel(const double* __restrict__ m, const double* __
         return;
     }
     const double dmp = fmax(fmax(prof[z], prof[Pz + y]), prof[Pz + Py + x]);
-    const double a = m[i] / (dt * dt);
+    const double a = static_cast<double>(m[i]) / (dt * dt);
     const double b = dmp / (2.0 * dt);
     c1[r * XP + x] = static_cast<float>((a - b) / (a + b));
     c2[r * XP + x] = static_cast<float>(1.0 / (a + b));
@@ -344,20 +350,24 @@ __global__ void prof_out_kernel(const unsigned long long* a, int n, double dt, f
     if (i < n) out[i] = static_cast<float>(__longlong_as_double(a[i]) / dt);
 }
 
-__global__ void to_f32_kernel(const double* __restrict__ src, float* __restrict__ dst,
-                              long long n, int Px, int XP) {
+// dense [rows][Px] -> pitched [rows][XP] (with a type conversion)
+template <class S, class D>
+__global__ void pitch_kernel(const S* __restrict__ src, D* __restrict__ dst, long long n, int Px,
+                             int XP) {
     const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
     if (i >= n) return;
     const long long r = i / Px, x = i - r * Px;
-    dst[r * XP + x] = static_cast<float>(src[i]);
+    dst[r * XP + x] = static_cast<D>(src[i]);
 }
 
-__global__ void to_f64_kernel(const float* __restrict__ src, double* __restrict__ dst,
-                              long long n, int Px, int XP) {
+// pitched [rows][XP] -> dense [rows][Px]
+template <class S, class D>
+__global__ void unpitch_kernel(const S* __restrict__ src, D* __restrict__ dst, long long n, int Px,
+                               int XP) {
     const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
     if (i >= n) return;
     const long long r = i / Px, x = i - r * Px;
-    dst[i] = static_cast<double>(src[r * XP + x]);
+    dst[i] = static_cast<D>(src[r * XP + x]);
 }
 
 __global__ void nonfinite_kernel(const float* __restrict__ a, long long n,
@@ -548,17 +558,28 @@ cudaError_t launch_sample(const float* field, const long long* off, const float*
     return cudaGetLastError();
 }
 
-cudaError_t launch_coeffs(const FieldGeom& g, const double* m, const double* damp, double dt,
-                          float* c1, float* c2, cudaStream_t s) {
+template <class M>
+cudaError_t launch_coeffs_t(const FieldGeom& g, const M* m, const double* damp, double dt,
+                            float* c1, float* c2, cudaStream_t s) {
     const long long cells = static_cast<long long>(g.Pz) * g.Py * g.Px;
     coeffs_kernel<<<grid_for(cells, 256), 256, 0, s>>>(m, damp, dt, c1, c2, cells, g.Px, g.XP,
                                                         g.Py, g.ndim == 3 ? g.R : 0);
     return cudaGetLastError();
 }
 
-cudaError_t launch_coeffs_sep(const FieldGeom& g, const double* m, const double* prof, double dt,
-                              float* c1, float* c2, float* ez, float* ey, float* ex,
-                              cudaStream_t s) {
+cudaError_t launch_coeffs(const FieldGeom& g, const double* m, const double* damp, double dt,
+                          float* c1, float* c2, cudaStream_t s) {
+    return launch_coeffs_t(g, m, damp, dt, c1, c2, s);
+}
+cudaError_t launch_coeffs(const FieldGeom& g, const float* m, const double* damp, double dt,
+                          float* c1, float* c2, cudaStream_t s) {
+    return launch_coeffs_t(g, m, damp, dt, c1, c2, s);
+}
+
+template <class M>
+cudaError_t launch_coeffs_sep_t(const FieldGeom& g, const M* m, const double* prof, double dt,
+                                float* c1, float* c2, float* ez, float* ey, float* ex,
+                                cudaStream_t s) {
     const long long cells = static_cast<long long>(g.Pz) * g.Py * g.Px;
     coeffs_sep_kernel<<<grid_for(cells, 256), 256, 0, s>>>(m, prof, dt, c1, c2, cells, g.Px, g.XP,
                                                             g.Py, g.Pz, g.R);
@@ -567,6 +588,16 @@ cudaError_t launch_coeffs_sep(const FieldGeom& g, const double* m, const double*
     prof_out_kernel<<<grid_for(g.Py, 256), 256, 0, s>>>(bits + g.Pz, g.Py, dt, ey);
     prof_out_kernel<<<grid_for(g.Px, 256), 256, 0, s>>>(bits + g.Pz + g.Py, g.Px, dt, ex);
     return cudaGetLastError();
+}
+cudaError_t launch_coeffs_sep(const FieldGeom& g, const double* m, const double* prof, double dt,
+                              float* c1, float* c2, float* ez, float* ey, float* ex,
+                              cudaStream_t s) {
+    return launch_coeffs_sep_t(g, m, prof, dt, c1, c2, ez, ey, ex, s);
+}
+cudaError_t launch_coeffs_sep(const FieldGeom& g, const float* m, const double* prof, double dt,
+                              float* c1, float* c2, float* ez, float* ey, float* ex,
+                              cudaStream_t s) {
+    return launch_coeffs_sep_t(g, m, prof, dt, c1, c2, ez, ey, ex, s);
 }
 
 cudaError_t launch_damp_profiles(const double* damp, int Pz, int Py, int Px, double dt,
@@ -581,7 +612,10 @@ cudaError_t launch_damp_profiles(const double* damp, int Pz, int Py, int Px, dou
     prof_fill_kernel<<<grid_for(n, 256), 256, 0, s>>>(scratch, n);
     prof_min_kernel<<<dim3((Py + kProfRows - 1) / kProfRows, Pz), 256, 0, s>>>(damp, Pz, Py, Px,
                                                                                  pz, py, px);
-    prof_check_kernel<<<4 * 148, 256, 0, s>>>(damp, Pz, Py, Px, pz, py, px, mismatch);
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess)
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    prof_check_kernel<<<4 * sms, 256, 0, s>>>(damp, Pz, Py, Px, pz, py, px, mismatch);
     prof_out_kernel<<<grid_for(Pz, 256), 256, 0, s>>>(pz, Pz, dt, ez);
     prof_out_kernel<<<grid_for(Py, 256), 256, 0, s>>>(py, Py, dt, ey);
     prof_out_kernel<<<grid_for(Px, 256), 256, 0, s>>>(px, Px, dt, ex);
@@ -592,7 +626,7 @@ cudaError_t launch_to_f32(const FieldGeom& g, const double* src, float* dst, lon
                           cudaStream_t s) {
     const long long n = rows * g.Pz * g.Py * g.Px;
     if (n == 0) return cudaSuccess;
-    to_f32_kernel<<<grid_for(n, 256), 256, 0, s>>>(src, dst, n, g.Px, g.XP);
+    pitch_kernel<<<grid_for(n, 256), 256, 0, s>>>(src, dst, n, g.Px, g.XP);
     return cudaGetLastError();
 }
 
@@ -600,19 +634,35 @@ cudaError_t launch_to_f64(const FieldGeom& g, const float* src, double* dst, lon
                           cudaStream_t s) {
     const long long n = rows * g.Pz * g.Py * g.Px;
     if (n == 0) return cudaSuccess;
-    to_f64_kernel<<<grid_for(n, 256), 256, 0, s>>>(src, dst, n, g.Px, g.XP);
+    unpitch_kernel<<<grid_for(n, 256), 256, 0, s>>>(src, dst, n, g.Px, g.XP);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pitch_f32(const FieldGeom& g, const float* src, float* dst, long long rows,
+                             cudaStream_t s) {
+    const long long n = rows * g.Pz * g.Py * g.Px;
+    if (n == 0) return cudaSuccess;
+    pitch_kernel<<<grid_for(n, 256), 256, 0, s>>>(src, dst, n, g.Px, g.XP);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_unpitch_f32(const FieldGeom& g, const float* src, float* dst, long long rows,
+                               cudaStream_t s) {
+    const long long n = rows * g.Pz * g.Py * g.Px;
+    if (n == 0) return cudaSuccess;
+    unpitch_kernel<<<grid_for(n, 256), 256, 0, s>>>(src, dst, n, g.Px, g.XP);
     return cudaGetLastError();
 }
 
 cudaError_t launch_dense_to_f32(const double* src, float* dst, long long n, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
-    to_f32_kernel<<<grid_for(n, 256), 256, 0, s>>>(src, dst, n, 1, 1);
+    pitch_kernel<<<grid_for(n, 256), 256, 0, s>>>(src, dst, n, 1, 1);
     return cudaGetLastError();
 }
 
 cudaError_t launch_dense_to_f64(const float* src, double* dst, long long n, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
-    to_f64_kernel<<<grid_for(n, 256), 256, 0, s>>>(src, dst, n, 1, 1);
+    unpitch_kernel<<<grid_for(n, 256), 256, 0, s>>>(src, dst, n, 1, 1);
     return cudaGetLastError();
 }
 

@@ -291,6 +291,18 @@ cudaError_t launch_to_f32(const FieldGeom& g, const double* src, float* dst, lon
 cudaError_t launch_to_f64(const FieldGeom& g, const float* src, double* dst, long long rows,
                           cudaStream_t s);
 cudaError_t launch_dense_to_f32(const double* src, float* dst, long long n, cudaStream_t s);
+// fp32 rows: dense [rows][Px] <-> pitched [rows][XP] (host-narrowed uploads,
+// downloads widened on the host, hostio.cpp)
+cudaError_t launch_pitch_f32(const FieldGeom& g, const float* src, float* dst, long long rows,
+                             cudaStream_t s);
+cudaError_t launch_unpitch_f32(const FieldGeom& g, const float* src, float* dst, long long rows,
+                               cudaStream_t s);
+// m narrowed on the host (only when exact): the same coefficients
+cudaError_t launch_coeffs(const FieldGeom& g, const float* m, const double* damp, double dt,
+                          float* c1, float* c2, cudaStream_t s);
+cudaError_t launch_coeffs_sep(const FieldGeom& g, const float* m, const double* prof, double dt,
+                              float* c1, float* c2, float* ez, float* ey, float* ex,
+                              cudaStream_t s);
 cudaError_t launch_dense_to_f64(const float* src, double* dst, long long n, cudaStream_t s);
 // Counts non-finite values (the reference's check_finite, seismic.cpp:39-44).
 cudaError_t launch_count_nonfinite(const float* a, long long n, unsigned long long* counter,

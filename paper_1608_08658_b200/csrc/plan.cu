@@ -342,9 +342,21 @@ void create(const sfdb200_desc& gd, Comm* comm, sfdb200_plan& p) {
     ck(cudaStreamSynchronize(p.stream), "plan setup");
 }
 
+// Pageable host arrays move at half width (hostio.cpp copy_h2d_narrow /
+// copy_d2h_widen): traces and history rows are rounded to fp32 on the host
+// exactly as the device would round them, and fp32 results widen exactly,
+// so the bits are those of the fp64 path.  Page-locked arrays keep the
+// direct fp64 DMA (no host pass).
+bool narrow_ok(const void* host) { return env_int("SFDB200_NARROW", 1) && !host_pinned(host); }
+
 void upload_trace(sfdb200_plan& p, SparseDev& s, const double* data) {
     const long long n = p.d.nt * s.n;
     if (n == 0) return;
+    if (narrow_ok(data)) {
+        copy_h2d_narrow(p, s.trace, data, static_cast<size_t>(n), false);
+        p.h2d += n * 4;
+        return;
+    }
     p.ensure_staging(static_cast<size_t>(n));
     copy_h2d(p, p.staging, data, static_cast<size_t>(n) * 8);
     ck(launch_dense_to_f32(p.staging, s.trace, n, p.stream), "convert");
@@ -354,6 +366,11 @@ void upload_trace(sfdb200_plan& p, SparseDev& s, const double* data) {
 void download_trace(sfdb200_plan& p, SparseDev& s, double* out) {
     const long long n = p.d.nt * s.n;
     if (n == 0) return;
+    if (narrow_ok(out)) {
+        copy_d2h_widen(p, out, s.trace, static_cast<size_t>(n));
+        p.d2h += n * 4;
+        return;
+    }
     p.ensure_staging(static_cast<size_t>(n));
     ck(launch_dense_to_f64(s.trace, p.staging, n, p.stream), "convert");
     copy_d2h(p, out, p.staging, static_cast<size_t>(n) * 8);
@@ -366,10 +383,19 @@ void upload_rows(sfdb200_plan& p, const double* src, float* dst, long long rows)
     const long long cells = p.cells(), pc = p.plane_cells();
     const long long gcells = pc * p.gd.padded[0];
     p.ensure_staging(static_cast<size_t>(cells));
+    const bool narrow = rows > 0 && narrow_ok(src);
+    float* st32 = reinterpret_cast<float*>(p.staging);
     for (long long r = 0; r < rows; ++r) {
-        copy_h2d(p, p.staging, src + r * gcells + p.zoff * pc, static_cast<size_t>(cells) * 8);
-        ck(launch_to_f32(p.g, p.staging, dst + r * p.g.slot, 1, p.stream), "convert");
-        p.h2d += cells * 8;
+        const double* row = src + r * gcells + p.zoff * pc;
+        if (narrow) {
+            copy_h2d_narrow(p, st32, row, static_cast<size_t>(cells), false);
+            ck(launch_pitch_f32(p.g, st32, dst + r * p.g.slot, 1, p.stream), "pitch");
+            p.h2d += cells * 4;
+        } else {
+            copy_h2d(p, p.staging, row, static_cast<size_t>(cells) * 8);
+            ck(launch_to_f32(p.g, p.staging, dst + r * p.g.slot, 1, p.stream), "convert");
+            p.h2d += cells * 8;
+        }
     }
 }
 
@@ -380,12 +406,20 @@ void download_rows(sfdb200_plan& p, const float* src, double* dst, long long row
     const long lo = p.rank == 0 ? 0 : p.g.R;
     const long hi = p.rank == p.world - 1 ? p.g.Pz : p.g.Pz - p.g.R;
     p.ensure_staging(static_cast<size_t>(cells));
+    const bool narrow = rows > 0 && narrow_ok(dst);
+    float* st32 = reinterpret_cast<float*>(p.staging);
     for (long long r = 0; r < rows; ++r) {
-        ck(launch_to_f64(p.g, src + r * p.g.slot, p.staging, 1, p.stream), "convert");
-        copy_d2h(p, dst + r * gcells + (p.zoff + lo) * pc, p.staging + lo * pc,
-                 static_cast<size_t>((hi - lo) * pc) * 8);
-        ck(cudaStreamSynchronize(p.stream), "D2H");
-        p.d2h += (hi - lo) * pc * 8;
+        double* out = dst + r * gcells + (p.zoff + lo) * pc;
+        if (narrow) {
+            ck(launch_unpitch_f32(p.g, src + r * p.g.slot, st32, 1, p.stream), "unpitch");
+            copy_d2h_widen(p, out, st32 + lo * pc, static_cast<size_t>((hi - lo) * pc));
+            p.d2h += (hi - lo) * pc * 4;
+        } else {
+            ck(launch_to_f64(p.g, src + r * p.g.slot, p.staging, 1, p.stream), "convert");
+            copy_d2h(p, out, p.staging + lo * pc, static_cast<size_t>((hi - lo) * pc) * 8);
+            ck(cudaStreamSynchronize(p.stream), "D2H");
+            p.d2h += (hi - lo) * pc * 8;
+        }
     }
 }
 
@@ -497,8 +531,15 @@ void do_upload(sfdb200_plan& p, void** argv) {
         sep_check = std::async(std::launch::async, [&] {
             return host_sep_damp(damp + off, p.g.Pz, p.g.Py, p.g.Px, p.hprof);
         });
+    // A pageable m whose values are all fp32-representable (the usual case:
+    // models are fp32 data) travels narrowed, 4 B per cell; the coefficient
+    // kernels widen it back exactly.  Anything else moves as fp64.
+    bool m32 = false;
+    float* m32p = reinterpret_cast<float*>(p.staging);
     try {
-        copy_h2d(p, p.staging, m + off, static_cast<size_t>(cells) * 8);
+        if (env_int("SFDB200_NARROW", 1) && !host_pinned(m + off))
+            m32 = copy_h2d_narrow(p, m32p, m + off, static_cast<size_t>(cells), true);
+        if (!m32) copy_h2d(p, p.staging, m + off, static_cast<size_t>(cells) * 8);
     } catch (...) {
         if (sep_check.valid()) sep_check.wait();
         throw;
@@ -510,12 +551,15 @@ void do_upload(sfdb200_plan& p, void** argv) {
                            p.stream),
            "H2D");
         float* ez = p.eprof;
-        ck(launch_coeffs_sep(p.g, p.staging, prof, d.dt, p.c1, p.c2, ez, ez + p.g.Pz,
-                             ez + p.g.Pz + p.g.Py, p.stream),
+        ck(m32 ? launch_coeffs_sep(p.g, m32p, prof, d.dt, p.c1, p.c2, ez, ez + p.g.Pz,
+                                   ez + p.g.Pz + p.g.Py, p.stream)
+               : launch_coeffs_sep(p.g, p.staging, prof, d.dt, p.c1, p.c2, ez, ez + p.g.Pz,
+                                   ez + p.g.Pz + p.g.Py, p.stream),
            "coeffs");
     } else {
         copy_h2d(p, p.staging + cells, damp + off, static_cast<size_t>(cells) * 8);
-        ck(launch_coeffs(p.g, p.staging, p.staging + cells, d.dt, p.c1, p.c2, p.stream),
+        ck(m32 ? launch_coeffs(p.g, m32p, p.staging + cells, d.dt, p.c1, p.c2, p.stream)
+               : launch_coeffs(p.g, p.staging, p.staging + cells, d.dt, p.c1, p.c2, p.stream),
            "coeffs");
     }
     // Host work while the model is in flight: the sparse sets' data hashes
@@ -556,7 +600,8 @@ void do_upload(sfdb200_plan& p, void** argv) {
     p.base.ey = p.sep_damp ? p.eprof + p.g.Pz : nullptr;
     p.base.ex = p.sep_damp ? p.eprof + p.g.Pz + p.g.Py : nullptr;
     ck(cudaStreamSynchronize(p.stream), "coeffs");
-    p.h2d += host_sep ? cells * 8 + static_cast<long long>(p.hprof.size()) * 8 : 2 * cells * 8;
+    p.h2d += (m32 ? cells * 4 : cells * 8) +
+             (host_sep ? static_cast<long long>(p.hprof.size()) * 8 : cells * 8);
 
     if (grad && p.ck_fwd) {  // history recomputed per segment from checkpoints
         const long rows = p.ck_fwd->ck_interval + 2;
@@ -1001,7 +1046,10 @@ void flush_rows(sfdb200_plan& p, long upto) {
     SparseDev& s = p.rec;
     if (!p.host_rec || upto <= p.flushed || !s.n) return;
     const long long n = (upto - p.flushed) * s.n;
-    if (static_cast<size_t>(n) > p.xstaging_elems) {  // sized for the whole record once
+    // pageable record: fp32 rows, widened by stream host functions (half the
+    // PCIe bytes); pinned: converted on the device and DMA'd as fp64
+    const bool widen = !p.host_rec_pinned && env_int("SFDB200_NARROW", 1);
+    if (!widen && static_cast<size_t>(n) > p.xstaging_elems) {  // sized for the whole record once
         ck(cudaStreamSynchronize(p.xstream), "flush");
         cudaFree(p.xstaging);
         p.xstaging = nullptr;
@@ -1011,14 +1059,20 @@ void flush_rows(sfdb200_plan& p, long upto) {
     ck(cudaEventRecord(p.ev_flush, p.stream), "event");
     ck(cudaStreamWaitEvent(p.xstream, p.ev_flush, 0), "wait");
     const long long off = p.flushed * s.n;
-    ck(launch_dense_to_f64(s.trace + off, p.xstaging + off, n, p.xstream), "convert");
-    if (p.host_rec_pinned)
-        ck(cudaMemcpyAsync(p.host_rec + off, p.xstaging + off, n * 8, cudaMemcpyDeviceToHost,
-                           p.xstream), "D2H");
-    else
-        copy_d2h_stream_pageable(p, p.host_rec + off, p.xstaging + off,
-                                 static_cast<size_t>(n) * 8, p.xstream);
-    p.d2h += n * 8;
+    if (widen) {
+        copy_d2h_stream_widen(p, p.host_rec + off, s.trace + off, static_cast<size_t>(n),
+                              p.xstream);
+        p.d2h += n * 4;
+    } else {
+        ck(launch_dense_to_f64(s.trace + off, p.xstaging + off, n, p.xstream), "convert");
+        if (p.host_rec_pinned)
+            ck(cudaMemcpyAsync(p.host_rec + off, p.xstaging + off, n * 8, cudaMemcpyDeviceToHost,
+                               p.xstream), "D2H");
+        else
+            copy_d2h_stream_pageable(p, p.host_rec + off, p.xstaging + off,
+                                     static_cast<size_t>(n) * 8, p.xstream);
+        p.d2h += n * 8;
+    }
     p.flushed = upto;
 }
 

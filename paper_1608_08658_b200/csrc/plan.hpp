@@ -267,6 +267,17 @@ bool host_pinned(const void* ptr);
 void copy_h2d(sfdb200_plan& p, void* dst, const void* src, size_t bytes);
 void copy_d2h(sfdb200_plan& p, void* dst, const void* src, size_t bytes);
 void release_pinned(sfdb200_plan& p);
+// Half-width transfers for pageable caller buffers: host threads narrow the
+// fp64 values to fp32 into the pinned chunks (round to nearest, the device's
+// own conversion), so PCIe carries 4 B per value instead of 8, and widen
+// fp32 values back (exact) on the way down.  copy_h2d_narrow with exact =
+// true returns false -- having copied nothing that matters -- as soon as a
+// value is not exactly representable in fp32 (the caller then moves fp64).
+bool copy_h2d_narrow(sfdb200_plan& p, float* dst, const double* src, size_t count, bool exact);
+void copy_d2h_widen(sfdb200_plan& p, double* dst, const float* src, size_t count);
+// The same on stream s, drained into dst by stream host functions.
+void copy_d2h_stream_widen(sfdb200_plan& p, double* dst, const float* src, size_t count,
+                           cudaStream_t s);
 // Stream-ordered D2H into a pageable destination on stream s (the record
 // streamed during a run): through the plan's two xpin chunks, each drained by
 // a stream host function, so the caller's thread never blocks.
