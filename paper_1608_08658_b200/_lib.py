@@ -92,14 +92,24 @@ EXPORTS = tuple(_SIGS)
 _lib = None
 
 
+DEBUG_LIB_PATH = os.path.join(PKG_DIR, "libsfdb200_debug.so")
+
+
+def lib_path():
+    """libsfdb200.so, or with SFDB200_LIBRARY=debug the build whose kernels
+    check every global access they make (csrc/kernels.cuh SFDB_CHECK)."""
+    return DEBUG_LIB_PATH if os.environ.get("SFDB200_LIBRARY") == "debug" else LIB_PATH
+
+
 def lib():
     """Loads libsfdb200.so (fails loudly when it was not built)."""
     global _lib
     if _lib is None:
-        if not os.path.exists(LIB_PATH):
-            raise ImportError(f"{LIB_PATH} is missing: build it with "
+        path = lib_path()
+        if not os.path.exists(path):
+            raise ImportError(f"{path} is missing: build it with "
                               "`python -c 'import __graft_entry__ as g; g.build()'`")
-        lib_ = C.CDLL(LIB_PATH)
+        lib_ = C.CDLL(path)
         for name, (res, args) in _SIGS.items():
             f = getattr(lib_, name)
             f.restype = res

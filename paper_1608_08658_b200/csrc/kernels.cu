@@ -86,8 +86,11 @@ __global__ void __launch_bounds__(256) loop2d_kernel(const Loop2dArgs a) {
         for (long q = q0 + tid; q < q1; q += nth) {
             float acc = 0.0f;
 #pragma unroll
-            for (int c = 0; c < 4; ++c)
-                acc = fmaf(__ldg(a.smp_w + 4 * q + c), __ldcg(field + a.smp_off[4 * q + c]), acc);
+            for (int c = 0; c < 4; ++c) {
+                const long long o = a.smp_off[4 * q + c];
+                if (SFDB_CHECK(a.dbg, o >= 0 && o < a.slot, kDbg2d))
+                    acc = fmaf(__ldg(a.smp_w + 4 * q + c), __ldcg(field + o), acc);
+            }
             a.smp_trace[row * a.smp_n + a.smp_pt[q]] = acc;
         }
     };
@@ -130,6 +133,7 @@ __global__ void __launch_bounds__(256) loop2d_kernel(const Loop2dArgs a) {
             const long irow = fwd ? t - 1 : t;
             for (int e = e_begin + tid; e < e_end; e += nth) {
                 const long long o = a.inj_off[e];
+                if (!SFDB_CHECK(a.dbg, o >= 0 && o < a.slot, kDbg2d)) continue;
                 const float delta = a.inj_coef[e] * __ldg(a.inj_trace + irow * a.inj_n + a.inj_pt[e]);
                 atomicAdd(out + o, delta);
                 if constexpr (GRAD)

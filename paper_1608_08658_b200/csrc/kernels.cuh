@@ -30,6 +30,28 @@ struct FieldGeom {
 // (algebraically the reference's (2a u1 - (a-b) u2 + lap)/(a+b),
 // tests/golden/forward_3d_full.c:44-49).  With GRAD the same pass accumulates
 // the imaging condition grad += -(1/dt^2) u_t (v_t - 2 v_{t+1} + v_{t+2}).
+// Debug builds (make debug -> libsfdb200_debug.so, -DSFDB200_DEBUG): the
+// kernels check their global-memory accesses against the rows they address
+// and, on a violation, record the first check's code in *dbg and skip the
+// access (the host then fails the plan: download / sfdb200_plan_check).
+// Release builds compile the checks away.
+#ifdef SFDB200_DEBUG
+#define SFDB_CHECK(flag, cond, code) \
+    ((cond) || ((flag) ? (atomicCAS((flag), 0u, static_cast<unsigned int>(code)), false) : false))
+#else
+#define SFDB_CHECK(flag, cond, code) true
+#endif
+enum DebugCheck : unsigned int {
+    kDbgStore = 1,      // sweep store outside the output row
+    kDbgGradStore = 2,  // gradient store outside the gradient row
+    kDbgPeerStore = 3,  // P2P store outside the neighbour's row
+    kDbgSample = 4,     // receiver corner outside the sampled row
+    kDbgInject = 5,     // injection corner outside the written row
+    kDbgTmaPlane = 6,   // TMA plane coordinate outside the field
+    kDbgQueue = 7,      // z-queue prologue load outside the field
+    kDbg2d = 8          // 2-D loop: sparse offset outside the row
+};
+
 struct SweepArgs {
     float* out;             // output row base
     const float* u1;        // row read at stencil offsets
@@ -97,6 +119,12 @@ struct SweepArgs {
     // This rank's sticky broken flag (P2P with step counters): once set, the
     // boundary items skip their peer stores and the step publication.
     const unsigned int* broken;
+    // Debug checks (SFDB_CHECK): elements per row of this plan's fields and
+    // of the neighbours' (P2P), the neighbours' rows written this step, the flag.
+    long long slot;
+    long long peer_slot[2];
+    const float* peer_row[2];
+    unsigned int* dbg;
 };
 
 struct SweepMaps {          // TMA descriptors (3-D only)
@@ -191,6 +219,7 @@ struct Loop2dArgs {
     long smp_cnt, smp_per_cta;
     float* smp_trace;
     long smp_n;
+    unsigned int* dbg;         // debug builds (SFDB_CHECK)
 };
 cudaError_t launch_loop2d(const Loop2dArgs& a, int R, bool grad, int ctas, cudaStream_t s);
 

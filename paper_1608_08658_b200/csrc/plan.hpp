@@ -196,6 +196,7 @@ struct sfdb200_plan {
     cudaEvent_t pin_ev[2] = {nullptr, nullptr};
     unsigned long long* counter = nullptr;
     unsigned int* flag = nullptr;
+    unsigned int* dbg = nullptr;  // debug builds: first failed access check (kernels.cuh)
 
     cudaStream_t own_stream = nullptr;
     cudaStream_t stream = nullptr;

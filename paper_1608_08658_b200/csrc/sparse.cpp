@@ -180,6 +180,9 @@ void upload_sparse(sfdb200_plan& p, SparseDev& s, const long* idx, const double*
             k.x = pos[nd - 1];
             k.dense = dense;
             k.owned = p.owns_plane(k.zl);
+            // every corner a table addresses lies in this rank's rows
+            if (k.owned && (k.zl < 0 || k.zl >= g.Pz))
+                fail(SFDB200_ECUDA, "internal: an owned sparse corner lies outside the slab");
             k.off = k.zl * g.pz + k.y * g.py + k.x;
             k.updated = k.zl >= R && k.zl < g.Pz - R && k.x >= R && k.x < g.Px - R &&
                         (nd == 2 || (k.y >= R && k.y < g.Py - R));
@@ -315,6 +318,11 @@ void upload_sparse(sfdb200_plan& p, SparseDev& s, const long* idx, const double*
             a_base.push_back(b.off);
             a_pt.push_back(static_cast<int>(q));
         }
+#ifdef SFDB200_DEBUG
+        // Fault injection for the access-check test (debug builds only): the
+        // first receiver's base moves one row past the end of the field row.
+        if (env_int("SFDB200_DEBUG_FAULT", 0) == 1 && !a_base.empty()) a_base[0] += g.slot;
+#endif
         if (nd == 2 && p.nc2d) {  // cluster loop: by the band of the base row
             struct K { int cta; long q; };
             std::vector<K> ks;

@@ -175,7 +175,9 @@ __device__ __noinline__ void sample_cta(const SweepArgs& a, long long py, long l
     const int per = (a.smp_n + nctas - 1) / nctas;
     const int e0 = cta * per, e1 = min(e0 + per, a.smp_n);
     for (int e = e0 + tid; e < e1; e += NT) {
-        const float* u = a.u1 + __ldg(a.smp_base + e);
+        const long long b0 = __ldg(a.smp_base + e);
+        if (!SFDB_CHECK(a.dbg, b0 >= 0 && b0 + pz + py + 1 < a.slot, kDbgSample)) continue;
+        const float* u = a.u1 + b0;
         const float4 wl = __ldg(reinterpret_cast<const float4*>(a.smp_w) + 2 * e);
         const float4 wh = __ldg(reinterpret_cast<const float4*>(a.smp_w) + 2 * e + 1);
         const float* v = u + pz;
@@ -197,6 +199,7 @@ __device__ __noinline__ void inject_cta(const SweepArgs& a, int cta, int tid) {
     const int e0 = __ldg(a.inj_tab + cta), e1 = __ldg(a.inj_tab + cta + 1);
     for (int e = e0 + tid; e < e1; e += NT) {
         const long long o = __ldg(a.inj_off + e);
+        if (!SFDB_CHECK(a.dbg, o >= 0 && o < a.slot, kDbgInject)) continue;
         const float delta = __ldg(a.inj_coef + e) * __ldg(a.inj_row + __ldg(a.inj_pt + e));
         atomicAdd(a.out + o, delta);
         if constexpr (GRAD)
@@ -562,6 +565,12 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
                     float* sb = smem + st * T::SF;
                     uint64_t* bar = &full[st];
                     const int z = z0 + dz * i;
+                    {
+                        const long long planes = a.slot / pz;
+                        SFDB_CHECK(a.dbg, z >= 0 && z < planes && z + dz * R >= 0 &&
+                                              z + dz * R < planes,
+                                   kDbgTmaPlane);
+                    }
                     // SEP: -ez[z] rides in the stage, ordered before the consumers'
                     // acquire by the release of this arrive.
                     if constexpr (SEP) sb[T::O_NEZ] = cur;
@@ -628,7 +637,10 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
 #pragma unroll
             for (int t = 0; t < 2 * R; ++t) {
                 const long long o = static_cast<long long>(z0 + dz * (t - R)) * pz;
-                q[jj][t] = y < Py ? __ldg(reinterpret_cast<const float2*>(c + o)) : f2(0.0f, 0.0f);
+                const bool in = SFDB_CHECK(
+                    a.dbg, y >= Py || (c + o >= a.u1 && c + o + 2 <= a.u1 + a.slot), kDbgQueue);
+                q[jj][t] = y < Py && in ? __ldg(reinterpret_cast<const float2*>(c + o))
+                                        : f2(0.0f, 0.0f);
             }
         }
         // Store only the 32-byte sectors that hold updated cells (whole sectors:
@@ -722,11 +734,16 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
                 const float2 inc = fma2(c1v, d, mul2(c2v, lp));
                 const float2 o = add2(c0, inc);
                 char* pj = cur + jj * rowb;
-                if (vy[jj]) st2(reinterpret_cast<float*>(pj), o);
+                const bool inb = SFDB_CHECK(
+                    a.dbg,
+                    !vy[jj] || (reinterpret_cast<float*>(pj) >= a.out &&
+                                reinterpret_cast<float*>(pj) + 2 <= a.out + a.slot),
+                    kDbgStore);
+                if (vy[jj] && inb) st2(reinterpret_cast<float*>(pj), o);
                 if constexpr (GRAD) {
                     const float2 vtt = fma2(d, mone, inc);
                     const float2 coef = mul2(nidt2, ld2(UT + ci));
-                    if (vy[jj])
+                    if (vy[jj] && inb)
                         st2(reinterpret_cast<float*>(pj + gdiff), fma2(coef, vtt, ld2(GR + ci)));
                 }
             }
@@ -784,7 +801,13 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
                     if (vy[jj]) {
                         const float* src = reinterpret_cast<const float*>(cp + jj * rowb);
                         const float2 v = __ldcg(reinterpret_cast<const float2*>(src));
-                        st2(reinterpret_cast<float*>(const_cast<char*>(cp + jj * rowb) + pd), v);
+                        float* dst = reinterpret_cast<float*>(const_cast<char*>(cp + jj * rowb) + pd);
+                        if (SFDB_CHECK(a.dbg,
+                                       !a.peer_row[bs] ||
+                                           (dst >= a.peer_row[bs] &&
+                                            dst + 2 <= a.peer_row[bs] + a.peer_slot[bs]),
+                                       kDbgPeerStore))
+                            st2(dst, v);
                     }
             }
             if (a.done) {
