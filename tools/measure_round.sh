@@ -44,7 +44,13 @@ print(c['variant'], c['zchunks'])")
   SFDB200_TILE=$1 SFDB200_ZCHUNKS=$2 timeout 600 python bench.py --workload cfg2 --time-steps 30 --steps 1 --warmup 3 --no-cpu --no-e2e > $OUT/short_cfg2.json 2>&1 && \
   SFDB200_TILE=$1 SFDB200_ZCHUNKS=$2 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $OUT/launches_cfg2.csv python bench.py --workload cfg2 --time-steps 30 --steps 1 --warmup 3 --no-cpu --no-e2e > $OUT/ncu_launch.log 2>&1
 fi
+[ -s $OUT/launches_cfg2.csv ] && python tools/launch_list.py $OUT/launches_cfg2.csv "ncu --metrics gpu__time_duration.sum --clock-control none -c 400 of: SFDB200_TILE/ZCHUNKS=<autotuned cfg2 pick> python bench.py --workload cfg2 --time-steps 30 --steps 1 --warmup 3 --no-cpu --no-e2e (cold-cache, serialised)" > $OUT/launches_cfg2.json
 cp profiles/ncu_summary.json $OUT/ncu_summary.json
 timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > $OUT/bench_reference_cfg2.json 2> $OUT/bench_reference_cfg2.err
 python tools/power_probe.py 4 > $OUT/power.jsonl 2>&1
+# gpurun merges at most 64 MiB back: keep the summaries, and only the cfg2 and
+# so-16 reports themselves
+for f in $OUT/*_full.ncu-rep; do
+  case $f in *cfg2_full*|*cfg4-so16_full*) ;; *) rm -f $f ;; esac
+done
 echo done
