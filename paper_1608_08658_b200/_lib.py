@@ -98,7 +98,12 @@ DEBUG_LIB_PATH = os.path.join(PKG_DIR, "libsfdb200_debug.so")
 def lib_path():
     """libsfdb200.so, or with SFDB200_LIBRARY=debug the build whose kernels
     check every global access they make (csrc/kernels.cuh SFDB_CHECK)."""
-    return DEBUG_LIB_PATH if os.environ.get("SFDB200_LIBRARY") == "debug" else LIB_PATH
+    sel = os.environ.get("SFDB200_LIBRARY", "")
+    if sel == "debug":
+        return DEBUG_LIB_PATH
+    if sel.endswith(".so"):  # an experiment build (tools/build_probe.sh)
+        return sel if os.path.isabs(sel) else os.path.join(PKG_DIR, sel)
+    return LIB_PATH
 
 
 def lib():

@@ -74,6 +74,13 @@ struct SweepArgs {
     // zdown_mask), so that chunks sharing a boundary read its planes at the
     // same time and the queue prologue hits L2.
     unsigned long long zdown;
+    // Pair kernel, one CTA per item, more tiles than resident slots: items are
+    // ordered in groups of `group` tiles (= the resident slots), all z chunks
+    // of a group in turn, chunk-major within it, every chunk streaming up; the
+    // slot a finished (tile, chunk k) frees is handed (in block order) to
+    // (tile, chunk k + 1), whose first 2R planes are the ones just read, still
+    // in L2.  0: tile-major order with zdown pairing.
+    int group;
     float w[kMaxRadius + 1];  // w_k / h^2
     float neg2nd;           // -2 * ndim
     float nidt2;            // -1 / dt^2
@@ -150,6 +157,8 @@ struct SweepConfig {        // 3-D tiling, chosen by choose_config()
                             // must match SweepArgs::ez != nullptr
     int ctas = 0;           // pair mapping: 0 = one CTA per (tile, z chunk) item, > 0 = that
                             // many persistent CTAs, < 0 = one per resident slot
+    int group = 1;          // pair mapping: grouped item order when tiles exceed the
+                            // resident slots (SweepArgs::group); SFDB200_GROUP=0 disables
     int tiles_x = 0, tiles_y = 0;
     size_t smem_bytes = 0;
     int ty() const { return 2 * by * ny; }

@@ -223,6 +223,7 @@ void choose_config(sfdb200_plan& p) {
     // Test knob: cap the persistent grid so every CTA runs many (tile, z chunk)
     // items (the multi-item path of sweep3d_pair_kernel on small grids).
     pick.ctas = env_int("SFDB200_CTAS", 0);
+    pick.group = env_int("SFDB200_GROUP", 1);
     p.cfg = pick;
 }
 

@@ -12,6 +12,10 @@
 
 #include "kernels.cuh"
 
+#ifndef SFDB200_PROBE
+#define SFDB200_PROBE 0
+#endif
+
 namespace sfdb200 {
 namespace detail {
 
@@ -507,6 +511,16 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
         } else {
             item -= a.nbi;
         }
+        const int tiles = ntx * nty;
+        if (bs < 0 && a.group > 0) {  // grouped order (SweepArgs::group)
+            const int zc = (nitems - a.nbi) / tiles;
+            const int g = item / (a.group * zc);
+            const int base = g * a.group;
+            const int gn = min(a.group, tiles - base);
+            const int rem = item - base * zc;
+            tz = rem / gn;
+            item = base + (rem - tz * gn) + tz * tiles;  // back to tile-major numbering
+        }
         const int r = item / ntx;
         x0 = (item - r * ntx) * T::TX;
         if (bs < 0) tz = r / nty;
@@ -683,12 +697,16 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
             // neighbours outside this thread's rows (yu[m] = row r0 - 1 - m,
             // yd[m] = row r0 + NY + m) are loaded at k = m + 1 and stay live for
             // NY iterations only, instead of all 2R of them for the whole plane.
+            // SFDB200_PROBE (experiments only, tools/build_probe.sh; wrong results):
+            // 1 = no x / y shared-memory reads, 2 = no y reads, 3 = no x reads.
+            constexpr bool PX = SFDB200_PROBE == 0 || SFDB200_PROBE == 2;
+            constexpr bool PY = SFDB200_PROBE == 0 || SFDB200_PROBE == 3;
             float w[NY][2 * WL + 2];
 #pragma unroll
             for (int jj = 0; jj < NY; ++jj)
 #pragma unroll
                 for (int m = 0; m <= WL; ++m) {
-                    const float2 v = ld2(hp + jj * T::BW - WL + 2 * m);
+                    const float2 v = PX ? ld2(hp + jj * T::BW - WL + 2 * m) : f2(0.0f, 0.0f);
                     w[jj][2 * m] = v.x;
                     w[jj][2 * m + 1] = v.y;
                 }
@@ -699,8 +717,8 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
             for (int jj = 0; jj < NY; ++jj) lap[jj] = lap2[jj] = f2(0.0f, 0.0f);
 #pragma unroll
             for (int k = 1; k <= R; ++k) {
-                yu[k - 1] = ld2(hp - k * T::BW);
-                yd[k - 1] = ld2(hp + (NY - 1 + k) * T::BW);
+                yu[k - 1] = PY ? ld2(hp - k * T::BW) : f2(0.0f, 0.0f);
+                yd[k - 1] = PY ? ld2(hp + (NY - 1 + k) * T::BW) : f2(0.0f, 0.0f);
 #pragma unroll
                 for (int jj = 0; jj < NY; ++jj) {
                     const float2 c0 = q[jj][slot(0)];
@@ -961,8 +979,15 @@ cudaError_t launch3d_pair_t(const FieldGeom& g, const SweepConfig& cfg, const Sw
     lc.attrs = at;
     lc.numAttrs = 1;
     SweepArgs b = a;
-    b.zdown = zdown_mask(cfg.tiles_x * cfg.tiles_y, cfg.zchunks,
-                         ctas < nitems ? ctas : static_cast<long long>(resident) * sms);
+    const long long slots = static_cast<long long>(resident) * sms;
+    const int tiles = cfg.tiles_x * cfg.tiles_y;
+    // cfg.group > 1 overrides the group size (test knob: the grouped order on
+    // grids smaller than the resident slots)
+    const long long gsize = cfg.group > 1 ? cfg.group : slots;
+    b.group = cfg.group && ctas == nitems && cfg.zchunks > 1 && tiles > gsize
+                  ? static_cast<int>(gsize)
+                  : 0;
+    b.zdown = b.group ? 0 : zdown_mask(tiles, cfg.zchunks, ctas < nitems ? ctas : slots);
     return cudaLaunchKernelEx(&lc, kern, m.uh, m.uc, m.c1, m.c2, m.ut, m.gr, b, g.Px, g.Py,
                               g.py, g.pz, cfg.tiles_x, cfg.tiles_y, nitems);
 }

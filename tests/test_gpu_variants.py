@@ -90,3 +90,42 @@ def test_persistent_multi_item(tile, ctas, zc):
     finally:
         os.environ.pop("SFDB200_CTAS", None)
         os.environ.pop("SFDB200_ZCHUNKS", None)
+
+
+@pytest.mark.parametrize("group,zc,so", [(3, 3, 8), (5, 4, 8), (7, 2, 16), (2, 2, 16)])
+def test_grouped_item_order(group, zc, so):
+    """The grouped item order (SweepArgs::group: tiles in groups of the
+    resident slots, every z chunk of a group in turn, all streaming up), forced
+    on a small grid with a small group size: forward (bitwise equal to the
+    tile-major order, the same arithmetic per point) and gradient."""
+    from paper_1608_08658_b200 import _lib as L
+    w = configs.cfg2(n=40, nt=62, nbpml=8, nrec_side=7) if so == 8 else \
+        configs.cfg4(so, n=40, nt=62, nbpml=8)
+    model = S.make_model(w.interior, w.h, w.nbpml, w.space_order, w.m_interior)
+    src = S.locate_points(model, w.src_coords)
+    rec = S.locate_points(model, w.rec_coords)
+    os.environ["SFDB200_ZCHUNKS"] = str(zc)
+    outs = []
+    try:
+        for g in (str(group), "0"):
+            os.environ["SFDB200_GROUP"] = g
+            _forced("4,2,4,4,1" if so == 8 else "4,2,4,2,1")
+            f = S.forward(model, src, w.wavelet, rec, w.nt, w.dt, False)
+            outs.append((f.u, f.record.data))
+        assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+        u, r = O.forward(model.padded, w.space_order, w.h, w.dt, w.nt, model.m, model.damp,
+                         src.idx, src.w, w.wavelet, rec.idx, rec.w)
+        assert O.rel_l2(outs[0][0], u) <= TOL and O.rel_l2(outs[0][1], r) <= TOL
+        if so == 8:
+            os.environ["SFDB200_GROUP"] = str(group)
+            us, rs = O.forward(model.padded, w.space_order, w.h, w.dt, w.nt, model.m,
+                               model.damp, src.idx, src.w, w.wavelet, rec.idx, rec.w, save=True)
+            resid = O._f64(np.random.default_rng(3).standard_normal(rs.shape).astype(np.float32))
+            gr = S.gradient(model, rec, S.ShotRecord(w.nt, w.dt, rec.npoints, resid), us, w.nt,
+                            w.dt)
+            go, _ = O.gradient(model.padded, w.space_order, w.h, w.dt, w.nt, model.m, model.damp,
+                               us, rec.idx, rec.w, resid)
+            assert O.rel_l2(gr.grad, go) <= TOL
+    finally:
+        os.environ.pop("SFDB200_ZCHUNKS", None)
+        os.environ.pop("SFDB200_GROUP", None)
