@@ -299,3 +299,56 @@ def test_p2p_abort_fails_every_rank(world, rank):
     for r, e in enumerate(errors):
         if abs(r - rank) <= 1:
             assert e == L.ECUDA, (r, errors)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_bench_slab_inputs_through_emulated_ranks(world, one_tiling):
+    """bench.py's N > 1 inputs on the device: each rank's slab problem
+    (bench.slab_problem: only its rows generated, global-shaped model arrays
+    written only in its planes) uploaded into its loopback plan, the ranks run
+    in lockstep with the fused P2P stores, assembled -- equal to one GPU on the
+    full cfg5-style model (a 40^3 interior here), bitwise (the four sources'
+    corners do not collide)."""
+    import torch
+    import types
+    import bench
+    from scipy.ndimage import gaussian_filter1d
+    one_tiling(16)
+    n = 40
+    raw = (1500.0 + 3000.0 * np.random.default_rng(1).random(n ** 3)).reshape(n, n, n)
+    for ax in range(3):
+        raw = gaussian_filter1d(raw, 16.0, axis=ax, mode="nearest", truncate=4.0)
+    lohi = (float(raw.min()), float(raw.max()))
+    args = types.SimpleNamespace(time_steps=60)
+    full = configs.cfg5(n=n, nt=62, nrec_side=8)
+    fm = S.make_model(full.interior, full.h, full.nbpml, 16, full.m_interior)
+    src, rec = S.locate_points(fm, full.src_coords), S.locate_points(fm, full.rec_coords)
+    wav = np.ascontiguousarray(full.wavelet.reshape(full.nt, -1))
+    ref = S.forward(fm, src, wav, rec, full.nt, full.dt, False)
+    stream = torch.cuda.Stream()
+    comms = [L.Comm.loopback(world, r, 0) for r in range(world)]
+    plans, outs = [], []
+    for r in range(world):
+        w, model = bench.slab_problem(L, S, args, world, r, n=n, minmax=lambda a, b: lohi)
+        p = L.Plan(L.FORWARD, 3, model.padded, 16, w.nt, w.dt, w.h, src.npoints, rec.npoints,
+                   False, 0, comm=comms[r])
+        p.set_stream(stream.cuda_stream)
+        u, tr = np.zeros((3, *model.padded)), np.zeros((w.nt, rec.npoints))
+        argv = [u, model.m, model.damp, src.idx, src.w, np.ascontiguousarray(w.wavelet), rec.idx,
+                rec.w, tr]
+        plans.append(p)
+        outs.append((argv, u, tr))
+    L.peer_group(plans)
+    for p, (argv, _, _) in zip(plans, outs):
+        p.upload(argv)
+    L.execute_group(plans)
+    u_sum, tr_sum = 0, 0
+    for p, (argv, u, tr) in zip(plans, outs):
+        p.download(argv)
+        u_sum = u_sum + u
+        tr_sum = tr_sum + tr
+    for p in plans:
+        p.close()
+    for c in comms:
+        c.close()
+    assert np.array_equal(u_sum, ref.u) and np.array_equal(tr_sum, ref.record.data)
