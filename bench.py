@@ -364,7 +364,8 @@ def slab_problem(L, S, args, world, rank, n=1024, minmax=None):
         import torch.distributed as dist
 
         def minmax(a, b):
-            t = torch.tensor([-a, b], dtype=torch.float64, device="cuda")
+            dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+            t = torch.tensor([-a, b], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             return -float(t[0]), float(t[1])
 

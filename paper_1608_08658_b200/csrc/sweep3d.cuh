@@ -1019,6 +1019,12 @@ cudaError_t launch3d_r(const FieldGeom& g, const SweepConfig& cfg, const SweepMa
     SFDB_P(4, 2, 4, MB2, 1, 0)
     SFDB_P(4, 2, 3, MB3, 1, 0)
     SFDB_P(8, 2, 3, (R <= 4 ? 2 : 1), 1, 0)
+    // eight consumer warps, one row per thread: a 32 x 16 tile with a third
+    // of the y halo of the 32 x 8 one (the gradient's six staged boxes)
+    if constexpr (R <= 4) {
+        SFDB_P(8, 1, 4, 3, 0, 1)
+        SFDB_P(8, 1, 3, 3, 0, 1)
+    }
     // partial unrolls (queue shifted every 2 / 3 / 4 / 5 / 8 planes); five
     // stages fit four CTAs per SM only in the separable layout
     SFDB_P(4, 2, 4, MB2, 2, 0)

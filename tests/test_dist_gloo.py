@@ -129,3 +129,46 @@ def test_slab_split_covers_the_updated_range():
         assert all(ends[i][1] == ends[i + 1][0] for i in range(world - 1))
         sizes = [b - a for a, b in ends]
         assert max(sizes) - min(sizes) <= 1
+
+
+def _slab_rank(rank, world, port, outdir):
+    """bench.py's N > 1 input generation on one gloo rank: its rows, the
+    rescale range all-reduced over the ranks, its planes of the model."""
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    import types
+    import torch
+    import bench
+    n = 24
+    w, model = bench.slab_problem(L, S, types.SimpleNamespace(time_steps=10), world, rank, n=n)
+    P = model.padded[0]
+    zb, ze = L.slab(P, 16, world, rank)
+    lo = 0 if rank == 0 else zb
+    hi = P if rank == world - 1 else ze
+    mg = np.zeros((P, P, P))
+    dg = np.zeros((P, P, P))
+    mg[lo:hi] = model.m.reshape(P, P, P)[lo:hi]
+    dg[lo:hi] = model.damp.reshape(P, P, P)[lo:hi]
+    mt, dt_ = torch.from_numpy(mg), torch.from_numpy(dg)
+    dist.all_reduce(mt)
+    dist.all_reduce(dt_)
+    if rank == 0:
+        np.savez(os.path.join(outdir, "slab.npz"), m=mt.numpy(), damp=dt_.numpy(), dt=w.dt)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_bench_slab_inputs_over_gloo_ranks(world):
+    """The per-rank cfg5 inputs of bench.py --gpus N, generated on gloo ranks
+    (real all-reduce of the rescale range), assemble to the whole model bit
+    for bit (configs.cfg5 + make_model, the reference's make_model /
+    build_damping)."""
+    full = configs.cfg5(n=24, nt=12, nrec_side=4)
+    model = S.make_model(full.interior, full.h, full.nbpml, 16, full.m_interior)
+    with tempfile.TemporaryDirectory() as d:
+        mp.start_processes(_slab_rank, args=(world, _free_port(), d), nprocs=world,
+                           start_method="spawn")
+        res = np.load(os.path.join(d, "slab.npz"))
+    assert float(res["dt"]) == full.dt
+    assert np.array_equal(res["m"].ravel(), model.m)
+    assert np.array_equal(res["damp"].ravel(), model.damp)
