@@ -1,8 +1,8 @@
 // TEST INFRASTRUCTURE (links the unmodified reference, oracle/_ref/libsfdref.so).
 //
 // The B200 backend as a drop-in under the reference's own operator API: the
-// UNMODIFIED sfd::seismic::forward / adjoint / gradient (seismic.cpp:333-496)
-// and sfd::verify::adjoint_test (verify.cpp:123-177) run once with the
+// UNMODIFIED sfd::seismic::forward / adjoint / gradient (seismic.cpp:333-496),
+// sfd::verify::adjoint_test and taylor_test (verify.cpp:123-297) run once with the
 // reference's generic preset (its own JIT-compiled OpenMP C: the oracle) and
 // once with sfdb200::stencilfd_preset (every generated kernel swapped for the
 // sfdb200_call shim by bin/sfdb200-jit inside runtime::compile_and_load,
@@ -213,6 +213,30 @@ int main(int argc, char** argv) {
         a3.nt = 200;
         const verify::AdjointReport r3 = verify::adjoint_test(a3);
         gate("verify::adjoint_test (" + r3.descriptor + ")", r3.rel_discrepancy, 1e-5);
+
+        // verify::taylor_test (verify.cpp:179-297) through both presets: the
+        // objective's first- and second-order Taylor slopes (1 +- 0.1, 2 +- 0.2).
+        // The step list is the caller's knob (TaylorConfig::steps): 0.04 .. 0.01
+        // of the default 2 % blob sit in the objective's near-linear regime
+        // (larger steps are not, for either preset) while
+        // |Phi(m + h dm) - Phi(m) - h <g, dm>| stays ~10x above the fp32 noise
+        // of Phi differences (~1e-4 here, measured); the default list goes down
+        // to 1e-4, where only fp64 arithmetic resolves e1.
+        for (int b200 = 0; b200 < 2; ++b200) {
+            verify::TaylorConfig tc;
+            tc.steps = {0.04, 0.02, 0.01};
+            if (b200) tc.run.preset = sfdb200::stencilfd_preset(root);
+            const verify::TaylorReport tr = verify::taylor_test(tc);
+            const bool ok = tr.passed;
+            if (!ok && b200) ++failures;
+            std::printf("{\"check\": \"verify::taylor_test (%s preset)\", \"slope0\": %.4f, "
+                        "\"slope1\": %.4f, \"gdot\": %.6e, \"phi0\": %.6e, \"ok\": %s}\n",
+                        b200 ? "b200" : "generic", tr.slope0, tr.slope1, tr.gdot, tr.phi0,
+                        ok ? "true" : "false");
+            for (const verify::TaylorPoint& p : tr.points)
+                std::printf("# taylor %s h %.4g e0 %.6e e1 %.6e%s\n", b200 ? "b200" : "generic",
+                            p.step, p.e0, p.e1, p.excluded ? " excluded" : "");
+        }
     } catch (const std::exception& e) {
         std::printf("{\"error\": \"%s\"}\n", e.what());
         return 1;
