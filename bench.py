@@ -67,9 +67,9 @@ def parse():
     ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
                     help="N>1 with cfg2: weak = one cfg2 slab per GPU, "
                          "strong = the cfg2 grid split over the GPUs")
-    ap.add_argument("--measure-1gpu", action="store_true",
-                    help="N>1: rank 0 also times the same workload on one GPU "
-                         "(config.one_gpu) for the parallel efficiency")
+    ap.add_argument("--no-1gpu", action="store_true",
+                    help="N>1: skip rank 0's one-GPU run of the same workload "
+                         "(config.one_gpu, the denominator of config.parallel_efficiency)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--checkpoint", type=int, default=0,
                     help="cfg3: checkpoint interval k (0 = whole history in HBM)")
@@ -611,7 +611,7 @@ def run_ours(args):
         cb.pop("seconds", None)
 
     one_gpu = None
-    if world > 1 and args.measure_1gpu:
+    if world > 1 and not args.no_1gpu:
         one_gpu = measure_one_gpu(args, rank, dist, torch)
 
     if rank == 0:
@@ -643,8 +643,11 @@ def run_ours(args):
 
 
 def measure_one_gpu(args, rank, dist, torch):
-    """Rank 0 times the same workload on its GPU alone (the other ranks wait):
-    the denominator of the strong-scaling efficiency."""
+    """Rank 0 times the same workload on its GPU alone while the other ranks
+    wait at a barrier: the denominator of the strong-scaling efficiency
+    (config.one_gpu; the driver computes its own from the per-N lines).  Same
+    method as `value`: warm-up execute, then one execute between CUDA events
+    on the plan's stream."""
     res = None
     if rank == 0:
         from paper_1608_08658_b200 import _lib as L
@@ -655,16 +658,22 @@ def measure_one_gpu(args, rank, dist, torch):
         rec = S.locate_points(model, w.rec_coords)
         p = L.Plan(L.FORWARD, 3, model.padded, w.space_order, w.nt, w.dt, w.h, src.npoints,
                    rec.npoints, False, int(os.environ.get("LOCAL_RANK", "0")))
-        p.upload([None, model.m, model.damp, src.idx, src.w, w.wavelet, rec.idx, rec.w,
-                  np.zeros((w.nt, rec.npoints))])
+        stream = torch.cuda.Stream()
+        p.set_stream(stream.cuda_stream)
+        p.upload([None, model.m, model.damp, src.idx, src.w, np.ascontiguousarray(w.wavelet),
+                  rec.idx, rec.w, np.zeros((w.nt, rec.npoints))])
         p.execute()
         torch.cuda.synchronize()
-        t0 = time.perf_counter()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
         p.execute()
+        e1.record(stream)
+        torch.cuda.synchronize()
         p.check()
-        el = time.perf_counter() - t0
-        res = {"workload": w.name, "value": w.points_per_step * p.steps / el / 1e9,
-               "timing": "one execute() on rank 0's GPU, host clock around a synchronised run"}
+        ms = e0.elapsed_time(e1)
+        res = {"workload": w.name, "value": w.points_per_step * p.steps / (ms / 1e3) / 1e9,
+               "ms_per_step": ms, "sweep": p.info().get("instantiation"),
+               "timing": "rank 0 alone, one execute() after a warm-up, CUDA events"}
         p.close()
         del model
     dist.barrier()
