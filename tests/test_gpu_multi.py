@@ -27,7 +27,7 @@ def test_two_ranks_bench_and_exchange(exchange):
     env = dict(os.environ, SFDB200_EXCHANGE=exchange)
     env.pop("WORLD_SIZE", None)
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2",
-                          "--time-steps", "10", "--steps", "1", "--warmup", "1", "--no-cpu"],
+                          "--time-steps", "10", "--steps", "1", "--warmup", "1", "--no-cpu", "--no-1gpu"],
                          capture_output=True, text=True, env=env, timeout=1800, cwd=ROOT)
     assert out.returncode == 0, out.stderr[-3000:]
     line = json.loads(out.stdout.strip().splitlines()[-1])
