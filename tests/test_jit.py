@@ -135,3 +135,22 @@ def test_unsupported_kernel_fails_the_compile(tmp_path):
     out, _ = _compile_like_reference(tmp_path, src, _preset_flags())
     assert out.returncode != 0
     assert "not a seismic forward / adjoint / gradient kernel" in out.stderr + out.stdout
+
+
+GOLDEN = "/root/reference/proj/tests/golden"
+
+
+@pytest.mark.skipif(not os.path.isdir(GOLDEN), reason="reference sources not present")
+def test_reference_golden_kernels(tmp_path):
+    """The reference's own golden emitted C (proj/tests/golden, pinned by its
+    acceptance test, acceptance.cpp:228-229): the Forward kernel reads back as
+    24^3 padded, so 2, nt 12, one source, two receivers, h = 0.1, dt = 1e-3;
+    the sparse-free `Plain` test kernel is not a seismic operator and is refused."""
+    d = _describe(tmp_path, open(os.path.join(GOLDEN, "forward_3d_full.c")).read())
+    assert (d["name"], d["kind"], d["ndim"], d["padded"]) == ("Forward", 0, 3, [24, 24, 24])
+    assert (d["space_order"], d["nt"], d["nsrc"], d["nrec"], d["save"]) == (2, 12, 1, 2, 0)
+    assert abs(d["h"] - 0.1) <= 1e-16 and abs(d["dt"] - 1e-3) <= 1e-18
+    path = tmp_path / "plain.c"
+    path.write_text(open(os.path.join(GOLDEN, "plain_2d_all_off.c")).read())
+    out = subprocess.run([JIT, "--describe", str(path)], capture_output=True, text=True)
+    assert out.returncode != 0 and "not a seismic" in out.stderr
