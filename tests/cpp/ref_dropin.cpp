@@ -14,6 +14,7 @@
 //
 //   ref_dropin <repo root>      (prints one JSON line per check; rc 0 = all pass)
 
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -188,13 +189,50 @@ void operators(const std::string& root, int ndim, int so, long nt) {
 
 }  // namespace
 
+// --bench: the cfg2 shape (256^3 interior + 40-point layer, so 8, 1000
+// steps, one source, 256 x 256 receivers) through the unmodified
+// seismic::forward with the B200 preset, three runs: the reference's own
+// RunStats (the timed kernel call, runtime.cpp:335-353) and the wall time of
+// the whole operator call (its host-side copies, allocation and check_finite
+// included) -- what a caller of the reference API gets end to end.
+int bench(const std::string& root) {
+    const std::vector<long> n{256, 256, 256};
+    const double h = 10.0;
+    seismic::VelocityModel model = seismic::make_model(n, h, 40, 8, slowness(n, 1500.0, 4500.0));
+    const double dt = 0.4 * h / 4500.0;
+    const long nt = 1002;
+    const double span = 255 * h;
+    std::vector<std::vector<double>> rec_c;
+    for (int j = 0; j < 256; ++j)
+        for (int i = 0; i < 256; ++i) rec_c.push_back({20.0, (j + 0.5) * span / 256, (i + 0.5) * span / 256});
+    const seismic::SparsePoints src = seismic::locate_points(model, {{10.0, span / 2, span / 2}});
+    const seismic::SparsePoints rec = seismic::locate_points(model, rec_c);
+    const std::vector<double> w = seismic::ricker(12.0, 0.1, nt, dt);
+    seismic::RunConfig gpu;
+    gpu.preset = sfdb200::stencilfd_preset(root);
+    const double pts = 336.0 * 336.0 * 336.0 * static_cast<double>(nt - 2);
+    for (int r = 0; r < 3; ++r) {
+        const auto t0 = std::chrono::steady_clock::now();
+        const seismic::ForwardResult f = seismic::forward(model, src, w, rec, nt, dt, false, gpu);
+        const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        std::printf("{\"bench\": \"cfg2 shape through sfd::seismic::forward, b200 preset\", \"run\": %d, "
+                    "\"kernel_call_s\": %.4f, \"gpts_kernel_call\": %.2f, \"operator_wall_s\": %.4f, "
+                    "\"gpts_operator_wall\": %.2f, \"reference_gflops\": %.1f}\n",
+                    r, f.stats.seconds, pts / f.stats.seconds / 1e9, wall, pts / wall / 1e9,
+                    f.stats.gflops);
+        std::fflush(stdout);
+    }
+    return 0;
+}
+
 int main(int argc, char** argv) {
     std::locale::global(std::locale::classic());
     if (argc < 2) {
-        std::fprintf(stderr, "usage: ref_dropin <repo root>\n");
+        std::fprintf(stderr, "usage: ref_dropin <repo root> [--bench]\n");
         return 2;
     }
     const std::string root = argv[1];
+    if (argc > 2 && std::string(argv[2]) == "--bench") return bench(root);
     try {
         operators(root, 3, 8, 160);
         operators(root, 3, 16, 90);
