@@ -21,6 +21,7 @@
 #include <algorithm>
 #include <cstring>
 #include <locale>
+#include <memory>
 #include <exception>
 #include <string>
 #include <vector>
@@ -136,6 +137,44 @@ int sfdref_forward(int ndim, const long* interior, double h, long nbpml, int so,
             m, src, std::vector<double>(src_trace, src_trace + nt * nsrc), rec, nt, dt,
             save != 0, config_of(portable));
         if (u_out) std::memcpy(u_out, f.u.data(), f.u.size() * sizeof(double));
+        if (rec_out)
+            std::memcpy(rec_out, f.record.data.data(), f.record.data.size() * sizeof(double));
+        if (seconds) *seconds = f.stats.seconds;
+    });
+}
+
+/// A model and its sparse sets built once (make_model, locate_points) and run
+/// many times: the reference arm of bench.py times seismic::forward on cfg5
+/// (1120^3), whose model construction alone takes seconds per call.
+struct RefProblem {
+    seismic::VelocityModel model;
+    seismic::SparsePoints src, rec;
+};
+
+void* sfdref_problem_create(int ndim, const long* interior, double h, long nbpml, int so,
+                            const double* m_interior, long nsrc, const double* src_coords,
+                            long nrec, const double* rec_coords) {
+    RefProblem* p = nullptr;
+    const int rc = guarded([&] {
+        auto q = std::make_unique<RefProblem>();
+        q->model = model_of(ndim, interior, h, nbpml, so, m_interior);
+        q->src = seismic::locate_points(q->model, coords_of(nsrc, ndim, src_coords));
+        q->rec = seismic::locate_points(q->model, coords_of(nrec, ndim, rec_coords));
+        p = q.release();
+    });
+    return rc == 0 ? p : nullptr;
+}
+
+void sfdref_problem_free(void* p) { delete static_cast<RefProblem*>(p); }
+
+/// seismic::forward on a created problem; rec_out / seconds may be null.
+int sfdref_problem_forward(void* prob, const double* src_trace, long nt, double dt,
+                           double* rec_out, double* seconds) {
+    return guarded([&] {
+        RefProblem& q = *static_cast<RefProblem*>(prob);
+        const seismic::ForwardResult f = seismic::forward(
+            q.model, q.src, std::vector<double>(src_trace, src_trace + nt * q.src.npoints), q.rec,
+            nt, dt, false, config_of(0));
         if (rec_out)
             std::memcpy(rec_out, f.record.data.data(), f.record.data.size() * sizeof(double));
         if (seconds) *seconds = f.stats.seconds;

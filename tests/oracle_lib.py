@@ -71,6 +71,9 @@ _REF_SIGS = {
     "sfdref_load_record": (_i, [C.c_char_p, _lp, _dp, _lp, C.POINTER(_i), _dp, _dp]),
     "sfdref_dump_grid": (_i, [_dp, _i, _lp, _L, _L, C.c_char_p]),
     "sfdref_objective": (_i, [_dp, _dp, _L, _dp, _dp]),
+    "sfdref_problem_create": (_P, [_i, _lp, _D, _L, _i, _dp, _L, _dp, _L, _dp]),
+    "sfdref_problem_free": (None, [_P]),
+    "sfdref_problem_forward": (_i, [_P, _dp, _L, _D, _dp, _dp]),
 }
 
 
@@ -350,6 +353,35 @@ def ref_generate(kind, interior, h, nbpml, so, m_interior, nsrc, nrec, nt, dt, s
     buf = C.create_string_buffer(need.value)
     _check_ref(ref().sfdref_generate(*args, buf, need.value, C.byref(need)))
     return buf.value.decode()
+
+
+class RefProblem:
+    """A reference model + sparse sets built once (sfdref_problem_create) and run
+    with seismic::forward many times (the reference arm's repeated samples)."""
+
+    def __init__(self, interior, h, nbpml, so, m_interior, src_coords, rec_coords):
+        interior = _i64(interior)
+        nd = len(interior)
+        self.src = _f64(src_coords).reshape(-1, nd)
+        self.rec = _f64(rec_coords).reshape(-1, nd)
+        self.handle = ref().sfdref_problem_create(
+            nd, _l(interior), C.c_double(h), C.c_long(nbpml), so, _d(_f64(m_interior).ravel()),
+            len(self.src), _d(self.src), len(self.rec), _d(self.rec))
+        if not self.handle:
+            raise ValueError(ref().sfdref_last_error().decode())
+
+    def forward(self, src_trace, nt, dt):
+        """RunStats.seconds of one seismic::forward call (kernel call incl. first touch)."""
+        secs = C.c_double()
+        _check_ref(ref().sfdref_problem_forward(self.handle, _d(_f64(src_trace).ravel()),
+                                                C.c_long(nt), C.c_double(dt), None,
+                                                _d_ref(secs)))
+        return secs.value
+
+    def close(self):
+        if self.handle:
+            ref().sfdref_problem_free(self.handle)
+            self.handle = None
 
 
 def ref_objective(syn, obs):
