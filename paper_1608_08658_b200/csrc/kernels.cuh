@@ -116,6 +116,7 @@ struct SweepArgs {
     // done_target) publishes sig_value to the neighbours' step counters
     // sig[0], sig[1] (system-scope release).  nbi = 0: no boundary items.
     int nbi;
+    int blen;               // planes per boundary item (its first / last R are sent)
     int bside[2];
     int bz[2];
     long long pdelta[2];

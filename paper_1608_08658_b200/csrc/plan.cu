@@ -140,6 +140,31 @@ void validate(const sfdb200_desc& d) {
     if (d.flags & ~SFDB200_F_GRAD_NO_ROW2) fail(SFDB200_EINVAL, "unknown descriptor flags");
 }
 
+// Boundary items: the R planes next to each neighbour are swept first and
+// exchanged while the interior runs.  The NCCL phase sweeps exactly those R
+// planes; a fused P2P launch lets each boundary item stream blen = k R planes
+// (k <= 3, the R planes it sends at the neighbour's end) so that thin slabs are
+// not split into many short items with a 2R-plane queue prologue each
+// (cfg5 at 8 ranks: the decomposition's own efficiency bound 88.6 % with one
+// R-plane item a side, tools/emulated_scaling.py).
+void set_boundary(sfdb200_plan& p, int Pz, int R, bool p2p) {
+    const int sides = (p.rank > 0 ? 1 : 0) + (p.rank < p.world - 1 ? 1 : 0);
+    const int owned = Pz - 2 * R;
+    int bl = R;
+    if (p2p && sides > 0)
+        for (int k = 3; k >= 2; --k)
+            if (owned - sides * k * R >= 2 * R + 4) {
+                bl = k * R;
+                break;
+            }
+    if (const int e = env_int("SFDB200_BLEN", 0); p2p && e >= R && owned - sides * e >= 1) bl = e;
+    p.blen = bl;
+    p.zint_lo = R + (p.rank > 0 ? bl : 0);
+    p.zint_hi = Pz - R - (p.rank < p.world - 1 ? bl : 0);
+    if (p.zint_hi <= p.zint_lo)
+        fail(SFDB200_EINVAL, "z slab too thin: each rank needs more than 2*(so/2) planes");
+}
+
 // Compiled sweep variants worth timing for radius R, best-first (B200
 // measurements, profiles/r01): the column-pair mapping throughout (8-byte
 // shared-memory reads, 8-byte stores); above R = 4 the z loop is unrolled by
@@ -266,12 +291,9 @@ void create(const sfdb200_desc& gd, Comm* comm, sfdb200_plan& p) {
     p.d = gd;
     p.d.padded[0] = (ze - zb) + 2 * R;
     const sfdb200_desc& d = p.d;
-    // Interior launch: all owned planes, minus the R boundary planes next to a
+    // Interior launch: all owned planes, minus the boundary planes next to a
     // neighbour (those are swept first and exchanged while the interior runs).
-    p.zint_lo = R + (p.rank > 0 ? R : 0);
-    p.zint_hi = static_cast<int>(d.padded[0]) - R - (p.rank < p.world - 1 ? R : 0);
-    if (p.zint_hi <= p.zint_lo)
-        fail(SFDB200_EINVAL, "z slab too thin: each rank needs more than 2*(so/2) planes");
+    set_boundary(p, static_cast<int>(d.padded[0]), R, false);
 
     FieldGeom& g = p.g;
     g.ndim = d.ndim;
@@ -797,11 +819,12 @@ void phase_interior(sfdb200_plan& p, long i, StepState& st) {
         if (p.cfg.pair != 1) fail(SFDB200_EINVAL, "the P2P exchange needs a column-pair tiling");
         const int R = g.R;
         c.nbi = nbi;
+        c.blen = p.blen;
         int grp = 0;
         for (int side = 0; side < 2; ++side) {
             if (!p.peer_field[side]) continue;
             c.bside[grp++] = side;
-            c.bz[side] = side == 0 ? R : g.Pz - 2 * R;
+            c.bz[side] = side == 0 ? R : g.Pz - R - p.blen;
             c.pdelta[side] = p2p_delta(p, side, st.a.row_out);
             c.peer_slot[side] = p.peer_slot[side];
             c.peer_row[side] = p.peer_field[side] + st.a.row_out * p.peer_slot[side];
@@ -1712,6 +1735,9 @@ int sfdb200_plan_ipc_import(sfdb200_plan* p, const void* lower, const void* uppe
         if (!p) fail(SFDB200_EINVAL, "null argument");
         ck(cudaSetDevice(p->d.device), "cudaSetDevice");
         p2p_import(*p, lower, upper);
+        set_boundary(*p, p->g.Pz, p->g.R, true);
+        p->tuned = false;
+        choose_config(*p);
     });
 }
 
@@ -1736,6 +1762,9 @@ int sfdb200_plan_peer_group(sfdb200_plan** plans, int n) {
             }
             p.p2p = true;
             p.p2p_sync = false;  // execute_group's lockstep phases order the steps
+            set_boundary(p, p.g.Pz, p.g.R, true);
+            p.tuned = false;
+            choose_config(p);
         }
     });
 }

@@ -140,6 +140,7 @@ struct sfdb200_plan {
     int world = 1, rank = 0;
     long zoff = 0;
     int zint_lo = 0, zint_hi = 0;  // interior sweep launch (local planes)
+    int blen = 0;                  // planes per boundary item (plan.cu set_boundary)
     int ctas2d = 0;                // 2-D: cooperative time-loop grid
     int nc2d = 0;                  // 2-D: CTAs of the single-cluster time loop (0: cooperative)
     long long per_cta2d = 0;       // 2-D: updated points per CTA

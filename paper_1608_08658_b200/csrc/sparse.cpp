@@ -31,10 +31,11 @@ Owner owner_of(const sfdb200_plan& p, long zl, long y, long x) {
     const int tile = bx + c.tiles_x * by, tiles = c.tiles_x * c.tiles_y;
     const int nbi = p2p_boundary_items(p);
     if (nbi) {
-        const bool lo = p.rank > 0 && zl >= R && zl < 2 * R;
-        const bool hi = p.rank < p.world - 1 && zl >= p.g.Pz - 2 * R && zl < p.g.Pz - R;
+        const int hb = p.g.Pz - R - p.blen;  // first plane of the upper boundary items
+        const bool lo = p.rank > 0 && zl >= R && zl < R + p.blen;
+        const bool hi = p.rank < p.world - 1 && zl >= hb && zl < p.g.Pz - R;
         if (lo) return {tile, static_cast<int>(zl - R)};
-        if (hi) return {(p.rank > 0 ? tiles : 0) + tile, static_cast<int>(zl - (p.g.Pz - 2 * R))};
+        if (hi) return {(p.rank > 0 ? tiles : 0) + tile, static_cast<int>(zl - hb)};
     }
     const long zr = zl - p.zint_lo;
     const int bz = static_cast<int>(zr / c.zlen);
@@ -48,8 +49,8 @@ bool in_interior(const sfdb200_plan& p, long zl, long y, long x) {
     if (!in_xy) return false;
     if (zl >= p.zint_lo && zl < p.zint_hi) return true;
     if (!p2p_boundary_items(p)) return false;
-    return (p.rank > 0 && zl >= R && zl < 2 * R) ||
-           (p.rank < p.world - 1 && zl >= p.g.Pz - 2 * R && zl < p.g.Pz - R);
+    return (p.rank > 0 && zl >= R && zl < R + p.blen) ||
+           (p.rank < p.world - 1 && zl >= p.g.Pz - R - p.blen && zl < p.g.Pz - R);
 }
 
 int ctas_of(const sfdb200_plan& p) {

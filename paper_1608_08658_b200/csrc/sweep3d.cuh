@@ -527,7 +527,7 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
         y0 = R + (r - tz * nty) * T::TY;
         if (bs >= 0) {
             zb = a.bz[bs];
-            ze = zb + R;
+            ze = zb + a.blen;
         } else {
             zb = a.zlo + tz * a.zchunk;
             ze = min(zb + a.zchunk, a.zhi);
@@ -812,7 +812,8 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
             const long long pd = a.pdelta[bs];
             const char* c = reinterpret_cast<const char*>(
                 a.out + static_cast<long long>(z0) * pz + static_cast<long long>(y0 + r0) * py + x);
-            for (int i = 0; i < n; ++i) {
+            // the R planes at the neighbour's end of the item (it streams up)
+            for (int i = bs == 0 ? 0 : n - R; i < (bs == 0 ? R : n); ++i) {
                 const char* cp = c + static_cast<long long>(i) * planeb;
 #pragma unroll
                 for (int jj = 0; jj < NY; ++jj)
