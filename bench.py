@@ -194,7 +194,8 @@ def ncu_traffic(workload, info, ndim):
     tiling the bench autotuned to has no capture."""
     if ndim != 3:
         return None, "2-D: L2 / shared-memory resident, no DRAM roofline"
-    key = f"{workload}|{info.get('instantiation')}|z{info.get('zchunks')}"
+    key = f"{workload}|{info.get('instantiation')}|z{info.get('zchunks')}" + \
+        ("|dyn" if info.get("ctas") == -2 else "")
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(p) as fh:

@@ -127,6 +127,11 @@ struct SweepArgs {
     // This rank's sticky broken flag (P2P with step counters): once set, the
     // boundary items skip their peer stores and the step publication.
     const unsigned int* broken;
+    // Pair kernel, dynamic persistent mode (SweepConfig::ctas == -2, separable
+    // layout): the producer lane of each resident CTA takes the next item from
+    // this counter and stages its index with the item's first plane; the CTA
+    // taking the launch's last fetch resets it to 0 for the next launch.
+    unsigned long long* item_ctr;
     // Debug checks (SFDB_CHECK): elements per row of this plan's fields and
     // of the neighbours' (P2P), the neighbours' rows written this step, the flag.
     long long slot;
@@ -157,7 +162,9 @@ struct SweepConfig {        // 3-D tiling, chosen by choose_config()
     int sep = 1;            // pair mapping: separable-damping stage layout (no c1 box);
                             // must match SweepArgs::ez != nullptr
     int ctas = 0;           // pair mapping: 0 = one CTA per (tile, z chunk) item, > 0 = that
-                            // many persistent CTAs, < 0 = one per resident slot
+                            // many persistent CTAs, -1 = one per resident slot (items
+                            // round robin), -2 = one per resident slot taking items from
+                            // a counter (SweepArgs::item_ctr; separable layout)
     int group = 1;          // pair mapping: grouped item order when tiles exceed the
                             // resident slots (SweepArgs::group); SFDB200_GROUP=0 disables
     int tiles_x = 0, tiles_y = 0;

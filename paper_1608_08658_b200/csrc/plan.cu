@@ -53,6 +53,7 @@ sfdb200_plan::~sfdb200_plan() {
     cudaFree(ck_store);
     cudaFree(flag);
     cudaFree(dbg);
+    cudaFree(item_ctr);
     if (own_hist) cudaFree(hist);
     cudaFree(grad);
     for (SparseDev* s : {&src, &rec}) {
@@ -333,6 +334,9 @@ void create(const sfdb200_desc& gd, Comm* comm, sfdb200_plan& p) {
     if (p.grad_kind()) p.grad = dalloc<float>(static_cast<size_t>(g.slot));
     p.counter = dalloc<unsigned long long>(1);
     p.flag = dalloc<unsigned int>(1);
+    p.item_ctr = dalloc<unsigned long long>(1);  // dynamic persistent sweeps
+    ck(cudaMemsetAsync(p.item_ctr, 0, sizeof(unsigned long long), p.stream), "memset");
+    p.base.item_ctr = p.item_ctr;
     p.dbg = dalloc<unsigned int>(1);  // debug builds: the first failed access check
     ck(cudaMemsetAsync(p.dbg, 0, sizeof(unsigned int), p.stream), "memset");
     p.base.dbg = p.dbg;
@@ -507,6 +511,41 @@ void autotune(sfdb200_plan& p) {
             if (c.zchunks != zc) continue;
             int occ = 0;
             if (sweep3d_occupancy(p.g, c, p.grad_kind(), &occ) != cudaSuccess || occ < 1) continue;
+            p.cfg = c;
+            build_maps(p);
+            a.zchunk = c.zlen;
+            float t = 1e30f;
+            for (int rep = 0; rep < 4; ++rep) {
+                ck(cudaEventRecord(e0, p.stream), "event");
+                ck(launch_sweep3d(p.g, c, p.maps, a, p.grad_kind(), p.stream), "autotune");
+                ck(cudaEventRecord(e1, p.stream), "event");
+                ck(cudaEventSynchronize(e1), "autotune");
+                float ms = 0;
+                ck(cudaEventElapsedTime(&ms, e0, e1), "elapsed");
+                if (rep > 0) t = std::min(t, ms);
+            }
+            if (t < best) {
+                best = t;
+                pick = c;
+            }
+            p.cands.emplace_back(t, c);
+        }
+    }
+    // Dynamic persistent form (one CTA per resident slot taking items from a
+    // counter, SweepConfig::ctas = -2) of the fastest separable pair tilings:
+    // it hides each item's start behind the previous one, which pays where
+    // items are short (thin z slabs at many ranks).
+    {
+        std::vector<std::pair<float, SweepConfig>> top(p.cands);
+        std::stable_sort(top.begin(), top.end(),
+                         [](const auto& x, const auto& y) { return x.first < y.first; });
+        int tried = 0;
+        for (const auto& tc : top) {
+            if (tried == 3 || !env_int("SFDB200_DYNAMIC", 1)) break;
+            if (!tc.second.pair || !tc.second.sep || tc.second.ctas != 0) continue;
+            ++tried;
+            SweepConfig c = tc.second;
+            c.ctas = -2;
             p.cfg = c;
             build_maps(p);
             a.zchunk = c.zlen;
@@ -1829,7 +1868,7 @@ int sfdb200_plan_info(const sfdb200_plan* p, char* buf, long len) {
                       "\"smem_bytes\": %zu, \"fused_sparse\": %s, \"slab\": [%ld, %ld], "
                       "\"x_pitch\": %d, \"mapping\": \"%s\", \"pdl\": %s, "
                       "\"separable_damping\": %s, \"bytes_per_point\": %d, \"cluster2d_ctas\": %d, \"z_unroll\": %d, \"variant\": \"%d,%d,%d,%d,%d\", "
-                      "\"instantiation\": \"%s\"}",
+                      "\"instantiation\": \"%s\", \"ctas\": %d}",
                       c.ty(), c.by + 1, 2 * c.ny, c.stages, c.tiles_x, c.tiles_y, c.zchunks,
                       c.zlen, c.smem_bytes, p->fused ? "true" : "false", p->zoff + p->g.R,
                       p->zoff + p->g.Pz - p->g.R, p->g.XP,
@@ -1842,7 +1881,8 @@ int sfdb200_plan_info(const sfdb200_plan* p, char* buf, long len) {
                       c.rot == 1 ? 2 * p->g.R + 1 : (c.rot == 0 ? 1 : c.rot), c.by, c.ny,
                       c.stages, c.rot, c.pair,
                       p->g.ndim == 3 ? sweep3d_instantiation(p->g, c, p->grad_kind()).c_str()
-                                     : (p->nc2d ? "cluster2d_kernel" : "loop2d_kernel"));
+                                     : (p->nc2d ? "cluster2d_kernel" : "loop2d_kernel"),
+                      c.ctas);
     });
 }
 

@@ -198,6 +198,7 @@ struct sfdb200_plan {
     unsigned long long* counter = nullptr;
     unsigned int* flag = nullptr;
     unsigned int* dbg = nullptr;  // debug builds: first failed access check (kernels.cuh)
+    unsigned long long* item_ctr = nullptr;  // dynamic persistent sweeps (SweepArgs::item_ctr)
 
     cudaStream_t own_stream = nullptr;
     cudaStream_t stream = nullptr;

@@ -488,6 +488,7 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
     using T = Tile<R, BY, NY, GRAD, SEP>;
     constexpr int Q = T::Q;
     constexpr int WL = (R + 1) & ~1;  // x window [x - WL, x + 1 + WL], 8-byte aligned
+    const bool dyn = SEP && a.item_ctr != nullptr;  // dynamic persistent mode
     constexpr bool SST = UN % S == 0;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     float* smem = reinterpret_cast<float*>(smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u));
@@ -556,17 +557,29 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
                 if (j >= S) mbar_wait(&empty[st], ((j / S) - 1) & 1);
                 return st;
             };
-            for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
-                int x0, y0, zb, ze, z0, dz, bs;
-                decode(item, x0, y0, zb, ze, z0, dz, bs);
-                const int n = ze - zb;
-                if (n <= 0) continue;
+            // Dynamic mode: items from the counter, each item's index staged
+            // with its first plane; the last fetch of the launch resets it.
+            auto fetch = [&]() -> int {
+                const unsigned long long v = atomicAdd(a.item_ctr, 1ull);
+                if (v + 1 == static_cast<unsigned long long>(nitems) + gridDim.x)
+                    atomicExch(a.item_ctr, 0ull);
+                return v < static_cast<unsigned long long>(nitems) ? static_cast<int>(v) : nitems;
+            };
+            auto align = [&]() {
                 if constexpr (SST) {
                     while (j % S != 0) {  // skip stage: completes on the arrive alone
                         mbar_arrive(&full[acquire()]);
                         ++j;
                     }
                 }
+            };
+            for (int item = dyn ? fetch() : blockIdx.x; item < nitems;
+                 item = dyn ? fetch() : item + gridDim.x) {
+                int x0, y0, zb, ze, z0, dz, bs;
+                decode(item, x0, y0, zb, ze, z0, dz, bs);
+                const int n = ze - zb;
+                if (n <= 0) continue;
+                align();
                 const float* ezp = SEP ? a.ez + z0 : nullptr;
                 float nxt = 0.0f;
                 if constexpr (SEP) nxt = -__ldg(ezp);
@@ -585,9 +598,13 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
                                               z + dz * R < planes,
                                    kDbgTmaPlane);
                     }
-                    // SEP: -ez[z] rides in the stage, ordered before the consumers'
-                    // acquire by the release of this arrive.
-                    if constexpr (SEP) sb[T::O_NEZ] = cur;
+                    // SEP: -ez[z] (and in dynamic mode the item index, with the
+                    // item's first plane) ride in the stage, ordered before the
+                    // consumers' acquire by the release of this arrive.
+                    if constexpr (SEP) {
+                        sb[T::O_NEZ] = cur;
+                        if (dyn && i == 0) sb[T::O_NEZ + 1] = __int_as_float(item);
+                    }
                     mbar_arrive_expect_tx(bar, T::BYTES);
                     tma_load_4d(sb, &tm_uh, x0 - T::RA, y0 - R, z, a.row_u1, bar);
                     tma_load_4d(sb + T::O_U1C, &tm_uc, x0, y0, z + dz * R, a.row_u1, bar);
@@ -600,6 +617,13 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
                     }
                     ++j;
                 }
+            }
+            if (dyn) {  // end of work: a stage holding index -1, no transfer
+                align();
+                const int st = acquire();
+                smem[st * T::SF + T::O_NEZ + 1] = __int_as_float(-1);
+                mbar_arrive(&full[st]);
+                ++j;
             }
         }
         return;
@@ -623,11 +647,7 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
     const long long gdiff = GRAD ? reinterpret_cast<char*>(a.grad) - reinterpret_cast<char*>(a.out) : 0;
     uint32_t j = 0;  // stage sequence number, as the producer's
 
-    for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
-        int x0, y0, zb, ze, z0, dz, bs;
-        decode(item, x0, y0, zb, ze, z0, dz, bs);
-        const int n = ze - zb;
-        if (n <= 0) continue;
+    auto align = [&]() {
         if constexpr (SST) {
             while (j % S != 0) {
                 const int st = static_cast<int>(j % S);
@@ -637,6 +657,22 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
                 ++j;
             }
         }
+    };
+    for (int item = blockIdx.x;; item += gridDim.x) {
+        if (dyn) {  // the next item's index rides in its first stage
+            align();
+            const int st = static_cast<int>(j % S);
+            mbar_wait(&full[st], (j / S) & 1);
+            item = __float_as_int(smem[st * T::SF + T::O_NEZ + 1]);
+            if (item < 0) break;
+        } else if (item >= nitems) {
+            break;
+        }
+        int x0, y0, zb, ze, z0, dz, bs;
+        decode(item, x0, y0, zb, ze, z0, dz, bs);
+        const int n = ze - zb;
+        if (n <= 0) continue;
+        align();
         const int x = x0 + 2 * px;
         // Queue slot of plane z0 + dz (t - R) is t (t < 2R), loaded directly
         // (the loads overlap the producer filling the ring with the item's
@@ -966,9 +1002,12 @@ cudaError_t launch3d_pair_t(const FieldGeom& g, const SweepConfig& cfg, const Sw
     const int nitems = cfg.tiles_x * cfg.tiles_y * cfg.zchunks + a.nbi;  // + P2P boundary tiles
     // cfg.ctas: 0 = one CTA per item (the hardware hands items to free slots
     // dynamically), > 0 = that many persistent CTAs, < 0 = one per resident slot.
-    const int ctas = cfg.ctas > 0   ? std::min(cfg.ctas, nitems)
-                     : cfg.ctas < 0 ? std::min(nitems, resident * sms)
-                                    : nitems;
+    // (the dynamic mode needs the separable stage layout's spare slot for the
+    // item index; without it, or without a counter, one CTA per item)
+    const bool dyn = cfg.ctas == -2 && SEP && a.item_ctr;
+    const int ctas = cfg.ctas > 0           ? std::min(cfg.ctas, nitems)
+                     : (cfg.ctas == -1 || dyn) ? std::min(nitems, resident * sms)
+                                               : nitems;
     cudaLaunchConfig_t lc{};
     lc.gridDim = dim3(static_cast<unsigned>(ctas));  // CTA c: items c, c + ctas, ...
     lc.blockDim = dim3(32, BY + 1);
@@ -980,6 +1019,7 @@ cudaError_t launch3d_pair_t(const FieldGeom& g, const SweepConfig& cfg, const Sw
     lc.attrs = at;
     lc.numAttrs = 1;
     SweepArgs b = a;
+    if (!dyn) b.item_ctr = nullptr;
     const long long slots = static_cast<long long>(resident) * sms;
     const int tiles = cfg.tiles_x * cfg.tiles_y;
     // cfg.group > 1 overrides the group size (test knob: the grouped order on

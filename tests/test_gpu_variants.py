@@ -129,3 +129,40 @@ def test_grouped_item_order(group, zc, so):
     finally:
         os.environ.pop("SFDB200_ZCHUNKS", None)
         os.environ.pop("SFDB200_GROUP", None)
+
+
+@pytest.mark.parametrize("so,zc", [(8, 3), (16, 2), (4, 4)])
+def test_dynamic_persistent_items(so, zc):
+    """Dynamic persistent sweeps (SweepConfig::ctas = -2: one CTA per resident
+    slot taking (tile, z chunk) items from a counter, the item index staged
+    with the item's first plane, an end-of-work stage): forward bitwise equal to
+    one CTA per item, gradient against the oracle."""
+    w = configs.cfg2(n=40, nt=62, nbpml=8, nrec_side=7) if so == 8 else \
+        configs.cfg4(so, n=40, nt=62, nbpml=8)
+    model = S.make_model(w.interior, w.h, w.nbpml, w.space_order, w.m_interior)
+    src = S.locate_points(model, w.src_coords)
+    rec = S.locate_points(model, w.rec_coords)
+    os.environ["SFDB200_ZCHUNKS"] = str(zc)
+    outs = []
+    try:
+        for ctas in ("-2", "0"):
+            os.environ["SFDB200_CTAS"] = ctas
+            _forced("4,2,4,4,1" if so != 16 else "4,2,4,2,1")
+            f = S.forward(model, src, w.wavelet, rec, w.nt, w.dt, False)
+            outs.append((f.u, f.record.data))
+        assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+        u, r = O.forward(model.padded, w.space_order, w.h, w.dt, w.nt, model.m, model.damp,
+                         src.idx, src.w, w.wavelet, rec.idx, rec.w)
+        assert O.rel_l2(outs[0][0], u) <= TOL and O.rel_l2(outs[0][1], r) <= TOL
+        if so == 8:
+            os.environ["SFDB200_CTAS"] = "-2"
+            us, rs = O.forward(model.padded, w.space_order, w.h, w.dt, w.nt, model.m,
+                               model.damp, src.idx, src.w, w.wavelet, rec.idx, rec.w, save=True)
+            resid = O._f64(np.random.default_rng(3).standard_normal(rs.shape).astype(np.float32))
+            g = S.gradient(model, rec, S.ShotRecord(w.nt, w.dt, rec.npoints, resid), us, w.nt, w.dt)
+            go, _ = O.gradient(model.padded, w.space_order, w.h, w.dt, w.nt, model.m, model.damp,
+                               us, rec.idx, rec.w, resid)
+            assert O.rel_l2(g.grad, go) <= TOL
+    finally:
+        os.environ.pop("SFDB200_ZCHUNKS", None)
+        os.environ.pop("SFDB200_CTAS", None)

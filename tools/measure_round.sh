@@ -21,8 +21,9 @@ capture() {  # workload, bench line, extra tool args
   [ -s $line ] || return
   set -- $(python -c "
 import json; d=json.loads(open('$line').read().strip().splitlines()[-1]); c=d['config']['sweep']
-print(c['variant'], c['zchunks'])")
+print(c['variant'], c['zchunks'], c.get('ctas', 0))")
   local tile=$1 zc=$2
+  export SFDB200_CTAS=$3
   if [ $wl = cfg3 ]; then
     SFDB200_TILE=$tile SFDB200_ZCHUNKS=$zc timeout 600 python tools/tune.py --workload cfg3 --gradient --time-steps 8 --tiles $tile --zchunks $zc --reps 1 > $OUT/ncu_pre_$wl.log 2>&1 && \
     SFDB200_TILE=$tile SFDB200_ZCHUNKS=$zc timeout 900 ncu --set full --import-source on --clock-control none -k regex:sweep3d --launch-skip 4 --launch-count 1 -o $OUT/${wl}_full python tools/tune.py --workload cfg3 --gradient --time-steps 8 --tiles $tile --zchunks $zc --reps 1 > $OUT/ncu_$wl.log 2>&1
@@ -32,6 +33,7 @@ print(c['variant'], c['zchunks'])")
   fi
   python tools/ncu_summary.py $OUT/${wl}_full.ncu-rep > $OUT/ncu_${wl}_full.json
   python tools/ncu_traffic.py $OUT/${wl}_full.ncu-rep $line profiles/${OUT#gpurun_out/}/ncu_${wl}_full.json > $OUT/ncu_traffic_$wl.json
+  unset SFDB200_CTAS
 }
 for wl in $WLS; do
   case $wl in cfg1) ;; *) capture $wl $OUT/bench_$wl.json ;; esac

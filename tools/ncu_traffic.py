@@ -46,7 +46,8 @@ def main(rep, line_path, source):
         d = json.load(open(p))
     except Exception:
         d = {}
-    d.setdefault("captures", {})[f"{name}|{inst}|z{zc}"] = got
+    key = f"{name}|{inst}|z{zc}" + ("|dyn" if sweep.get("ctas") == -2 else "")
+    d.setdefault("captures", {})[key] = got
     d["_key"] = "<workload>|<kernel instantiation>|z<zchunks> (bench.py ncu_traffic)"
     json.dump(d, open(p, "w"), indent=1)
     print(json.dumps(got))
