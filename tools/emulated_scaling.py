@@ -26,6 +26,9 @@ def main():
     ap.add_argument("--workload", default="cfg5")
     ap.add_argument("--time-steps", type=int, default=50)
     ap.add_argument("--ranks", default="2,4,8")
+    ap.add_argument("--no-p2p", action="store_true",
+                    help="ghost planes by device copies between the plans (the planes the "
+                         "NCCL exchange sends) instead of the fused P2P launch")
     args = ap.parse_args()
     import torch
     import bench
@@ -70,7 +73,8 @@ def main():
                        src.npoints, rec.npoints, False, 0, comm=comms[r])
             q.set_stream(stream.cuda_stream)
             plans.append(q)
-        L.peer_group(plans)
+        if not args.no_p2p:
+            L.peer_group(plans)
         for q in plans:
             q.upload(argv())
         ms = timed(lambda: L.execute_group(plans))
