@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <initializer_list>
 #include <mutex>
 #include <string>
@@ -919,6 +920,27 @@ inline std::string kernel_name(const char* base, std::initializer_list<int> args
     return s + ">";
 }
 
+// Shared-memory carveout of the sweep kernels.  The gradient kernels ask for
+// the whole array as shared memory: with the driver's choice cfg3's gradient
+// sweep ran 4 CTAs per SM where its registers allow 5 (115 vs 110 us per
+// sweep, +3-5 % Gpts/s, profiles/r02p).  The forward kernels are register-
+// limited at the driver's carveout and keep it (all-shared measured neutral
+// to -2 %, the smaller L1).  SFDB200_CARVEOUT (percent; -1 = the driver's
+// choice) overrides both.
+template <typename K>
+cudaError_t set_sweep_attrs(K kern, size_t smem, bool grad) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    static const int env = [] {
+        const char* v = std::getenv("SFDB200_CARVEOUT");
+        return v && *v ? std::atoi(v) : -2;
+    }();
+    const int pct = env != -2 ? env : grad ? static_cast<int>(cudaSharedmemCarveoutMaxShared) : -1;
+    if (pct < 0) return cudaSuccess;
+    return cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+}
+
 // occ != nullptr: report resident CTAs per SM instead of launching.
 template <int R, int BY, int NY, int S, bool GRAD>
 cudaError_t launch3d_t(const FieldGeom& g, const SweepConfig& cfg, const SweepMaps& m,
@@ -929,8 +951,7 @@ cudaError_t launch3d_t(const FieldGeom& g, const SweepConfig& cfg, const SweepMa
         return cudaSuccess;
     }
     const size_t smem = sweep3d_smem_bytes(R, cfg, GRAD);
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
+    cudaError_t e = set_sweep_attrs(kern, smem, GRAD);
     if (e != cudaSuccess) return e;
     if (occ) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, kern, 32 * (BY + 1), smem);
     cudaLaunchConfig_t lc{};
@@ -978,8 +999,7 @@ cudaError_t launch3d_pair_t(const FieldGeom& g, const SweepConfig& cfg, const Sw
     {
         std::lock_guard<std::mutex> lk(cache.mu);
         if (occ || cache.smem[dev] != smem) {
-            e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(smem));
+            e = set_sweep_attrs(kern, smem, GRAD);
             if (e != cudaSuccess) return e;
             int r = 0;
             e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&r, kern, 32 * (BY + 1), smem);
