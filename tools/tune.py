@@ -70,7 +70,7 @@ def main():
             step_ms = e0.elapsed_time(e1) / plan.steps
             gbs = plan.info()["bytes_per_point"] * plan.points_per_step / (best / 1e3) / 1e9
             print(json.dumps({"workload": w.name, "tile": tile, "zchunks": zc,
-                              "sweep_ms": best, "cfg": plan.info(), "gpts": plan.points_per_step / best / 1e6,
+                              "sweep_ms": best, "step_ms": step_ms, "cfg": plan.info(), "gpts": plan.points_per_step / best / 1e6,
                               "alg_GBps": gbs}), flush=True)
             plan.close()
 
