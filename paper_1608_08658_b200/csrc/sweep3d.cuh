@@ -763,8 +763,15 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
                         jj - k >= 0 ? q[(jj - k) >= 0 ? jj - k : 0][slot(0)] : yu[k - jj - 1];
                     const float2 yp =
                         jj + k < NY ? q[(jj + k) < NY ? jj + k : 0][slot(0)] : yd[jj + k - NY];
-                    const float2 xs = add2(f2(w[jj][WL - k], w[jj][WL - k + 1]),
-                                           f2(w[jj][WL + k], w[jj][WL + k + 1]));
+                    // (x - k, x + 1 - k) straddles two loaded pairs when WL - k is
+                    // odd: two scalar adds (same rounding) instead of moves that
+                    // re-pair the operands for one packed add
+                    const float2 xs =
+                        ((WL - k) & 1)
+                            ? f2(__fadd_rn(w[jj][WL - k], w[jj][WL + k]),
+                                 __fadd_rn(w[jj][WL - k + 1], w[jj][WL + k + 1]))
+                            : add2(f2(w[jj][WL - k], w[jj][WL - k + 1]),
+                                   f2(w[jj][WL + k], w[jj][WL + k + 1]));
                     const float2 zs = add2(q[jj][slot(-k)], q[jj][slot(k)]);
                     float2 sk = add2(add2(xs, add2(ym, yp)), zs);
                     sk = fma2(neg2nd, c0, sk);
