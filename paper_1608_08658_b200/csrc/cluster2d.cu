@@ -177,8 +177,13 @@ __global__ void __launch_bounds__(Shape<GRAD>::NT, 1) cluster2d_kernel(const Clu
                     float2 lap = f2(0.f, 0.f);
 #pragma unroll
                     for (int k = 1; k <= R; ++k) {
-                        const float2 xs = add2(f2(w[WL - k], w[WL - k + 1]),
-                                               f2(w[WL + k], w[WL + k + 1]));
+                        // misaligned pairs: two scalar adds (same rounding) instead of
+                        // re-pairing moves + one packed add, as in the 3-D pair sweep
+                        const float2 xs = ((WL - k) & 1)
+                                              ? f2(__fadd_rn(w[WL - k], w[WL + k]),
+                                                   __fadd_rn(w[WL - k + 1], w[WL + k + 1]))
+                                              : add2(f2(w[WL - k], w[WL - k + 1]),
+                                                     f2(w[WL + k], w[WL + k + 1]));
                         const float2 zs = add2(zw[j + R - k], zw[j + R + k]);
                         float2 s = add2(xs, zs);
                         s = fma2(neg2nd, c0, s);
