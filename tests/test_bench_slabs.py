@@ -57,3 +57,32 @@ def test_slab_model_planes_equal_the_full_model(world):
         # nothing outside the slab was written (those pages stay unbacked)
         assert not mv[:z0].any() and not mv[z1:].any()
     assert v.shape == (n, n, n)
+
+
+def test_reference_sample_is_cropped_to_host_memory(monkeypatch):
+    """bench.py's reference arm: on a host that cannot hold the reference's fp64
+    grids of the workload, the sample keeps the x / y extents, sources and
+    receivers and crops the interior along z (and says so); otherwise the
+    workload is untouched."""
+    import builtins
+    w = configs.cfg2(n=64, nt=12)
+    same, note = bench.fit_reference_to_memory(w)
+    assert same is w and note == ""
+    real_open = builtins.open
+
+    class Meminfo:
+        def __enter__(self):
+            return iter(["MemTotal: 1 kB\n", "MemAvailable: 600000 kB\n"])
+
+        def __exit__(self, *a):
+            return False
+
+    monkeypatch.setattr(builtins, "open",
+                        lambda p, *a, **k: Meminfo() if p == "/proc/meminfo" else real_open(p, *a, **k))
+    c, note = bench.fit_reference_to_memory(w)
+    assert c.interior[1:] == w.interior[1:] and 8 <= c.interior[0] < w.interior[0]
+    assert c.m_interior.size == int(np.prod(c.interior)) and "cropped" in note
+    full = np.asarray(w.m_interior).reshape(w.interior)
+    assert np.array_equal(c.m_interior.reshape(c.interior), full[:c.interior[0]])
+    assert 14 * 8 * np.prod(c.padded) <= 0.6 * 600000 * 1024
+    assert w.interior[0] == 64  # the caller's workload is not modified
