@@ -9,7 +9,12 @@ The gradient gets 5e-5 here: it sums u[t] times the second time difference of
 the adjoint field, which is smaller than the field by (omega dt)^2 (~6e-3 for
 these pulses), so the fp32 rounding of the stored v rows reaches the gradient
 amplified by ~1/(omega dt)^2; on the BASELINE configurations' full runs it
-stays at 1e-6 .. 2e-6 (tests/test_gpu_protocol.py gates them at 1e-5)."""
+stays at 1e-6 .. 2e-6 (tests/test_gpu_protocol.py gates them at 1e-5).  A
+600-case run of this file (profiles/r02q/fuzz600.txt) passes every wavefield,
+record and adjoint gate; two 2-D so-2 gradients land at 5.1e-5 and 8.8e-5 with
+their forward / adjoint fields at 1e-7 / 4e-7 (that floor, tools/fuzz_case.py)."""
+import os
+
 import numpy as np
 import pytest
 
@@ -60,7 +65,8 @@ def _close(a, b, tol=TOL):
     return O.rel_l2(a, b) <= tol
 
 
-@pytest.mark.parametrize("seed", range(48))
+# SFDB200_FUZZ_CASES widens the campaign (profiles/ keeps the log of a 600-case run)
+@pytest.mark.parametrize("seed", range(int(os.environ.get("SFDB200_FUZZ_CASES", "48"))))
 def test_random_operator_case(seed):
     model, src, rec, wav, nt, dt = _case(seed)
     P, so, h = model.padded, model.space_order, model.h
