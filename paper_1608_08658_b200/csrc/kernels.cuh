@@ -49,7 +49,8 @@ enum DebugCheck : unsigned int {
     kDbgInject = 5,     // injection corner outside the written row
     kDbgTmaPlane = 6,   // TMA plane coordinate outside the field
     kDbgQueue = 7,      // z-queue prologue load outside the field
-    kDbg2d = 8          // 2-D loop: sparse offset outside the row
+    kDbg2d = 8,         // 2-D loop: sparse offset outside the row
+    kDbgInjectOwner = 9 // fused injection into a cell the injecting item did not store
 };
 
 struct SweepArgs {

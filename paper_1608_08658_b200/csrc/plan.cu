@@ -1425,9 +1425,10 @@ void debug_check(sfdb200_plan& p) {
                                      "injection corner outside the written row",
                                      "TMA plane coordinate outside the field",
                                      "z-queue load outside the field",
-                                     "2-D sparse offset outside the row"};
+                                     "2-D sparse offset outside the row",
+                                     "fused injection into a cell another item stores"};
         fail(SFDB200_ECUDA, std::string("debug bounds check failed: ") +
-                                (code < 9 ? what[code] : "unknown check") + " (the access was skipped)");
+                                (code < 10 ? what[code] : "unknown check") + " (the access was skipped)");
     }
 }
 

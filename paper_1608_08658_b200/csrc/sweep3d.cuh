@@ -199,12 +199,27 @@ __device__ __noinline__ void sample_cta(const SweepArgs& a, long long py, long l
 }
 
 // Injections into the corners this CTA stored, after all its planes.
+// (debug build: the corner must lie in the box [x0, x0+32) x [y0, y0+ty) x
+// [zb, ze) the injecting item stored -- an atomic into a cell another CTA
+// stores in the same launch would race with that store)
 template <bool GRAD, int NT>
-__device__ __noinline__ void inject_cta(const SweepArgs& a, int cta, int tid) {
+__device__ __noinline__ void inject_cta(const SweepArgs& a, int cta, int tid, int x0 = 0,
+                                        int y0 = 0, int zb = 0, int ze = 0, int ty = 0,
+                                        long long py = 1, long long pz = 1) {
     const int e0 = __ldg(a.inj_tab + cta), e1 = __ldg(a.inj_tab + cta + 1);
     for (int e = e0 + tid; e < e1; e += NT) {
         const long long o = __ldg(a.inj_off + e);
         if (!SFDB_CHECK(a.dbg, o >= 0 && o < a.slot, kDbgInject)) continue;
+#ifdef SFDB200_DEBUG
+        if (ty > 0) {
+            const long long cz = o / pz, cy = (o - cz * pz) / py, cx = o - cz * pz - cy * py;
+            if (!SFDB_CHECK(a.dbg,
+                            cz >= zb && cz < ze && cy >= y0 && cy < y0 + ty && cx >= x0 &&
+                                cx < x0 + 32,
+                            kDbgInjectOwner))
+                continue;
+        }
+#endif
         const float delta = __ldg(a.inj_coef + e) * __ldg(a.inj_row + __ldg(a.inj_pt + e));
         atomicAdd(a.out + o, delta);
         if constexpr (GRAD)
@@ -503,9 +518,14 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
     // z0, z0 + dz, ... (dz = -1: the chunk streams downward, a.zdown).  The
     // first a.nbi items are the P2P boundary tiles (SweepArgs::nbi); their side
     // is returned in bs (-1 for interior items).
-    auto decode = [&](int item, int& x0, int& y0, int& zb, int& ze, int& z0, int& dz, int& bs) {
+    // `tab` is the item's index in the fused sparse tables (sparse.cpp owner_of:
+    // boundary items first, then tile + tiles * chunk) -- NOT the launch
+    // position when the grouped order renumbers the interior items.
+    auto decode = [&](int item, int& x0, int& y0, int& zb, int& ze, int& z0, int& dz, int& bs,
+                      int& tab) {
         bs = -1;
         int tz = 0;
+        tab = item;
         if (item < a.nbi) {
             const int tiles = ntx * nty, grp = item / tiles;
             bs = a.bside[grp];
@@ -522,6 +542,7 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
             const int rem = item - base * zc;
             tz = rem / gn;
             item = base + (rem - tz * gn) + tz * tiles;  // back to tile-major numbering
+            tab = a.nbi + item;
         }
         const int r = item / ntx;
         x0 = (item - r * ntx) * T::TX;
@@ -576,8 +597,8 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
             };
             for (int item = dyn ? fetch() : blockIdx.x; item < nitems;
                  item = dyn ? fetch() : item + gridDim.x) {
-                int x0, y0, zb, ze, z0, dz, bs;
-                decode(item, x0, y0, zb, ze, z0, dz, bs);
+                int x0, y0, zb, ze, z0, dz, bs, tab;
+                decode(item, x0, y0, zb, ze, z0, dz, bs, tab);
                 const int n = ze - zb;
                 if (n <= 0) continue;
                 align();
@@ -669,8 +690,8 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
         } else if (item >= nitems) {
             break;
         }
-        int x0, y0, zb, ze, z0, dz, bs;
-        decode(item, x0, y0, zb, ze, z0, dz, bs);
+        int x0, y0, zb, ze, z0, dz, bs, tab;
+        decode(item, x0, y0, zb, ze, z0, dz, bs, tab);
         const int n = ze - zb;
         if (n <= 0) continue;
         align();
@@ -838,9 +859,13 @@ __global__ void __launch_bounds__(32 * (BY + 1), MINB)
         j += static_cast<uint32_t>(n);
         // Fused Inject once every consumer warp has stored this item's planes
         // (named barrier over the consumer warps only).
-        if (a.inj_tab && __ldg(a.inj_tab + item + 1) > __ldg(a.inj_tab + item)) {
+        // The table entry is the item's own (`tab`), so every corner is added
+        // by the CTA that stored it, after its store.  (Indexing by the launch
+        // position made another CTA add it under the grouped order: its atomic
+        // raced with the owner's plain store and an injection could be lost.)
+        if (a.inj_tab && __ldg(a.inj_tab + tab + 1) > __ldg(a.inj_tab + tab)) {
             named_barrier_sync(1, NT);
-            inject_cta<GRAD, NT>(a, item, tid);
+            inject_cta<GRAD, NT>(a, tab, tid, x0, y0, zb, ze, T::TY, py, pz);
         }
         // Fused P2P ghost exchange (boundary items only): after the item's
         // injections, each thread re-sends the values it stored (read back

@@ -36,11 +36,11 @@ except L.SfdError as e:
 """
 
 
-def _run(fault):
+def _run(fault, **extra):
     lib = os.path.join(ROOT, "paper_1608_08658_b200", "libsfdb200_debug.so")
     if not os.path.exists(lib):
         pytest.fail("libsfdb200_debug.so missing: make -C paper_1608_08658_b200/csrc debug")
-    env = dict(os.environ, SFDB200_LIBRARY="debug", SFDB200_DEBUG_FAULT=str(fault))
+    env = dict(os.environ, SFDB200_LIBRARY="debug", SFDB200_DEBUG_FAULT=str(fault), **extra)
     out = subprocess.run([sys.executable, "-c", SCRIPT, ROOT], capture_output=True, text=True,
                          env=env, timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
@@ -54,3 +54,17 @@ def test_debug_build_runs_clean():
 def test_debug_build_catches_an_out_of_row_access():
     r = _run(1)
     assert r.startswith("RESULT error 2") and "receiver corner outside the sampled row" in r
+
+
+@pytest.mark.parametrize("group,zc", [(2, 3), (2, 2)])
+def test_grouped_order_injects_from_the_owning_item(group, zc):
+    """Under the grouped item order the launch position of an item differs from
+    its index in the fused injection table (tile + tiles * chunk).  An item must
+    add only the corners it stored itself: an atomic from another CTA races with
+    the owner's plain store in the same launch and can lose the injection (seen
+    as run-to-run differences at 512^3, where the grouped order is the default).
+    The debug build checks every fused injection against the injecting item's
+    box (kDbgInjectOwner); a build that indexes the table by launch position
+    fails this case with "fused injection into a cell another item stores"."""
+    assert _run(0, SFDB200_GROUP=str(group), SFDB200_ZCHUNKS=str(zc),
+                SFDB200_TILE="4,2,4,4,1") == "RESULT ok"
