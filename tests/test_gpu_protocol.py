@@ -385,3 +385,94 @@ def test_protocol_cfg5_full_size_properties():
     assert same
     assert np.all(np.isfinite(all_a)) and np.linalg.norm(all_a[:, -8192:]) > 0
     assert e_lin <= TOL and e_lin_vol <= TOL
+
+
+@_full
+def test_protocol_grouped_order_slab_ranks(monkeypatch):
+    """The grouped item order (more tiles than resident slots) together with the
+    fused P2P boundary items: a cfg5-shaped slab problem (64 x 768 x 768 + 40,
+    so 16, 4 sources at mid depth, 160 steps, receivers through the volume)
+    against the reference on one GPU, then z-slab-decomposed over 2 and 4
+    emulated ranks, bitwise equal to the one-GPU run."""
+    monkeypatch.setenv("SFDB200_TILE", "4,2,4,2,1")
+    n, so, nbpml, h, nt = (64, 768, 768), 16, 40, 10.0, 162
+    v = configs.smooth_random_velocity(n, 1, 16.0)
+    m = configs._round32(1.0 / v ** 2).ravel()
+    dt = configs._crit(m.min(), 3, so, h)
+    sp = [(k - 1) * h for k in n]
+    srcs = np.array([[0.5 * sp[0] + 3.0, a, b] for a in (0.25 * sp[1] + 1.0, 0.75 * sp[1] - 2.0)
+                     for b in (0.25 * sp[2] + 4.0, 0.75 * sp[2] - 3.0)])
+    rng = np.random.default_rng(11)
+    recs = np.concatenate([rng.random((4096, 3)) * np.array(sp),
+                           srcs + rng.uniform(-150.0, 150.0, (4, 3)).clip(-0.4 * sp[0], 0.4 * sp[0])])
+    w = configs.Workload("cfg5-slab-64x768x768", 3, list(n), so, nt, dt, m,
+                         configs._ricker(10.0, nt, dt, 4), srcs, recs, h, nbpml, 10.0)
+    f, model, src, rec = _forward_case("grouped order: 64x768x768+40 so16 160 steps 4 src", w)
+    tiles = -(-model.padded[2] // 32) * -(-(model.padded[1] - so) // 16)
+    assert tiles > 3 * 148, tiles  # more tiles than resident slots: the grouped order is on
+    assert np.abs(f.record.data).max() > 0
+    diffs = {}
+    for world in (2, 4):
+        u, tr = _emulated_forward(w, model, src, rec, world)
+        diffs[world] = (float(np.abs(u - f.u).max()), float(np.abs(tr - f.record.data).max()))
+    _log("grouped order + boundary items: 64x768x768 so16 z slabs vs 1 GPU (emulated ranks)",
+         max_abs_diff=diffs, tiles=int(tiles))
+    for world, (du, dt_) in diffs.items():
+        assert du == 0.0 and dt_ == 0.0, (world, du, dt_)
+
+
+@_full
+def test_protocol_adjoint_and_gradient_chain_512():
+    """The adjoint at 512^3 + 40 (so 8, 100 steps: grouped order, thousands of
+    fused injection corners from a receiver carpet, fused sampling at the
+    sources) against the reference, and the device gradient chain at the same
+    size (60 steps, 54 GB history in HBM): checkpointed = full history, and the
+    directional derivative of the objective."""
+    import dataclasses
+    w = configs.cfg4(8, nt=102)
+    model = S.make_model(w.interior, w.h, w.nbpml, w.space_order, w.m_interior)
+    sp = (w.interior[0] - 1) * w.h
+    rng = np.random.default_rng(7)
+    rec_c = np.concatenate([configs._carpet(64, sp, 20.0), rng.random((2048, 3)) * sp])
+    src_c = 0.3 * sp + rng.random((3, 3)) * 0.4 * sp
+    rec = S.locate_points(model, rec_c)
+    src = S.locate_points(model, src_c)
+    white = rng.standard_normal((w.nt, rec.npoints))
+    pulse = S.ricker(15.0, 1.2 / 15.0, w.nt, w.dt)
+    sm = np.stack([np.convolve(white[:, r], pulse)[:w.nt] for r in range(rec.npoints)], 1)
+    resid = O._f64((sm / np.abs(sm).max()).astype(np.float32))
+    a = S.adjoint(model, rec, S.ShotRecord(w.nt, w.dt, rec.npoints, resid), src, w.nt, w.dt)
+    vo, so_, t_ref = O.ref_adjoint(w.interior, w.h, w.nbpml, w.space_order, w.m_interior, rec_c,
+                                   resid, src_c, w.nt, w.dt)
+    e_adj = [O.rel_l2(np.asarray(a.v)[t % 3], vo[t % 3]) for t in (4, 3, 2)]
+    e_src = O.rel_l2(a.src_samples.data, so_)
+    del a, vo
+    # gradient chain, 60 steps
+    nt = 62
+    wav = np.ascontiguousarray(np.asarray(w.wavelet)[:nt].reshape(nt, -1)[:, :1])
+    one = S.locate_points(model, np.array([[0.5 * sp, 0.5 * sp, 0.5 * sp]]))
+    near = S.locate_points(model, 0.5 * sp + rng.uniform(-120.0, 120.0, (512, 3)))
+    i = np.indices(w.interior)
+    bump = np.exp(-sum((i[d] - 0.5 * w.interior[d] - 4.0) ** 2 for d in range(3)) / (2 * 6.0 ** 2))
+    mt = np.asarray(w.m_interior).reshape(w.interior) * (1.0 + 0.05 * bump)
+    true = S.make_model(w.interior, w.h, w.nbpml, w.space_order, configs._round32(mt).ravel())
+    obs = S.forward(true, one, wav, near, nt, w.dt, False).record
+    chain = S.fwi_gradient(model, one, wav, near, obs, nt, w.dt, checkpoint_interval=0)
+    ck = S.fwi_gradient(model, one, wav, near, obs, nt, w.dt, checkpoint_interval=10)
+    e_ck = O.rel_l2(ck.grad, chain.grad)
+    dm = np.zeros(model.cells())
+    S.add_interior(model, (np.asarray(w.m_interior).max() * 0.01 * bump).ravel(), 1.0, dm)
+    gdot = float(np.dot(np.asarray(chain.grad).ravel(), dm))
+    phis = []
+    for sgn in (1.0, -1.0):
+        mp = dataclasses.replace(model, m=np.asarray(model.m) + sgn * dm)
+        phis.append(S.objective(S.forward(mp, one, wav, near, nt, w.dt, False).record, obs))
+    fd = (phis[0] - phis[1]) / 2.0
+    _log("adjoint 512^3+40 so8 100 steps vs reference; gradient chain 60 steps",
+         padded=list(map(int, model.padded)), nrec=rec.npoints, adjoint_slot_rel_l2=e_adj,
+         adjoint_source_samples_rel_l2=e_src, checker_s=t_ref, checkpointed_vs_full_rel_l2=e_ck,
+         grad_dot_dm=gdot, central_difference=fd, directional_rel_err=abs(fd - gdot) / abs(fd),
+         phi=chain.phi)
+    assert max(e_adj) <= TOL and e_src <= TOL
+    assert e_ck <= 2e-5
+    assert abs(fd - gdot) <= 0.03 * abs(fd)
