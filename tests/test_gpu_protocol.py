@@ -253,7 +253,7 @@ def test_protocol_cfg2_full_size():
 
 
 @_full
-@pytest.mark.parametrize("so", [2, 4, 8, 12, 16])
+@pytest.mark.parametrize("so", [2, 4, 6, 8, 10, 12, 14, 16])
 def test_protocol_cfg4_full_size(so):
     _forward_case(f"cfg4 FULL 512^3+40 so{so} 200 steps", configs.cfg4(so))
 
