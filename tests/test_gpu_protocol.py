@@ -247,9 +247,42 @@ _full = pytest.mark.skipif(os.environ.get("SFDB200_FULL_PARITY") != "1" or not O
                            reason="opt-in: SFDB200_FULL_PARITY=1 and the built reference")
 
 
-@_full
+@pytest.mark.skipif(not O.have_ref(), reason="needs the built reference (oracle/_ref)")
 def test_protocol_cfg2_full_size():
+    """BASELINE configs[1] exactly as benched (344^3 padded, 1000 steps, 65,536
+    receivers) against the unmodified reference: ~40 s of its CPU path, so this
+    one full-size case runs with the default suite."""
     _forward_case("cfg2 FULL 256^3+40 so8 1000 steps 256^2 carpet", configs.cfg2())
+
+
+@pytest.mark.parametrize("so,tile", [(4, "4,2,4,4,1"), (16, "4,2,4,2,1")])
+def test_protocol_grouped_order_wide_grid(monkeypatch, so, tile):
+    """A wide, thin grid (24 x 704 x 704 + 40) has more (x, y) tiles than the
+    GPU has resident CTA slots, so the grouped item order of the 512^3-and-up
+    workloads is active at a size the checker finishes in seconds: three
+    sources at mid depth, 2,000 receivers through the volume, three z chunks.
+    Against the checker, and three identical runs bit-identical (an injection
+    added by a CTA that does not own the cell races with the owner's store)."""
+    monkeypatch.setenv("SFDB200_TILE", tile)
+    monkeypatch.setenv("SFDB200_ZCHUNKS", "3")
+    n, nbpml, h, nt = (24, 704, 704), 40, 10.0, 82
+    rng = np.random.default_rng(so)
+    v = 1500.0 + 2500.0 * rng.random(n)
+    for ax in range(3):
+        v = 0.5 * v + 0.25 * (np.roll(v, 1, ax) + np.roll(v, -1, ax))
+    m = configs._round32(1.0 / v ** 2).ravel()
+    dt = 0.8 * configs._crit(m.min(), 3, so, h)
+    sp = np.array([(k - 1) * h for k in n])
+    srcs = np.array([0.5, 0.31, 0.72]) * sp + rng.uniform(-40.0, 40.0, (3, 3))
+    recs = rng.random((2000, 3)) * sp
+    w = configs.Workload(f"wide-24x704x704-so{so}", 3, list(n), so, nt, dt, m,
+                         configs._ricker(12.0, nt, dt, 3), srcs, recs, h, nbpml, 12.0)
+    f, model, src, rec = _forward_case(f"grouped order: 24x704x704+40 so{so} 80 steps 3 src", w)
+    tiles = -(-model.padded[2] // 32) * -(-(model.padded[1] - so) // 16)
+    assert tiles > 5 * 148, tiles
+    for _ in range(2):
+        g = S.forward(model, src, w.wavelet, rec, w.nt, w.dt, False)
+        assert np.array_equal(g.u, f.u) and np.array_equal(g.record.data, f.record.data)
 
 
 @_full
