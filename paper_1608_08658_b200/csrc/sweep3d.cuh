@@ -454,7 +454,7 @@ __global__ void __launch_bounds__(32 * (BY + 1), 4)
     // barrier over the consumer warps only).
     if (a.inj_tab) {
         named_barrier_sync(1, NT);
-        inject_cta<GRAD, NT>(a, cta, tid);
+        inject_cta<GRAD, NT>(a, cta, tid, x0, y0, zb, ze, T::TY, py, pz);
     }
 }
 
