@@ -100,9 +100,11 @@ struct SweepArgs {
     int smp_n;              // entries
     float* smp_row;         // trace row being sampled
     // Inject into this step's output once the CTA has stored all its planes
-    // (codegen.cpp:436-449): entries of CTA c are [inj_tab[c], inj_tab[c+1]),
-    // the corners it stores; colliding corners are summed with atomics.
-    const int* inj_tab;
+    // (codegen.cpp:436-449): the runs of item c are [inj_tab[c], inj_tab[c+1]),
+    // one run per cell it stores; a run's entries (colliding corners) are
+    // summed in the reference's (p, c) order and added once.
+    const int* inj_tab;      // CSR over the items of runs (the entries of one cell)
+    const int* inj_run;      // run r = entries [inj_run[r], inj_run[r + 1])
     const long long* inj_off;
     const float* inj_coef;
     const int* inj_pt;

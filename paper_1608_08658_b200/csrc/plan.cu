@@ -879,6 +879,7 @@ void phase_interior(sfdb200_plan& p, long i, StepState& st) {
     }
     if (p.fused && inj.f_tab) {
         c.inj_tab = inj.f_tab;
+        c.inj_run = inj.f_run;
         c.inj_off = inj.f_off;
         c.inj_coef = inj.f_coef;
         c.inj_pt = inj.f_pt;
@@ -1228,6 +1229,7 @@ void recompute_step(sfdb200_plan& fp, const SweepMaps& maps, float* seg, long ts
     const float* row = src.n ? src.trace + (t - 1) * src.n : nullptr;  // forward: trace row t-1
     if (fp.fused && src.f_tab) {
         a.inj_tab = src.f_tab;
+        a.inj_run = src.f_run;
         a.inj_off = src.f_off;
         a.inj_coef = src.f_coef;
         a.inj_pt = src.f_pt;

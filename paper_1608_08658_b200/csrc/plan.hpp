@@ -63,7 +63,11 @@ struct SparseDev {
     // (applied by the CTA that stores the corner, after its planes), and the
     // rest (boundary / halo planes, or every entry when the sweep is not
     // fused) as a flat list.
+    // f_tab is a CSR over the launch's items of RUNS (the entries of one cell,
+    // adjacent and in the reference's (p, c) order); run r covers the entries
+    // [f_run[r], f_run[r + 1]).
     int* f_tab = nullptr;
+    int* f_run = nullptr;
     long long* f_off = nullptr;
     float* f_coef = nullptr;
     int* f_pt = nullptr;
@@ -100,7 +104,7 @@ struct SparseDev {
         for (void* q : bufs) cudaFree(q);
         bufs.clear();
         key = 0;
-        f_tab = nullptr; f_off = nullptr; f_coef = nullptr; f_pt = nullptr; f_gm = nullptr;
+        f_tab = nullptr; f_run = nullptr; f_off = nullptr; f_coef = nullptr; f_pt = nullptr; f_gm = nullptr;
         s_base = nullptr;
         inj_rest = InjectList{};
         smp_all = SampleList{};

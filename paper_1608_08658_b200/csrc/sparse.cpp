@@ -279,9 +279,13 @@ void upload_sparse(sfdb200_plan& p, SparseDev& s, const long* idx, const double*
         s.inj_rest.pt = s.upload(r_pt, st);
         s.inj_rest.gm = s.upload(r_gm, st);
         if (!fused.empty()) {
-            // CSR over the CTAs, the reference's (p, c) order within a CTA.
-            std::stable_sort(fused.begin(), fused.end(),
-                             [](const E& a, const E& b) { return a.o.cta < b.o.cta; });
+            // CSR over the CTAs; within a CTA by cell, the reference's (p, c)
+            // order among the entries of one cell (colliding corners): the
+            // kernel sums each cell's run in that order and adds it once, so
+            // the result does not depend on the order atomics land in.
+            std::stable_sort(fused.begin(), fused.end(), [&](const E& a, const E& b) {
+                return a.o.cta != b.o.cta ? a.o.cta < b.o.cta : cs[a.i].off < cs[b.i].off;
+            });
             std::vector<int> owner, ept;
             std::vector<long long> eoff;
             std::vector<float> ecoef;
@@ -294,8 +298,20 @@ void upload_sparse(sfdb200_plan& p, SparseDev& s, const long* idx, const double*
                 ept.push_back(static_cast<int>(e.i / C));
                 egm.push_back(1);
             }
+            // Runs: maximal groups of adjacent entries with the same item and
+            // cell.  The kernel walks an item's runs, one thread per run.
+            std::vector<int> run, run_owner;
+            for (size_t i = 0; i < eoff.size();) {
+                size_t j = i + 1;
+                while (j < eoff.size() && owner[j] == owner[i] && eoff[j] == eoff[i]) ++j;
+                run.push_back(static_cast<int>(i));
+                run_owner.push_back(owner[i]);
+                i = j;
+            }
+            run.push_back(static_cast<int>(eoff.size()));
             int most = 0;
-            s.f_tab = s.upload(csr_begin(owner, ctas_of(p), &most), st);
+            s.f_tab = s.upload(csr_begin(run_owner, ctas_of(p), &most), st);
+            s.f_run = s.upload(run, st);
             s.f_off = s.upload(eoff, st);
             s.f_coef = s.upload(ecoef, st);
             s.f_pt = s.upload(ept, st);

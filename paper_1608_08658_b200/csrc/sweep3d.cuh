@@ -206,8 +206,13 @@ template <bool GRAD, int NT>
 __device__ __noinline__ void inject_cta(const SweepArgs& a, int cta, int tid, int x0 = 0,
                                         int y0 = 0, int zb = 0, int ze = 0, int ty = 0,
                                         long long py = 1, long long pz = 1) {
-    const int e0 = __ldg(a.inj_tab + cta), e1 = __ldg(a.inj_tab + cta + 1);
-    for (int e = e0 + tid; e < e1; e += NT) {
+    const int r0 = __ldg(a.inj_tab + cta), r1 = __ldg(a.inj_tab + cta + 1);
+    // One thread per run: the entries of one cell, adjacent and in the
+    // reference's (p, c) order (sparse.cpp).  The run is summed in that order
+    // and added once, so colliding corners (a receiver carpet at the grid
+    // spacing) give the same bits on every run.
+    for (int r = r0 + tid; r < r1; r += NT) {
+        const int e = __ldg(a.inj_run + r), e1 = __ldg(a.inj_run + r + 1);
         const long long o = __ldg(a.inj_off + e);
         if (!SFDB_CHECK(a.dbg, o >= 0 && o < a.slot, kDbgInject)) continue;
 #ifdef SFDB200_DEBUG
@@ -220,7 +225,9 @@ __device__ __noinline__ void inject_cta(const SweepArgs& a, int cta, int tid, in
                 continue;
         }
 #endif
-        const float delta = __ldg(a.inj_coef + e) * __ldg(a.inj_row + __ldg(a.inj_pt + e));
+        float delta = __ldg(a.inj_coef + e) * __ldg(a.inj_row + __ldg(a.inj_pt + e));
+        for (int f = e + 1; f < e1; ++f)
+            delta += __ldg(a.inj_coef + f) * __ldg(a.inj_row + __ldg(a.inj_pt + f));
         atomicAdd(a.out + o, delta);
         if constexpr (GRAD)
             if (a.inj_gm[e]) atomicAdd(a.grad + o, a.nidt2 * __ldg(a.ut + o) * delta);

@@ -122,3 +122,43 @@ def test_gradient_plan_reused_across_shots(monkeypatch):
     go, _ = O.gradient(model.padded, w.space_order, w.h, w.dt, w.nt, model.m, model.damp, us,
                        rec.idx, rec.w, resid)
     assert O.rel_l2(want[2], go) <= 5e-5
+
+
+def test_colliding_injection_corners_are_deterministic(monkeypatch):
+    """A receiver carpet at the grid spacing shares corners between neighbours
+    (cfg3's 200 x 200 carpet): the fused injection sums each cell's entries in
+    the reference's (p, c) order and adds the sum once, so the adjoint and the
+    gradient are bit-identical from run to run and across z-chunk counts
+    (which change the CTA that owns a cell, not the order within the cell)."""
+    monkeypatch.setenv("SFDB200_TILE", "4,1,4,0,1")
+    rng = np.random.default_rng(9)
+    w = configs.cfg2(n=30, nt=62, nbpml=8, nrec_side=4)
+    model = S.make_model(w.interior, w.h, w.nbpml, w.space_order, w.m_interior)
+    span = (w.interior[0] - 1) * w.h
+    c = 3.3 + np.arange(24) * w.h                      # 24 x 24 carpet, spacing = h
+    yy, xx = np.meshgrid(c, c, indexing="ij")
+    rec = S.locate_points(model, np.stack([np.full(yy.size, 27.1), yy.ravel(), xx.ravel()], 1))
+    src = S.locate_points(model, np.array([[0.5 * span, 0.45 * span, 0.55 * span]]))
+    cells = [tuple(i + np.array([(k >> 2) & 1, (k >> 1) & 1, k & 1])) for i in rec.idx for k in range(8)]
+    assert len(set(cells)) < len(cells) // 3          # most corners are shared
+    wav = O._f64(np.asarray(w.wavelet).reshape(w.nt, -1)[:, :1])
+    us, rs = O.forward(model.padded, w.space_order, w.h, w.dt, w.nt, model.m, model.damp, src.idx,
+                       src.w, wav, rec.idx, rec.w, save=True)
+    resid = O._f64(rng.standard_normal(rs.shape).astype(np.float32))
+    rsr = S.ShotRecord(w.nt, w.dt, rec.npoints, resid)
+    outs = []
+    for zc in ("2", "2", "3", "2"):
+        monkeypatch.setenv("SFDB200_ZCHUNKS", zc)
+        a = S.adjoint(model, rec, rsr, src, w.nt, w.dt)
+        g = S.gradient(model, rec, rsr, us, w.nt, w.dt)
+        outs.append((np.asarray(a.v).copy(), np.asarray(a.src_samples.data).copy(),
+                     np.asarray(g.grad).copy()))
+    for o in outs[1:]:
+        for x, y in zip(o, outs[0]):
+            assert np.array_equal(x, y)
+    vo, so_ = O.adjoint(model.padded, w.space_order, w.h, w.dt, w.nt, model.m, model.damp, src.idx,
+                        src.w, rec.idx, rec.w, resid)
+    go, _ = O.gradient(model.padded, w.space_order, w.h, w.dt, w.nt, model.m, model.damp, us,
+                       rec.idx, rec.w, resid)
+    assert O.rel_l2(outs[0][0], vo) <= TOL and O.rel_l2(outs[0][1], so_) <= TOL
+    assert O.rel_l2(outs[0][2], go) <= 5e-5
